@@ -1,0 +1,165 @@
+/*
+ * monoalign_b200.h -- the C-ABI drop-in boundary of the B200-native
+ * maximum-path (Monotonic Alignment Search) call.
+ *
+ * Plain pointers and sizes only; no torch / CUDA-runtime types in the
+ * signatures (streams are passed as `void*` = cudaStream_t).  Implemented in
+ * paper_2409_07704_b200/csrc/ and built into
+ * paper_2409_07704_b200/_lib/libmonoalign_b200.so.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj):
+ *
+ *   mas_align_host    monoalign::align(const LikelihoodBatch&, const MasConfig&)
+ *                       include/monoalign/align.hpp:9-12, i.e. what the pybind
+ *                       binding's align_arrays / align_paths call
+ *                       (bindings/module.cpp:120-154) after copying numpy data
+ *                       into a LikelihoodBatch (module.cpp:88-99).
+ *   mas_align_device  same call on caller-owned device buffers (no host copy;
+ *                       the reference has no equivalent -- SURVEY.md 8(b)).
+ *   MAS_FLAG_UNCHECKED  parallel::detail::align_unchecked / reference::detail::
+ *                       align_unchecked (parallel.hpp:29-31, reference.hpp:42-44):
+ *                       skips validate_config so -inf / -1e9 sentinels run.
+ *   mas_plan_*        the same call split into enqueue-only + check, so the
+ *                       kernels can be captured in a CUDA graph / timed alone.
+ *   mas_generate_device  bench::generate_random_batch (bench.hpp:58,
+ *                       bench.cpp:164-180), bit-identical, for any item shard.
+ *   mas_errc_name     errc_name (types.cpp:8-29).
+ *
+ * Error convention: every entry returns a mas_status; on MAS_E_VALIDATION
+ * `err->errc` holds the reference Errc (errors.hpp:8-30 order) and
+ * `err->message` the exact text the reference's ValidationError carries
+ * (types.cpp:59-130), so a binding can raise ValueError with identical text
+ * (module.cpp:210-220).  MAS_E_CUDA means the device path failed (no CPU
+ * fallback exists).
+ */
+#ifndef MONOALIGN_B200_H
+#define MONOALIGN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MAS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define MAS_API __attribute__((visibility("default")))
+#else
+#define MAS_API
+#endif
+
+/* include/monoalign/errors.hpp:8-30, declaration order. */
+enum mas_errc {
+  MAS_ERRC_ZERO_DIM = 0,
+  MAS_ERRC_INFEASIBLE_LENGTHS = 1,
+  MAS_ERRC_LENGTHS_OUT_OF_RANGE = 2,
+  MAS_ERRC_NON_FINITE = 3,
+  MAS_ERRC_SPEECH_TOO_LONG = 4,
+  MAS_ERRC_SHAPE_MISMATCH = 5,
+  MAS_ERRC_INVALID_PATH = 6,
+  MAS_ERRC_INVALID_MATRIX = 7,
+  MAS_ERRC_INVALID_CONFIG = 8,
+  MAS_ERRC_TOO_LARGE = 9,
+  MAS_ERRC_EMPTY_REPORT = 10,
+  MAS_ERRC_INSUFFICIENT_POINTS = 11,
+  MAS_ERRC_IO_FAILURE = 12,
+  MAS_ERRC_BAD_MAGIC = 13,
+  MAS_ERRC_UNSUPPORTED_VERSION = 14,
+  MAS_ERRC_TRUNCATED_FILE = 15,
+  MAS_ERRC_DIMENSION_OVERFLOW = 16
+};
+
+enum mas_status {
+  MAS_OK = 0,
+  MAS_E_VALIDATION = 1, /* reference ValidationError -> ValueError / exit 2 */
+  MAS_E_IO = 2,         /* reference IoError -> OSError / exit 1 */
+  MAS_E_CUDA = 3,       /* CUDA runtime / launch failure */
+  MAS_E_UNSUPPORTED = 4 /* shape outside what the device path supports */
+};
+
+/* EngineKind, types.hpp:28 (declaration order). */
+enum mas_engine { MAS_ENGINE_REFERENCE = 0, MAS_ENGINE_PARALLEL = 1 };
+
+#define MAS_FLAG_UNCHECKED 0x1u /* skip validate_config (detail::align_unchecked) */
+
+typedef struct mas_error {
+  int32_t status;     /* enum mas_status */
+  int32_t errc;       /* enum mas_errc when status == MAS_E_VALIDATION, else -1 */
+  int32_t item;       /* failing item index, -1 if not item-specific */
+  int32_t reserved;
+  int64_t i, j;       /* NonFinite location (row, column), else -1 */
+  char message[512];  /* exact reference what() text */
+} mas_error_t;
+
+/* MasConfig, types.hpp:32-39. */
+typedef struct mas_config {
+  int32_t engine;       /* enum mas_engine, default MAS_ENGINE_PARALLEL */
+  float max_neg_val;    /* default -1e32f (kDefaultMaxNegVal, types.hpp:19) */
+  int32_t lane_padding; /* LanePadding; accepted and unobservable (parallel.hpp:12-15) */
+  int32_t threads;      /* validated >= 0 (types.cpp:66-68), otherwise ignored */
+  uint32_t flags;       /* MAS_FLAG_* */
+} mas_config_t;
+
+/* Fills the MasConfig defaults. */
+MAS_API void mas_config_default(mas_config_t* cfg);
+
+/*
+ * Host buffers in, host buffers out (pageable or pinned).
+ *   values   [batch][text_cap][speech_cap] float32 row-major (LikelihoodBatch::values)
+ *   lengths  [batch][2] uint32 (text, speech) (LikelihoodBatch::lengths) or NULL = full
+ *   out      [batch][text_cap][speech_cap] uint8 (AlignmentMatrix::values) or NULL
+ *   paths    [batch][speech_cap] int32, -1 past each item's speech length, or NULL
+ * Uses the calling thread's current CUDA device.  Synchronous.
+ */
+MAS_API int mas_align_host(const float* values, int32_t batch, int32_t text_cap, int32_t speech_cap,
+                   const uint32_t* lengths, const mas_config_t* cfg, uint8_t* out,
+                   int32_t* paths, mas_error_t* err);
+
+/*
+ * Device buffers (caller-owned, current device).  `row_pitch` = elements
+ * between consecutive text rows (>= speech_cap); items are text_cap rows
+ * apart.  `lengths` is a HOST array as above.  Enqueues on `stream` and
+ * synchronises it before returning (the NonFinite check needs the result).
+ */
+MAS_API int mas_align_device(const float* d_values, int64_t row_pitch, int32_t batch, int32_t text_cap,
+                     int32_t speech_cap, const uint32_t* lengths, const mas_config_t* cfg,
+                     uint8_t* d_out, int32_t* d_paths, void* stream, mas_error_t* err);
+
+/* ---- plan API: validation + workspace once, enqueue-only execution ------ */
+typedef struct mas_plan mas_plan_t;
+
+/* Validates config and lengths (host side) and allocates the workspace.
+ * Host-detectable item errors are recorded and reported by mas_plan_finish
+ * (lowest failing item wins, parallel.cpp:160-165). */
+MAS_API int mas_plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row_pitch,
+                    const uint32_t* lengths, const mas_config_t* cfg, mas_plan_t** plan,
+                    mas_error_t* err);
+/* Enqueues the kernels on `stream`; no host synchronisation. */
+MAS_API int mas_plan_enqueue(mas_plan_t* plan, const float* d_values, uint8_t* d_out, int32_t* d_paths,
+                     void* stream, mas_error_t* err);
+/* Synchronises `stream` and turns device-side NonFinite flags and recorded
+ * host-side item errors into the reference's error (or MAS_OK). */
+MAS_API int mas_plan_finish(mas_plan_t* plan, const float* d_values, void* stream, mas_error_t* err);
+/* Number of kernel launches one mas_plan_enqueue issues. */
+MAS_API int mas_plan_launches(const mas_plan_t* plan);
+/* Launch geometry chosen by the plan: {rows_per_warp, warps_per_cta,
+ * ctas_per_item (cluster size), stages, segment_columns}. */
+MAS_API void mas_plan_geometry(const mas_plan_t* plan, int32_t geom[5]);
+MAS_API void mas_plan_destroy(mas_plan_t* plan);
+
+/* bench::generate_random_batch(batch, text_cap, speech_cap, seed), items
+ * [first_item, first_item + batch) of that stream, written pitched into
+ * d_out[(b * text_cap + i) * row_pitch + j].  Bit-identical to the CPU. */
+MAS_API int mas_generate_device(uint64_t seed, int32_t batch, int32_t text_cap, int32_t speech_cap,
+                        int64_t first_item, int64_t row_pitch, float* d_out, void* stream);
+
+MAS_API const char* mas_errc_name(int32_t errc);
+MAS_API int mas_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MONOALIGN_B200_H */

@@ -1,0 +1,127 @@
+// ref_shim.cpp -- extern "C" entry points over the UNMODIFIED reference
+// library (/root/reference/proj/src/*.cpp compiled in place by
+// oracle/Makefile into oracle/_ref/libmonoalign_ref.so).
+//
+// TEST INFRASTRUCTURE ONLY: used by tests/ to pin the oracle restatement and
+// the CUDA path against the reference itself, and by bench.py's
+// `--impl reference` / cpu_baseline legs to time the reference CPU engines.
+// Never loaded by the product library.
+//
+// Calls go through the reference's own public C++ API:
+//   monoalign::align                     include/monoalign/align.hpp:9-12
+//   parallel::detail::align_unchecked    include/monoalign/parallel.hpp:29-31
+//   reference::detail::align_unchecked   include/monoalign/reference.hpp:42-44
+//   path_from_matrix                     include/monoalign/types.hpp:155-158
+//   bench::generate_random_batch         include/monoalign/bench.hpp:58
+//   oracle::best_paths                   include/monoalign/oracle.hpp:33
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+
+#include "monoalign/align.hpp"
+#include "monoalign/bench.hpp"
+#include "monoalign/oracle.hpp"
+
+namespace {
+
+void put_msg(const std::string& s, char* buf, int cap) {
+  if (!buf || cap <= 0) return;
+  std::size_t n = s.size() < static_cast<std::size_t>(cap - 1) ? s.size() : cap - 1;
+  std::memcpy(buf, s.data(), n);
+  buf[n] = '\0';
+}
+
+}  // namespace
+
+extern "C" {
+
+/// Returns -1 on success, else the Errc value (errors.hpp:8-30 order) with
+/// the exception text copied to msg.  unchecked=1 routes through
+/// detail::align_unchecked (no validate_config), the only way to run -inf /
+/// -1e9 sentinels.
+int ref_align(const float* q, int B, int T, int S, const std::int64_t* lengths, int engine,
+              float max_neg_val, int threads, int unchecked, std::uint8_t* out,
+              std::int32_t* paths, char* msg, int msg_cap) {
+  try {
+    monoalign::LikelihoodBatch batch(B, T, S);
+    std::memcpy(batch.values.data(), q, batch.values.size() * sizeof(float));
+    if (lengths) {
+      for (int b = 0; b < B; ++b) {
+        batch.lengths[b] = {static_cast<std::uint32_t>(lengths[2 * b]),
+                            static_cast<std::uint32_t>(lengths[2 * b + 1])};
+      }
+    }
+    monoalign::MasConfig cfg;
+    cfg.engine = engine == 1 ? monoalign::EngineKind::Reference : monoalign::EngineKind::Parallel;
+    cfg.max_neg_val = max_neg_val;
+    cfg.threads = threads;
+    monoalign::AlignmentMatrix m;
+    if (unchecked) {
+      m = engine == 1 ? monoalign::reference::detail::align_unchecked(batch, cfg)
+                      : monoalign::parallel::detail::align_unchecked(batch, cfg);
+    } else {
+      m = monoalign::align(batch, cfg);
+    }
+    if (out) std::memcpy(out, m.values.data(), m.values.size());
+    if (paths) {
+      for (int b = 0; b < B; ++b) {
+        const monoalign::PathVector p = monoalign::path_from_matrix(m, b);
+        for (int j = 0; j < S; ++j) {
+          paths[static_cast<std::size_t>(b) * S + j] =
+              j < static_cast<int>(p.size()) ? p[static_cast<std::size_t>(j)] : -1;
+        }
+      }
+    }
+    return -1;
+  } catch (const monoalign::Error& e) {
+    put_msg(e.what(), msg, msg_cap);
+    return static_cast<int>(e.code());
+  } catch (const std::exception& e) {
+    put_msg(e.what(), msg, msg_cap);
+    return 1000;
+  }
+}
+
+/// bench::generate_random_batch(b, t, s, seed) into out[b*t*s].
+int ref_generate(int b, int t, int s, std::uint64_t seed, float* out) {
+  try {
+    const monoalign::LikelihoodBatch batch = monoalign::bench::generate_random_batch(b, t, s, seed);
+    std::memcpy(out, batch.values.data(), batch.values.size() * sizeof(float));
+    return -1;
+  } catch (const monoalign::Error& e) {
+    return static_cast<int>(e.code());
+  }
+}
+
+std::uint64_t ref_mix_seed(std::uint64_t seed, std::uint64_t index) {
+  return monoalign::bench::detail::mix_seed(seed, index);
+}
+
+std::uint64_t ref_splitmix64(std::uint64_t* state) {
+  return monoalign::bench::detail::splitmix64(*state);
+}
+
+/// Exhaustive oracle (oracle.cpp): number of optimal paths (<= cap copied
+/// into paths[cap][s]) and the fp64 maximum score.  Returns -1 or Errc.
+int ref_best_paths(const float* q, int t, int s, double* max_score, int* n_paths,
+                   std::int32_t* paths, int cap) {
+  try {
+    const monoalign::LikelihoodView view{q, t, s, s};
+    const monoalign::oracle::BestPaths best = monoalign::oracle::best_paths(view);
+    *max_score = best.max_score;
+    *n_paths = static_cast<int>(best.paths.size());
+    for (int k = 0; k < cap && k < *n_paths; ++k) {
+      std::memcpy(paths + static_cast<std::size_t>(k) * s, best.paths[k].data(),
+                  sizeof(std::int32_t) * s);
+    }
+    return -1;
+  } catch (const monoalign::Error& e) {
+    return static_cast<int>(e.code());
+  }
+}
+
+unsigned ref_hardware_threads() { return std::thread::hardware_concurrency(); }
+
+}  // extern "C"

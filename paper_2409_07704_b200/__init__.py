@@ -1,0 +1,27 @@
+"""B200-native Monotonic Alignment Search -- drop-in for the reference
+``monoalign`` maximum-path call (python/monoalign/__init__.py:3-19).
+
+    from paper_2409_07704_b200 import align, align_paths
+
+All compute runs in the in-tree sm_100a library ``_lib/libmonoalign_b200.so``
+through its C-ABI (include/monoalign_b200.h).  There is no CPU fallback.
+"""
+
+from .api import (
+    Plan,
+    __version__,
+    _align_unchecked,
+    align,
+    align_paths,
+    generate_device,
+    generate_random_batch,
+)
+
+__all__ = [
+    "__version__",
+    "align",
+    "align_paths",
+    "generate_random_batch",
+    "generate_device",
+    "Plan",
+]

@@ -1,0 +1,269 @@
+"""Python surface of the drop-in: the reference's ``monoalign`` functions.
+
+Mirrors the pybind11 binding ``_monoalign`` (bindings/module.cpp:206-247 of
+the reference) call for call -- same names, keyword arguments, defaults,
+argument conversion, check order and exception types -- but every alignment
+is computed by the sm_100a kernels behind the C-ABI
+(include/monoalign_b200.h).  Additionally accepts torch CUDA tensors, which
+stay on the device (no host copy).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+__version__ = "1.0.0"  # MONOALIGN_VERSION, tests/python/test_smoke.py:9-10
+
+_DEFAULT_MAX_NEG_VAL = float(np.float32(-1e32))  # kDefaultMaxNegVal, types.hpp:19
+
+
+def _is_torch(x) -> bool:
+    mod = type(x).__module__
+    return mod.startswith("torch")
+
+
+# ---- module.cpp:21-35 make_config ------------------------------------------
+def _make_config(engine: str, max_neg_val: float, threads: int, unchecked: bool = False):
+    cfg = _lib.MasConfig()
+    _lib.load().mas_config_default(ctypes.byref(cfg))
+    if engine == "reference":
+        cfg.engine = _lib.MAS_ENGINE_REFERENCE
+    elif engine == "parallel":
+        cfg.engine = _lib.MAS_ENGINE_PARALLEL
+    else:
+        raise ValueError("unknown engine name: " + str(engine))
+    cfg.max_neg_val = float(max_neg_val)  # double -> float, module.cpp:32
+    cfg.threads = int(threads)
+    cfg.flags = _lib.MAS_FLAG_UNCHECKED if unchecked else 0
+    return cfg
+
+
+# ---- module.cpp:44-59 check_dims -------------------------------------------
+def _check_dims(shape):
+    if len(shape) not in (2, 3):
+        raise ValueError("values must be a [T, S] or [B, T, S] array")
+    was_2d = len(shape) == 2
+    b = 1 if was_2d else int(shape[0])
+    t = int(shape[0 if was_2d else 1])
+    s = int(shape[1 if was_2d else 2])
+    if b < 1 or t < 1 or s < 1:
+        raise ValueError("every array dimension must be at least 1")
+    return was_2d, b, t, s
+
+
+# ---- module.cpp:61-84 parse_lengths ----------------------------------------
+def _parse_lengths(lengths, b, t, s):
+    if _is_torch(lengths):
+        lengths = lengths.detach().cpu().numpy()
+    arr = np.ascontiguousarray(np.asarray(lengths), dtype=np.int64)
+    flat_pair = arr.ndim == 1 and arr.shape[0] == 2 and b == 1
+    per_item = arr.ndim == 2 and arr.shape[0] == b and arr.shape[1] == 2
+    if not flat_pair and not per_item:
+        raise ValueError("lengths must have shape [B, 2] (or [2] for a single item)")
+    arr = arr.reshape(b, 2)
+    for i in range(b):
+        lt, ls = int(arr[i, 0]), int(arr[i, 1])
+        if lt < 0 or ls < 0 or lt > t or ls > s:
+            raise ValueError(f"item {i}: lengths must lie in [0, T] x [0, S]")
+    return np.ascontiguousarray(arr.astype(np.uint32))
+
+
+def _prepare(values, lengths, engine, max_neg_val, threads, unchecked):
+    """batch_from_array + make_config, in the binding's order (module.cpp:120-125)."""
+    if _is_torch(values):
+        shape = tuple(values.shape)
+    else:
+        values = np.ascontiguousarray(values, dtype=np.float32)  # forcecast, module.cpp:18
+        shape = values.shape
+    was_2d, b, t, s = _check_dims(shape)
+    lens = None if lengths is None else _parse_lengths(lengths, b, t, s)
+    cfg = _make_config(engine, max_neg_val, threads, unchecked)
+    return values, lens, cfg, was_2d, b, t, s
+
+
+def _run_host(values, lens, cfg, b, t, s, want_out, want_paths):
+    lib = _lib.load()
+    out = np.empty((b, t, s), np.uint8) if want_out else None
+    paths = np.empty((b, s), np.int32) if want_paths else None
+    err = _lib.MasError()
+    rc = lib.mas_align_host(
+        values.ctypes.data, b, t, s, None if lens is None else lens.ctypes.data,
+        ctypes.byref(cfg), None if out is None else out.ctypes.data,
+        None if paths is None else paths.ctypes.data, ctypes.byref(err))
+    _lib.raise_for(rc, err)
+    return out, paths
+
+
+def _run_device(values, lens, cfg, b, t, s, want_out, want_paths):
+    import torch
+
+    lib = _lib.load()
+    dev = values.device
+    if values.dtype != torch.float32:
+        values = values.to(torch.float32)
+    values = values.reshape(b, t, s)
+    if values.stride(2) != 1 or values.stride(0) != t * values.stride(1):
+        values = values.contiguous()
+    pitch = values.stride(1)
+    out = torch.empty((b, t, s), dtype=torch.uint8, device=dev) if want_out else None
+    paths = torch.empty((b, s), dtype=torch.int32, device=dev) if want_paths else None
+    err = _lib.MasError()
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        rc = lib.mas_align_device(
+            values.data_ptr(), pitch, b, t, s, None if lens is None else lens.ctypes.data,
+            ctypes.byref(cfg), None if out is None else out.data_ptr(),
+            None if paths is None else paths.data_ptr(), ctypes.c_void_p(stream.cuda_stream),
+            ctypes.byref(err))
+    _lib.raise_for(rc, err)
+    return out, paths
+
+
+def _align_impl(values, lengths, engine, max_neg_val, threads, unchecked, want_out, want_paths):
+    values, lens, cfg, was_2d, b, t, s = _prepare(values, lengths, engine, max_neg_val, threads,
+                                                  unchecked)
+    if _is_torch(values) and values.is_cuda:
+        out, paths = _run_device(values, lens, cfg, b, t, s, want_out, want_paths)
+    else:
+        if _is_torch(values):
+            values = np.ascontiguousarray(values.detach().numpy(), dtype=np.float32)
+        out, paths = _run_host(values, lens, cfg, b, t, s, want_out, want_paths)
+    return out, paths, was_2d, lens, b, s
+
+
+def align(values, lengths=None, engine="parallel", max_neg_val=_DEFAULT_MAX_NEG_VAL, threads=0):
+    """Align a [T, S] or [B, T, S] float32 likelihood array; returns a uint8
+    alignment array of the same shape. Optional lengths ([B, 2] of (t, s))
+    mark each item's valid region.  (module.cpp:222-228; torch CUDA tensors
+    in -> torch CUDA tensor out.)"""
+    out, _, was_2d, _, _, _ = _align_impl(values, lengths, engine, max_neg_val, threads, False,
+                                          True, False)
+    return out[0] if was_2d else out
+
+
+def align_paths(values, lengths=None, engine="parallel", max_neg_val=_DEFAULT_MAX_NEG_VAL,
+                threads=0):
+    """Like align, but returns per-frame text indices: one int32 array per
+    item (a single array for 2-D input).  Each item's array has length s_b
+    (path_from_matrix walks the item's valid lengths, types.cpp:161-179)."""
+    _, paths, was_2d, lens, b, s = _align_impl(values, lengths, engine, max_neg_val, threads,
+                                               False, False, True)
+    result = []
+    for i in range(b):
+        sb = s if lens is None else int(lens[i, 1])
+        result.append(paths[i, :sb])
+    return result[0] if was_2d else result
+
+
+def _align_unchecked(values, lengths=None, engine="parallel", max_neg_val=_DEFAULT_MAX_NEG_VAL,
+                     threads=0):
+    """parallel::detail::align_unchecked / reference::detail::align_unchecked
+    (parallel.hpp:29-31, reference.hpp:42-44): no validate_config, so -inf and
+    -1e9 sentinels run.  Not part of the reference's Python surface; needed
+    for the sentinel boundary checks."""
+    out, _, was_2d, _, _, _ = _align_impl(values, lengths, engine, max_neg_val, threads, True,
+                                          True, False)
+    return out[0] if was_2d else out
+
+
+def generate_random_batch(b, t, s, seed):
+    """Deterministic uniform [-5, 5] float32 batch of shape [B, T, S]
+    (bench::generate_random_batch, bench.cpp:164-180), generated on the GPU
+    bit-identically and returned as numpy."""
+    import torch
+
+    if b < 1 or t < 1 or s < 1:
+        raise ValueError("batch dimensions must be at least 1")
+    if t > s:
+        raise ValueError("text length t exceeds speech length s")
+    buf = generate_device(b, t, s, seed)
+    return buf.cpu().numpy()
+
+
+def generate_device(b, t, s, seed, first_item=0, device=None, out=None, row_pitch=None):
+    """Items [first_item, first_item + b) of generate_random_batch(..., seed)
+    written on the GPU into a [b, t, row_pitch] float32 tensor (a view of the
+    first s columns is what the reference generates)."""
+    import torch
+
+    lib = _lib.load()
+    dev = torch.device("cuda") if device is None else torch.device(device)
+    pitch = s if row_pitch is None else int(row_pitch)
+    if out is None:
+        out = torch.empty((b, t, pitch), dtype=torch.float32, device=dev)
+    with torch.cuda.device(out.device):
+        stream = torch.cuda.current_stream(out.device)
+        rc = lib.mas_generate_device(int(seed) & (2**64 - 1), b, t, s, int(first_item), pitch,
+                                     out.data_ptr(), ctypes.c_void_p(stream.cuda_stream))
+    if rc != _lib.MAS_OK:
+        raise RuntimeError("mas_generate_device failed")
+    return out if pitch == s else out[:, :, :s]
+
+
+class Plan:
+    """Enqueue-only execution of the maximum-path call on device buffers
+    (mas_plan_* in include/monoalign_b200.h): validation and workspace once,
+    then kernels only -- what the benchmark times and a CUDA graph captures."""
+
+    def __init__(self, b, t, s, row_pitch=None, lengths=None, engine="parallel",
+                 max_neg_val=_DEFAULT_MAX_NEG_VAL, unchecked=False):
+        lib = _lib.load()
+        self._lib = lib
+        self.b, self.t, self.s = b, t, s
+        self.row_pitch = s if row_pitch is None else int(row_pitch)
+        lens = None if lengths is None else _parse_lengths(lengths, b, t, s)
+        self._lens = lens
+        cfg = _make_config(engine, max_neg_val, 0, unchecked)
+        handle = ctypes.c_void_p()
+        err = _lib.MasError()
+        rc = lib.mas_plan_create(b, t, s, self.row_pitch,
+                                 None if lens is None else lens.ctypes.data, ctypes.byref(cfg),
+                                 ctypes.byref(handle), ctypes.byref(err))
+        _lib.raise_for(rc, err)
+        self._h = handle
+
+    def enqueue(self, values, out=None, paths=None, stream=None):
+        import torch
+
+        err = _lib.MasError()
+        st = torch.cuda.current_stream() if stream is None else stream
+        rc = self._lib.mas_plan_enqueue(
+            self._h, values.data_ptr(), None if out is None else out.data_ptr(),
+            None if paths is None else paths.data_ptr(), ctypes.c_void_p(st.cuda_stream),
+            ctypes.byref(err))
+        _lib.raise_for(rc, err)
+
+    def finish(self, values, stream=None):
+        import torch
+
+        err = _lib.MasError()
+        st = torch.cuda.current_stream() if stream is None else stream
+        rc = self._lib.mas_plan_finish(self._h, values.data_ptr(),
+                                       ctypes.c_void_p(st.cuda_stream), ctypes.byref(err))
+        _lib.raise_for(rc, err)
+
+    @property
+    def launches(self) -> int:
+        return int(self._lib.mas_plan_launches(self._h))
+
+    @property
+    def geometry(self) -> dict:
+        g = (ctypes.c_int32 * 5)()
+        self._lib.mas_plan_geometry(self._h, ctypes.byref(g))
+        return {"rows_per_warp": g[0], "warps_per_cta": g[1], "ctas_per_item": g[2],
+                "stages": g[3], "segment_cols": g[4]}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.mas_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

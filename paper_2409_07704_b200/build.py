@@ -1,0 +1,61 @@
+"""Builds the in-tree CUDA library ``_lib/libmonoalign_b200.so`` for sm_100a.
+
+One shared object holds the kernels (csrc/mas_fwd.cu, csrc/mas_bt.cu), the
+extern "C" boundary (csrc/mas_abi.cu, include/monoalign_b200.h) and the C++
+mirror of the reference API (csrc/monoalign_api.cpp, include/monoalign/).
+The CUDA runtime is linked statically so the library does not clash with
+torch's bundled libcudart.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIBDIR = os.path.join(PKG, "_lib")
+LIB = os.path.join(LIBDIR, "libmonoalign_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+HOST_CXX = "/usr/bin/g++"  # dynamic libstdc++ 
+
+SOURCES = ["mas_abi.cu", "mas_fwd.cu", "mas_bt.cu", "monoalign_api.cpp"]
+HEADERS = ["mas_kernels.h", "mas_ptx.cuh"]
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
+    inc = os.path.join(ROOT, "include")
+    for dirpath, _, files in os.walk(inc):
+        deps += [os.path.join(dirpath, f) for f in files]
+    return any(os.path.exists(d) and os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    os.makedirs(LIBDIR, exist_ok=True)
+    cmd = [
+        NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+        "-ccbin", HOST_CXX, "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared",
+        "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+        "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
+        "-o", LIB,
+    ] + [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc build of libmonoalign_b200.so failed")
+    if verbose:
+        sys.stderr.write(res.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,570 @@
+// mas_abi.cu -- the extern "C" boundary (include/monoalign_b200.h):
+// host-side validation with the reference's exact error text, workspace and
+// launch-geometry planning, TMA descriptor encoding, and the host / device
+// entry points.  There is no CPU compute path: every alignment is produced
+// by the kernels in mas_fwd.cu / mas_bt.cu.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <new>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/monoalign_b200.h"
+#include "mas_kernels.h"
+
+namespace mas {
+cudaError_t bt_configure(int T_alloc, int L);
+}
+
+namespace {
+
+// ---- reference constants (include/monoalign/types.hpp:19-26) --------------
+constexpr float kDefaultMaxNegVal = -1e32f;
+constexpr float kMaxNegValCeiling = -1e30f;
+constexpr int64_t kMaxSpeechLen = 100000;
+
+const char* const kErrcNames[] = {
+    "ZeroDim",     "InfeasibleLengths", "LengthsOutOfRange",  "NonFinite", "SpeechTooLong",
+    "ShapeMismatch", "InvalidPath",     "InvalidMatrix",      "InvalidConfig", "TooLarge",
+    "EmptyReport", "InsufficientPoints", "IoFailure",         "BadMagic",  "UnsupportedVersion",
+    "TruncatedFile", "DimensionOverflow"};
+
+void clear_error(mas_error_t* err) {
+  if (!err) return;
+  err->status = MAS_OK;
+  err->errc = -1;
+  err->item = -1;
+  err->reserved = 0;
+  err->i = err->j = -1;
+  err->message[0] = '\0';
+}
+
+int set_error(mas_error_t* err, int status, int errc, int item, const std::string& msg) {
+  if (err) {
+    err->status = status;
+    err->errc = errc;
+    err->item = item;
+    std::snprintf(err->message, sizeof(err->message), "%s", msg.c_str());
+  }
+  return status;
+}
+
+int cuda_error(mas_error_t* err, cudaError_t e, const char* what) {
+  std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
+  return set_error(err, MAS_E_CUDA, -1, -1, msg);
+}
+
+#define MAS_CUDA(call, what)                               \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) return cuda_error(err, e_, what); \
+  } while (0)
+
+// validate_config, types.cpp:59-69 (same ostream formatting of the floats).
+int validate_config(const mas_config_t& cfg, mas_error_t* err) {
+  if (cfg.flags & MAS_FLAG_UNCHECKED) return MAS_OK;
+  if (!std::isfinite(cfg.max_neg_val) || cfg.max_neg_val > kMaxNegValCeiling) {
+    std::ostringstream msg;
+    msg << "max_neg_val must be finite and at most " << kMaxNegValCeiling << ", got "
+        << cfg.max_neg_val;
+    return set_error(err, MAS_E_VALIDATION, MAS_ERRC_INVALID_CONFIG, -1, msg.str());
+  }
+  if (cfg.threads < 0)
+    return set_error(err, MAS_E_VALIDATION, MAS_ERRC_INVALID_CONFIG, -1, "threads must be >= 0");
+  if (cfg.engine != MAS_ENGINE_REFERENCE && cfg.engine != MAS_ENGINE_PARALLEL)
+    return set_error(err, MAS_E_VALIDATION, MAS_ERRC_INVALID_CONFIG, -1, "unknown engine");
+  return MAS_OK;
+}
+
+// Batch-level checks (types.cpp:119-126 / parallel.cpp:118-125).
+int validate_dims(int32_t B, int32_t T, int32_t S, mas_error_t* err) {
+  if (B < 1 || T < 1 || S < 1)
+    return set_error(err, MAS_E_VALIDATION, MAS_ERRC_ZERO_DIM, -1,
+                     "batch and capacities must be at least 1");
+  return MAS_OK;
+}
+
+struct ItemError {
+  int item = -1;
+  int errc = -1;
+  std::string message;
+};
+
+// validate_item's length checks, types.cpp:81-106, in the reference order;
+// the NonFinite scan (:107-115) runs on the device.
+bool length_error(int b, uint32_t t, uint32_t s, int32_t T, int32_t S, ItemError* out) {
+  std::ostringstream d;
+  int code = -1;
+  if (t < 1 || s < 1) {
+    d << "valid lengths must be at least 1, got (" << t << ", " << s << ")";
+    code = MAS_ERRC_ZERO_DIM;
+  } else if (t > static_cast<uint32_t>(T) || s > static_cast<uint32_t>(S)) {
+    d << "valid lengths (" << t << ", " << s << ") exceed capacities (" << T << ", " << S << ")";
+    code = MAS_ERRC_LENGTHS_OUT_OF_RANGE;
+  } else if (s > kMaxSpeechLen) {
+    d << "speech length " << s << " exceeds the supported maximum " << kMaxSpeechLen;
+    code = MAS_ERRC_SPEECH_TOO_LONG;
+  } else if (t > s) {
+    d << "text length " << t << " exceeds speech length " << s
+      << "; every text unit needs at least one frame";
+    code = MAS_ERRC_INFEASIBLE_LENGTHS;
+  }
+  if (code < 0) return false;
+  std::ostringstream msg;
+  msg << "item " << b << ": " << d.str();  // fail_item, types.cpp:73-77
+  out->item = b;
+  out->errc = code;
+  out->message = msg.str();
+  return true;
+}
+
+std::string nonfinite_message(int b, int64_t i, int64_t j) {
+  std::ostringstream msg;
+  msg << "item " << b << ": non-finite likelihood at (" << i << ", " << j << ")";
+  return msg.str();
+}
+
+// ---- TMA descriptor encoding through the runtime's driver entry point ----
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// Map r (r = 0, 1) views rows {2k + r} of the whole [B*T_pad][pitch] input
+// as a 2-D tensor [B*T_pad/2][S_cap] with row stride 2*pitch, 32x32 boxes,
+// 128-byte swizzle.
+bool encode_maps(const float* q, int64_t pitch, int64_t rows_total, int64_t S, CUtensorMap* m0,
+                 CUtensorMap* m1) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  for (int r = 0; r < 2; ++r) {
+    CUtensorMap* m = r == 0 ? m0 : m1;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(rows_total / 2)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * pitch * 4)};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    void* addr = const_cast<float*>(q + r * pitch);
+    const CUresult res = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, addr, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) return false;
+  }
+  return true;
+}
+
+int num_sms() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+struct Geometry {
+  int W = 1, K = 1, N = 2, L = 256, Kseg = 1, T_alloc = 64, M = 1;
+};
+
+bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
+  const int warps = std::max(1, (t_max + mas::kRowsPerWarp - 1) / mas::kRowsPerWarp);
+  if (warps <= 4) {
+    g->K = 1;
+    g->W = warps;
+  } else if (warps <= 32) {
+    g->W = 4;
+    g->K = (warps + 3) / 4;
+  } else if (warps <= 8 * mas::kMaxClusterCtas) {
+    g->W = 8;
+    g->K = (warps + 7) / 8;
+  } else {
+    return false;
+  }
+  const int sms = num_sms();
+  const size_t budget = (static_cast<int64_t>(B) * g->K <= sms) ? 220 * 1024 : 110 * 1024;
+  int N = 8;
+  while (N > 2 && mas::fwd_smem_bytes(g->W, N) > budget) --N;
+  g->N = N;
+  g->T_alloc = g->K * g->W * mas::kRowsPerWarp;
+  g->M = (S_cap + 31) / 32;
+  // Backtrack segment: (L/32 + 1) words per row staged for every row.
+  int L = 256;
+  while (L > 32 && static_cast<size_t>(L / 32 + 1) * g->T_alloc * 4 > 96 * 1024) L -= 32;
+  g->L = L;
+  g->Kseg = (S_cap + L - 1) / L;
+  return true;
+}
+
+}  // namespace
+
+struct mas_plan {
+  int32_t B = 0, T = 0, S = 0;
+  int64_t pitch = 0;
+  int T_pad = 0;
+  int mode = 0;  // 0 parallel, 1 reference
+  float mnv = kDefaultMaxNegVal;
+  Geometry geo;
+  std::vector<uint32_t> lengths;  // [B][2], zeroed for items with host errors
+  ItemError first_host_error;
+  // device workspace
+  uint32_t* d_lengths = nullptr;
+  uint32_t* d_dirs = nullptr;
+  int32_t* d_segmap = nullptr;
+  int32_t* d_segrow = nullptr;  // [B][Kseg+1] then [B] counters
+  int* d_flags = nullptr;
+  unsigned long long* d_locate = nullptr;
+  int launches = 0;
+  int device = 0;
+};
+
+extern "C" {
+
+void mas_config_default(mas_config_t* cfg) {
+  cfg->engine = MAS_ENGINE_PARALLEL;
+  cfg->max_neg_val = kDefaultMaxNegVal;
+  cfg->lane_padding = 0;
+  cfg->threads = 0;
+  cfg->flags = 0;
+}
+
+const char* mas_errc_name(int32_t errc) {
+  if (errc < 0 || errc >= static_cast<int32_t>(sizeof(kErrcNames) / sizeof(kErrcNames[0])))
+    return "Unknown";
+  return kErrcNames[errc];
+}
+
+int mas_abi_version(void) { return MAS_ABI_VERSION; }
+
+void mas_plan_destroy(mas_plan_t* p) {
+  if (!p) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  cudaFree(p->d_lengths);
+  cudaFree(p->d_dirs);
+  cudaFree(p->d_segmap);
+  cudaFree(p->d_segrow);
+  cudaFree(p->d_flags);
+  cudaFree(p->d_locate);
+  cudaSetDevice(prev);
+  delete p;
+}
+
+int mas_plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row_pitch,
+                    const uint32_t* lengths, const mas_config_t* cfg_in, mas_plan_t** plan_out,
+                    mas_error_t* err) {
+  clear_error(err);
+  *plan_out = nullptr;
+  mas_config_t cfg;
+  if (cfg_in)
+    cfg = *cfg_in;
+  else
+    mas_config_default(&cfg);
+  int rc = validate_config(cfg, err);  // align_parallel / align_reference first step
+  if (rc) return rc;
+  rc = validate_dims(batch, text_cap, speech_cap, err);
+  if (rc) return rc;
+  if (row_pitch < speech_cap)
+    return set_error(err, MAS_E_UNSUPPORTED, -1, -1, "row_pitch must be >= speech_cap");
+
+  auto* p = new (std::nothrow) mas_plan();
+  if (!p) return set_error(err, MAS_E_UNSUPPORTED, -1, -1, "out of host memory");
+  cudaGetDevice(&p->device);
+  p->B = batch;
+  p->T = text_cap;
+  p->S = speech_cap;
+  p->pitch = row_pitch;
+  p->T_pad = text_cap;
+  p->mode = cfg.engine == MAS_ENGINE_REFERENCE ? 1 : 0;
+  p->mnv = cfg.max_neg_val;
+  p->lengths.resize(static_cast<size_t>(batch) * 2);
+  int t_max = 0;
+  for (int b = 0; b < batch; ++b) {
+    const uint32_t t = lengths ? lengths[2 * b] : static_cast<uint32_t>(text_cap);
+    const uint32_t s = lengths ? lengths[2 * b + 1] : static_cast<uint32_t>(speech_cap);
+    ItemError ie;
+    if (length_error(b, t, s, text_cap, speech_cap, &ie)) {
+      if (p->first_host_error.item < 0) p->first_host_error = ie;
+      p->lengths[2 * b] = 0;
+      p->lengths[2 * b + 1] = 0;
+    } else {
+      p->lengths[2 * b] = t;
+      p->lengths[2 * b + 1] = s;
+      t_max = std::max<int>(t_max, static_cast<int>(t));
+    }
+  }
+  if (!choose_geometry(batch, std::max(t_max, 1), speech_cap, &p->geo)) {
+    delete p;
+    return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
+                     "text length above 8192 rows is not supported by the device path");
+  }
+  const Geometry& g = p->geo;
+  auto fail = [&](cudaError_t e, const char* what) {
+    mas_plan_destroy(p);
+    return cuda_error(err, e, what);
+  };
+  cudaError_t e;
+  if ((e = mas::fwd_configure(g.W, g.N, g.K)) != cudaSuccess) return fail(e, "fwd_configure");
+  if ((e = mas::bt_configure(g.T_alloc, g.L)) != cudaSuccess) return fail(e, "bt_configure");
+  const size_t nB = static_cast<size_t>(batch);
+  if ((e = cudaMalloc(&p->d_lengths, nB * 2 * sizeof(uint32_t))) != cudaSuccess)
+    return fail(e, "cudaMalloc(lengths)");
+  if ((e = cudaMemcpy(p->d_lengths, p->lengths.data(), nB * 2 * sizeof(uint32_t),
+                      cudaMemcpyHostToDevice)) != cudaSuccess)
+    return fail(e, "cudaMemcpy(lengths)");
+  if ((e = cudaMalloc(&p->d_dirs, nB * g.M * g.T_alloc * sizeof(uint32_t))) != cudaSuccess)
+    return fail(e, "cudaMalloc(dirs)");
+  if ((e = cudaMalloc(&p->d_segmap, nB * g.Kseg * g.T_alloc * sizeof(int32_t))) != cudaSuccess)
+    return fail(e, "cudaMalloc(segmap)");
+  const size_t segrow_n = nB * (g.Kseg + 1) + nB;  // + per-item counters
+  if ((e = cudaMalloc(&p->d_segrow, segrow_n * sizeof(int32_t))) != cudaSuccess)
+    return fail(e, "cudaMalloc(segrow)");
+  if ((e = cudaMemset(p->d_segrow, 0, segrow_n * sizeof(int32_t))) != cudaSuccess)
+    return fail(e, "cudaMemset(segrow)");
+  if ((e = cudaMalloc(&p->d_flags, nB * sizeof(int))) != cudaSuccess)
+    return fail(e, "cudaMalloc(flags)");
+  if ((e = cudaMalloc(&p->d_locate, sizeof(unsigned long long))) != cudaSuccess)
+    return fail(e, "cudaMalloc(locate)");
+  *plan_out = p;
+  return MAS_OK;
+}
+
+int mas_plan_launches(const mas_plan_t* p) { return p ? p->launches : 0; }
+
+void mas_plan_geometry(const mas_plan_t* p, int32_t geom[5]) {
+  geom[0] = mas::kRowsPerWarp;
+  geom[1] = p->geo.W;
+  geom[2] = p->geo.K;
+  geom[3] = p->geo.N;
+  geom[4] = p->geo.L;
+}
+
+int mas_plan_enqueue(mas_plan_t* p, const float* d_values, uint8_t* d_out, int32_t* d_paths,
+                     void* stream_v, mas_error_t* err) {
+  clear_error(err);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  if ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (p->pitch & 3) != 0 || (p->T_pad & 1))
+    return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
+                     "device layout needs 16-byte base, pitch % 4 == 0 and even text_cap");
+  CUtensorMap tm0, tm1;
+  if (!encode_maps(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, &tm0, &tm1))
+    return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled failed");
+  const Geometry& g = p->geo;
+  MAS_CUDA(cudaMemsetAsync(p->d_flags, 0, sizeof(int) * p->B, stream), "cudaMemsetAsync(flags)");
+  mas::FwdArgs fa;
+  fa.lengths = p->d_lengths;
+  fa.dirs = p->d_dirs;
+  fa.flags = p->d_flags;
+  fa.T_pad = p->T_pad;
+  fa.M = g.M;
+  fa.T_alloc = g.T_alloc;
+  fa.K = g.K;
+  fa.W = g.W;
+  fa.N = g.N;
+  fa.mnv = p->mnv;
+  fa.row0_up = p->mode == 1 ? -std::numeric_limits<float>::infinity() : p->mnv;
+  MAS_CUDA(mas::launch_fwd(p->mode, tm0, tm1, fa, p->B, stream), "launch mas_fwd");
+  mas::BtArgs ba;
+  ba.lengths = p->d_lengths;
+  ba.dirs = p->d_dirs;
+  ba.seg_map = p->d_segmap;
+  ba.seg_row = p->d_segrow;
+  ba.out = d_out;
+  ba.paths = d_paths;
+  ba.B = p->B;
+  ba.T_cap = p->T;
+  ba.S_cap = p->S;
+  ba.M = g.M;
+  ba.T_alloc = g.T_alloc;
+  ba.L = g.L;
+  ba.Kseg = g.Kseg;
+  int nbt = 0;
+  MAS_CUDA(mas::launch_backtrack(ba, stream, &nbt), "launch backtrack");
+  p->launches = 1 + nbt;
+  return MAS_OK;
+}
+
+int mas_plan_finish(mas_plan_t* p, const float* d_values, void* stream_v, mas_error_t* err) {
+  clear_error(err);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  MAS_CUDA(cudaStreamSynchronize(stream), "kernel execution");
+  std::vector<int> flags(p->B);
+  MAS_CUDA(cudaMemcpy(flags.data(), p->d_flags, sizeof(int) * p->B, cudaMemcpyDeviceToHost),
+           "cudaMemcpy(flags)");
+  const int limit = p->first_host_error.item >= 0 ? p->first_host_error.item : p->B;
+  for (int b = 0; b < limit; ++b) {
+    if (!flags[b]) continue;
+    // Conservative device flag: confirm and locate exactly (row-major first).
+    const unsigned long long none = ~0ull;
+    MAS_CUDA(cudaMemcpyAsync(p->d_locate, &none, sizeof(none), cudaMemcpyHostToDevice, stream),
+             "locate init");
+    MAS_CUDA(mas::launch_locate_nonfinite(d_values, p->pitch, p->T_pad, b,
+                                          static_cast<int>(p->lengths[2 * b]),
+                                          static_cast<int>(p->lengths[2 * b + 1]), p->d_locate,
+                                          stream),
+             "locate");
+    unsigned long long hit = none;
+    MAS_CUDA(cudaMemcpyAsync(&hit, p->d_locate, sizeof(hit), cudaMemcpyDeviceToHost, stream),
+             "locate read");
+    MAS_CUDA(cudaStreamSynchronize(stream), "locate sync");
+    if (hit != none) {
+      const int64_t s = p->lengths[2 * b + 1];
+      const int64_t i = static_cast<int64_t>(hit / s), j = static_cast<int64_t>(hit % s);
+      set_error(err, MAS_E_VALIDATION, MAS_ERRC_NON_FINITE, b, nonfinite_message(b, i, j));
+      err->i = i;
+      err->j = j;
+      return MAS_E_VALIDATION;
+    }
+  }
+  if (p->first_host_error.item >= 0)
+    return set_error(err, MAS_E_VALIDATION, p->first_host_error.errc, p->first_host_error.item,
+                     p->first_host_error.message);
+  return MAS_OK;
+}
+
+int mas_align_device(const float* d_values, int64_t row_pitch, int32_t batch, int32_t text_cap,
+                     int32_t speech_cap, const uint32_t* lengths, const mas_config_t* cfg,
+                     uint8_t* d_out, int32_t* d_paths, void* stream_v, mas_error_t* err) {
+  clear_error(err);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  mas_plan_t* plan = nullptr;
+  int rc = mas_plan_create(batch, text_cap, speech_cap, row_pitch, lengths, cfg, &plan, err);
+  if (rc) return rc;
+  const float* q = d_values;
+  float* scratch = nullptr;
+  if ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (row_pitch & 3) != 0 ||
+      (text_cap & 1) != 0) {
+    // Re-pitch into an aligned [B][T_pad][pitch'] copy the TMA path accepts.
+    const int T_pad = (text_cap + 1) & ~1;
+    const int64_t pitch2 = (static_cast<int64_t>(speech_cap) + 3) & ~int64_t(3);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                    static_cast<size_t>(batch) * T_pad * pitch2 * 4, stream);
+    if (e != cudaSuccess) {
+      mas_plan_destroy(plan);
+      return cuda_error(err, e, "cudaMallocAsync(repitch)");
+    }
+    for (int b = 0; b < batch && e == cudaSuccess; ++b) {
+      e = cudaMemcpy2DAsync(scratch + static_cast<size_t>(b) * T_pad * pitch2, pitch2 * 4,
+                            d_values + static_cast<size_t>(b) * text_cap * row_pitch,
+                            row_pitch * 4, static_cast<size_t>(speech_cap) * 4, text_cap,
+                            cudaMemcpyDeviceToDevice, stream);
+    }
+    if (e != cudaSuccess) {
+      cudaFreeAsync(scratch, stream);
+      mas_plan_destroy(plan);
+      return cuda_error(err, e, "repitch copy");
+    }
+    plan->pitch = pitch2;
+    plan->T_pad = T_pad;
+    q = scratch;
+  }
+  rc = mas_plan_enqueue(plan, q, d_out, d_paths, stream, err);
+  if (rc == MAS_OK) rc = mas_plan_finish(plan, q, stream, err);
+  if (scratch) cudaFreeAsync(scratch, stream);
+  cudaStreamSynchronize(stream);
+  mas_plan_destroy(plan);
+  return rc;
+}
+
+int mas_align_host(const float* values, int32_t batch, int32_t text_cap, int32_t speech_cap,
+                   const uint32_t* lengths, const mas_config_t* cfg, uint8_t* out, int32_t* paths,
+                   mas_error_t* err) {
+  clear_error(err);
+  {
+    mas_config_t c;
+    if (cfg)
+      c = *cfg;
+    else
+      mas_config_default(&c);
+    int rc = validate_config(c, err);
+    if (rc) return rc;
+    rc = validate_dims(batch, text_cap, speech_cap, err);
+    if (rc) return rc;
+  }
+  cudaStream_t stream = cudaStreamPerThread;
+  const int T_pad = (text_cap + 1) & ~1;
+  const int64_t pitch = (static_cast<int64_t>(speech_cap) + 3) & ~int64_t(3);
+  const size_t q_bytes = static_cast<size_t>(batch) * T_pad * pitch * 4;
+  const size_t o_bytes = static_cast<size_t>(batch) * text_cap * speech_cap;
+  const size_t p_bytes = static_cast<size_t>(batch) * speech_cap * 4;
+  mas_plan_t* plan = nullptr;
+  int rc = mas_plan_create(batch, text_cap, speech_cap, pitch, lengths, cfg, &plan, err);
+  if (rc) return rc;
+  plan->T_pad = T_pad;
+  float* d_q = nullptr;
+  uint8_t* d_out = nullptr;
+  int32_t* d_paths = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_q), q_bytes, stream);
+  if (e == cudaSuccess && out) e = cudaMallocAsync(reinterpret_cast<void**>(&d_out), o_bytes, stream);
+  if (e == cudaSuccess && paths)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&d_paths), p_bytes, stream);
+  if (e == cudaSuccess) {
+    if (T_pad == text_cap) {
+      e = cudaMemcpy2DAsync(d_q, pitch * 4, values, static_cast<size_t>(speech_cap) * 4,
+                            static_cast<size_t>(speech_cap) * 4,
+                            static_cast<size_t>(batch) * text_cap, cudaMemcpyHostToDevice, stream);
+    } else {
+      for (int b = 0; b < batch && e == cudaSuccess; ++b)
+        e = cudaMemcpy2DAsync(d_q + static_cast<size_t>(b) * T_pad * pitch, pitch * 4,
+                              values + static_cast<size_t>(b) * text_cap * speech_cap,
+                              static_cast<size_t>(speech_cap) * 4,
+                              static_cast<size_t>(speech_cap) * 4, text_cap,
+                              cudaMemcpyHostToDevice, stream);
+    }
+  }
+  if (e != cudaSuccess) {
+    rc = cuda_error(err, e, "host->device staging");
+  } else {
+    rc = mas_plan_enqueue(plan, d_q, d_out, d_paths, stream, err);
+    if (rc == MAS_OK && out)
+      if ((e = cudaMemcpyAsync(out, d_out, o_bytes, cudaMemcpyDeviceToHost, stream)) != cudaSuccess)
+        rc = cuda_error(err, e, "device->host out");
+    if (rc == MAS_OK && paths)
+      if ((e = cudaMemcpyAsync(paths, d_paths, p_bytes, cudaMemcpyDeviceToHost, stream)) !=
+          cudaSuccess)
+        rc = cuda_error(err, e, "device->host paths");
+    if (rc == MAS_OK) rc = mas_plan_finish(plan, d_q, stream, err);
+  }
+  cudaFreeAsync(d_q, stream);
+  if (d_out) cudaFreeAsync(d_out, stream);
+  if (d_paths) cudaFreeAsync(d_paths, stream);
+  cudaStreamSynchronize(stream);
+  mas_plan_destroy(plan);
+  return rc;
+}
+
+int mas_generate_device(uint64_t seed, int32_t batch, int32_t text_cap, int32_t speech_cap,
+                        int64_t first_item, int64_t row_pitch, float* d_out, void* stream) {
+  // s0 = mix_seed(seed, 0) (bench.hpp:87-91, bench.cpp:172)
+  uint64_t st = seed ^ (0xd1342543de82ef95ULL * 1ull);
+  st += 0x9e3779b97f4a7c15ULL;
+  uint64_t z = st;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  const uint64_t s0 = z ^ (z >> 31);
+  const int64_t first_elem = first_item * static_cast<int64_t>(text_cap) * speech_cap;
+  const cudaError_t e = mas::launch_generate(s0, first_elem, batch, text_cap, speech_cap, row_pitch,
+                                             d_out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? MAS_OK : MAS_E_CUDA;
+}
+
+}  // extern "C"

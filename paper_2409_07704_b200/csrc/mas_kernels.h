@@ -1,0 +1,59 @@
+// mas_kernels.h -- launch parameters shared by the host ABI (mas_abi.cu) and
+// the device kernels.  See DESIGN.md for the data layout in HBM.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace mas {
+
+// Forward kernel geometry: every lane owns kRowsPerLane consecutive text
+// rows, every warp 32 * kRowsPerLane rows, and stages hold kStageCols speech
+// columns.
+constexpr int kRowsPerLane = 2;
+constexpr int kRowsPerWarp = 32 * kRowsPerLane;  // 64
+constexpr int kStageCols = 32;
+constexpr int kStageBytes = kRowsPerWarp * kStageCols * 4;  // 8 KiB
+constexpr int kFifoSlots = 8;  // boundary-row FIFO depth, in 32-column blocks
+constexpr int kMaxWarpsPerCta = 8;
+constexpr int kMaxClusterCtas = 16;
+
+struct FwdArgs {
+  const uint32_t* lengths;  // [B][2] (t, s); t == 0 marks an item not to run
+  uint32_t* dirs;           // [B][M][T_alloc] direction words, see DESIGN.md
+  int* flags;               // [B] NonFinite candidate flags
+  int T_pad;                // rows between items in the (pitched) input
+  int M;                    // direction words per row = ceil(S_cap / 32)
+  int T_alloc;              // rows per item in `dirs` = K * W * 64
+  int K;                    // CTAs per item (cluster size)
+  int W;                    // warps per CTA
+  int N;                    // TMA stages per warp
+  float mnv;                // max_neg_val
+  float row0_up;            // value above row 0: mnv (parallel) / -inf (reference)
+};
+
+struct BtArgs {
+  const uint32_t* lengths;  // [B][2]
+  const uint32_t* dirs;     // [B][M][T_alloc]
+  int32_t* seg_map;         // [B][Kseg][T_alloc] pass-1 maps (row at segment start)
+  int32_t* seg_row;         // [B][Kseg + 1] pass-2 path rows at segment starts
+  uint8_t* out;             // [B][T_cap][S_cap] or null
+  int32_t* paths;           // [B][S_cap] or null
+  int B, T_cap, S_cap, M, T_alloc;
+  int L;                    // segment length in columns (multiple of 32)
+  int Kseg;                 // ceil(S_cap / L)
+};
+
+size_t fwd_smem_bytes(int W, int N);
+cudaError_t launch_fwd(int mode, const CUtensorMap& tm0, const CUtensorMap& tm1, const FwdArgs& a,
+                       int B, cudaStream_t stream);
+cudaError_t launch_backtrack(const BtArgs& a, cudaStream_t stream, int* launches);
+cudaError_t launch_locate_nonfinite(const float* q, int64_t row_pitch, int T_pad, int b, int t,
+                                    int s, unsigned long long* d_result, cudaStream_t stream);
+cudaError_t launch_generate(uint64_t s0, int64_t first_elem, int B, int T, int S, int64_t pitch,
+                            float* out, cudaStream_t stream);
+cudaError_t fwd_configure(int W, int N, int K);
+int fwd_max_active_clusters(int W, int N, int K, int mode);
+
+}  // namespace mas
