@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -174,6 +175,20 @@ bool encode_maps(const float* q, int64_t pitch, int64_t rows_total, int64_t S, C
   return true;
 }
 
+// The uint8 output [B*T_cap][S_cap] as a 2-D tensor with 32 x 64 boxes: the
+// forward kernel TMA-stores zero tiles through it.
+bool encode_out_map(uint8_t* out, int64_t rows, int64_t S, CUtensorMap* m) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(S)};
+  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(mas::kRowsPerWarp)};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, out, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int num_sms() {
   int dev = 0, n = 148;
   cudaGetDevice(&dev);
@@ -206,11 +221,9 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
   g->N = N;
   g->T_alloc = g->K * g->W * mas::kRowsPerWarp;
   g->M = (S_cap + 31) / 32;
-  // Backtrack segment: (L/32 + 1) words per row staged for every row.
-  int L = 256;
-  while (L > 32 && static_cast<size_t>(L / 32 + 1) * g->T_alloc * 4 > 96 * 1024) L -= 32;
-  g->L = L;
-  g->Kseg = (S_cap + L - 1) / L;
+  // Output segment written by one writer CTA: [T_cap x L] bytes.
+  g->L = 256;
+  g->Kseg = (S_cap + g->L - 1) / g->L;
   return true;
 }
 
@@ -228,8 +241,7 @@ struct mas_plan {
   // device workspace
   uint32_t* d_lengths = nullptr;
   uint32_t* d_dirs = nullptr;
-  int32_t* d_segmap = nullptr;
-  int32_t* d_segrow = nullptr;  // [B][Kseg+1] then [B] counters
+  bool all_full = true;  // every item spans the full [T_cap x S_cap]
   int* d_flags = nullptr;
   unsigned long long* d_locate = nullptr;
   int launches = 0;
@@ -261,8 +273,6 @@ void mas_plan_destroy(mas_plan_t* p) {
   cudaSetDevice(p->device);
   cudaFree(p->d_lengths);
   cudaFree(p->d_dirs);
-  cudaFree(p->d_segmap);
-  cudaFree(p->d_segrow);
   cudaFree(p->d_flags);
   cudaFree(p->d_locate);
   cudaSetDevice(prev);
@@ -306,9 +316,12 @@ int mas_plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t
       if (p->first_host_error.item < 0) p->first_host_error = ie;
       p->lengths[2 * b] = 0;
       p->lengths[2 * b + 1] = 0;
+      p->all_full = false;
     } else {
       p->lengths[2 * b] = t;
       p->lengths[2 * b + 1] = s;
+      if (t != static_cast<uint32_t>(text_cap) || s != static_cast<uint32_t>(speech_cap))
+        p->all_full = false;
       t_max = std::max<int>(t_max, static_cast<int>(t));
     }
   }
@@ -333,13 +346,6 @@ int mas_plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t
     return fail(e, "cudaMemcpy(lengths)");
   if ((e = cudaMalloc(&p->d_dirs, nB * g.M * g.T_alloc * sizeof(uint32_t))) != cudaSuccess)
     return fail(e, "cudaMalloc(dirs)");
-  if ((e = cudaMalloc(&p->d_segmap, nB * g.Kseg * g.T_alloc * sizeof(int32_t))) != cudaSuccess)
-    return fail(e, "cudaMalloc(segmap)");
-  const size_t segrow_n = nB * (g.Kseg + 1) + nB;  // + per-item counters
-  if ((e = cudaMalloc(&p->d_segrow, segrow_n * sizeof(int32_t))) != cudaSuccess)
-    return fail(e, "cudaMalloc(segrow)");
-  if ((e = cudaMemset(p->d_segrow, 0, segrow_n * sizeof(int32_t))) != cudaSuccess)
-    return fail(e, "cudaMemset(segrow)");
   if ((e = cudaMalloc(&p->d_flags, nB * sizeof(int))) != cudaSuccess)
     return fail(e, "cudaMalloc(flags)");
   if ((e = cudaMalloc(&p->d_locate, sizeof(unsigned long long))) != cudaSuccess)
@@ -382,23 +388,39 @@ int mas_plan_enqueue(mas_plan_t* p, const float* d_values, uint8_t* d_out, int32
   fa.N = g.N;
   fa.mnv = p->mnv;
   fa.row0_up = p->mode == 1 ? -std::numeric_limits<float>::infinity() : p->mnv;
-  MAS_CUDA(mas::launch_fwd(p->mode, tm0, tm1, fa, p->B, stream), "launch mas_fwd");
+  // The output's zero fill rides along with the forward pass when every
+  // item is full length (its warps then cover every row and column); ragged
+  // batches get a stream-ordered memset instead.
+  static const bool no_fuse = [] {
+    const char* e = std::getenv("MAS_NO_FUSED_ZERO");
+    return e && e[0] == '1';
+  }();
+  const bool fused_zero = d_out && !no_fuse && p->all_full && (p->S % 16) == 0 &&
+                          (reinterpret_cast<uintptr_t>(d_out) & 15u) == 0;
+  if (d_out && !fused_zero) {
+    MAS_CUDA(cudaMemsetAsync(d_out, 0, static_cast<size_t>(p->B) * p->T * p->S, stream),
+             "cudaMemsetAsync(out)");
+  }
+  CUtensorMap tm_out;
+  std::memset(&tm_out, 0, sizeof(tm_out));
+  if (fused_zero && !encode_out_map(d_out, static_cast<int64_t>(p->B) * p->T, p->S, &tm_out))
+    return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled(out) failed");
+  fa.zero_fill = fused_zero ? 1 : 0;
+  fa.T_cap = p->T;
+  fa.S_cap = p->S;
+  MAS_CUDA(mas::launch_fwd(p->mode, tm0, tm1, tm_out, fa, p->B, stream), "launch mas_fwd");
   mas::BtArgs ba;
   ba.lengths = p->d_lengths;
   ba.dirs = p->d_dirs;
-  ba.seg_map = p->d_segmap;
-  ba.seg_row = p->d_segrow;
+  ba.path = d_paths;
   ba.out = d_out;
-  ba.paths = d_paths;
   ba.B = p->B;
   ba.T_cap = p->T;
   ba.S_cap = p->S;
   ba.M = g.M;
   ba.T_alloc = g.T_alloc;
-  ba.L = g.L;
-  ba.Kseg = g.Kseg;
   int nbt = 0;
-  MAS_CUDA(mas::launch_backtrack(ba, stream, &nbt), "launch backtrack");
+  if (d_out || d_paths) MAS_CUDA(mas::launch_backtrack(ba, stream, &nbt), "launch backtrack");
   p->launches = 1 + nbt;
   return MAS_OK;
 }

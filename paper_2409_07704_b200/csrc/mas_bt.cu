@@ -1,26 +1,24 @@
-// mas_bt.cu -- K2: the backtrack and output writer, plus the generator (K3)
-// and the NonFinite locator.
+// mas_bt.cu -- K2: the backtrack, plus the generator (K3) and the NonFinite
+// locator.
 //
 // The reference walk (src/backtrack.hpp:21-32) is one serial pass per item:
 //   cur = t-1; path[s-1] = cur;
 //   for j = s-2..0: if (cur > 0 && Q[cur-1][j] > Q[cur][j]) --cur; path[j] = cur;
 // followed by write_path (src/types.cpp:181-185) into a zeroed [T][S] byte
 // matrix (types.cpp:40-47).  Here the walk reads the forward kernel's
-// direction bits, bit(i, j) == (Q[i-1][j] > Q[i][j]), and is split over
-// speech segments of L columns so it runs on the whole GPU:
+// direction bits, bit(i, j) == (Q[i-1][j] > Q[i][j]), stored as one u32 per
+// row per 32 columns (word m of row i holds columns 32m-1 .. 32m+30).  The
+// zero fill of the output happens in the forward kernel (or a memset for
+// ragged shapes), so this kernel only walks and scatters the ones:
 //
-//   pass 1 (bt_segmap):  for every segment k and EVERY possible entry row x,
-//       G_k(x) = row of the walk at column kL when it is at row x at column
-//       (k+1)L -- independent walks, one thread each, over the segment's
-//       direction words staged in shared memory.  The walk jumps row to row
-//       with a find-last-set-bit per 32-column word (one step per text row,
-//       not per speech column).  The CTA of the item's last segment walks
-//       from (t-1, s-1) instead; the last CTA of the item to finish then
-//       chains P_k = G_k(P_{k+1}) down to column 0.
-//   pass 2 (bt_write):  each segment re-walks from its known entry row,
-//       producing path[j], and writes its [T_cap x L] slice of the output
-//       with 16-byte stores (zeros everywhere but the path) plus the int32
-//       path row -- so the dense output is written exactly once.
+//   one warp per item walks row to row rather than column to column --
+//   inside a 32-column word the next step down is a find-last-set-bit, so
+//   an item costs ~(t + s/32) dependent steps instead of s.  The window of
+//   direction words the walk can reach in a block (at most 32 rows per
+//   block) is prefetched kWinStages blocks ahead with cp.async; lane 0 walks
+//   with a one-row load lookahead; each finished 32-column block is expanded
+//   by the whole warp (popc of the exit mask) into path[] and the ones of
+//   the alignment matrix.
 #include <cstdio>
 #include <cstdlib>
 
@@ -30,201 +28,109 @@ namespace mas {
 
 namespace {
 
-constexpr int kBtThreads = 256;
+constexpr int kWinStages = 8;                      // blocks prefetched ahead
+constexpr int kWinWords = 9;                       // words per lane per stage
+constexpr int kWinRows = 32 * kWinWords;           // >= 32 * kWinStages + 1 rows
 
-// Highest set-bit position <= p (and >= lo) in row y of the staged words,
-// or -1.  Word wi of the tile holds positions (m0 + wi) * 32 + [0, 32);
-// position p == column p-1 (direction words are offset by one column).
-__device__ __forceinline__ int find_exit(const uint32_t* __restrict__ words, int nrows_stride, int y,
-                                         int p, int lo, int m0) {
-  int wi = (p >> 5) - m0;
-  uint32_t w = words[wi * nrows_stride + y] & (0xffffffffu >> (31 - (p & 31)));
-  const int lo_wi = (lo >> 5) - m0;
-  const uint32_t lo_mask = 0xffffffffu << (lo & 31);
-  if (wi == lo_wi) w &= lo_mask;
-  while (w == 0u) {
-    --wi;
-    if (wi < lo_wi) return -1;
-    w = words[wi * nrows_stride + y];
-    if (wi == lo_wi) w &= lo_mask;
-  }
-  return (m0 + wi) * 32 + 31 - __clz(w);
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Walk from row y entering at position p (testing column p-1 first) down to
-// position lo; returns the row at column lo-1.  Optionally records
-// path[j - col0] for every column j visited.
-__device__ __forceinline__ int walk(const uint32_t* __restrict__ words, int stride, int y, int p,
-                                   int lo, int m0, int32_t* path, int col0) {
-  while (y > 0 && p >= lo) {
-    const int pe = find_exit(words, stride, y, p, lo, m0);
-    if (pe < 0) break;
-    if (path) {
-      for (int j = p - 1; j >= pe; --j) path[j - col0] = y;  // columns pe..p-1 stay in row y
-      path[pe - 1 - col0] = y - 1;
+// Prefetch block m's direction words for rows [base - kWinRows + 1, base]
+// into stage `st`: lane l copies rows base - l - 32 i.
+__device__ __forceinline__ void prefetch_window(uint32_t win_smem, int st, const uint32_t* src,
+                                                int T_alloc, int m, int base, int lane) {
+  if (m >= 0) {
+    const uint32_t* col = src + static_cast<size_t>(m) * T_alloc;
+#pragma unroll
+    for (int i = 0; i < kWinWords; ++i) {
+      const int idx = lane + 32 * i;
+      const int row = base - idx;
+      cp_async4(win_smem + static_cast<uint32_t>((st * kWinRows + idx) * 4),
+                col + (row >= 0 ? row : 0), row >= 0);
     }
-    --y;
-    p = pe - 1;
   }
-  if (path) {
-    for (int j = p - 1; j >= lo - 1; --j) path[j - col0] = y;
-  }
-  return y;
+  cp_async_commit();
 }
 
-__global__ void __launch_bounds__(kBtThreads) bt_segmap_kernel(const BtArgs a, int* counters) {
-  extern __shared__ uint32_t words[];  // [NW][t_b]
-  __shared__ int s_last;
-  const int k = blockIdx.x;
-  const int b = blockIdx.y;
-  const int t_b = static_cast<int>(a.lengths[2 * b]);
-  const int s_b = static_cast<int>(a.lengths[2 * b + 1]);
-  if (t_b <= 0 || s_b <= 0) return;
-  const int Kb = (s_b + a.L - 1) / a.L;
-  if (k >= Kb) return;
-  const int NW = a.L / 32 + 1;
-  const int m0 = (k * a.L) >> 5;
-
-  // Stage the segment's direction words for rows [0, t_b).
+__global__ void __launch_bounds__(32) bt_walk_kernel(const BtArgs a) {
+  __shared__ uint32_t win[kWinStages * kWinRows];
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x;
+  const int t = static_cast<int>(a.lengths[2 * b]);
+  const int s = static_cast<int>(a.lengths[2 * b + 1]);
+  int32_t* path = a.path ? a.path + static_cast<size_t>(b) * a.S_cap : nullptr;
+  uint8_t* out = a.out ? a.out + static_cast<size_t>(b) * a.T_cap * a.S_cap : nullptr;
+  if (path)
+    for (int j = (s > 0 ? s : 0) + lane; j < a.S_cap; j += 32) path[j] = -1;
+  if (t <= 0 || s <= 0) return;
   const uint32_t* src = a.dirs + static_cast<size_t>(b) * a.M * a.T_alloc;
-  const int nw_avail = (a.M - m0) < NW ? (a.M - m0) : NW;
-  for (int idx = threadIdx.x; idx < NW * t_b; idx += blockDim.x) {
-    const int wi = idx / t_b;
-    const int y = idx - wi * t_b;
-    words[idx] = wi < nw_avail ? __ldcg(src + static_cast<size_t>(m0 + wi) * a.T_alloc + y) : 0u;
+  const uint32_t win_smem = static_cast<uint32_t>(__cvta_generic_to_shared(win));
+
+  int cur = t - 1;
+  if (lane == 0) {  // backtrack.hpp:23-24
+    if (path) path[s - 1] = cur;
+    if (out) out[static_cast<size_t>(cur) * a.S_cap + s - 1] = 1;
   }
-  __syncthreads();
-
-  const int lo = k * a.L + 1;  // column kL
-  int32_t* segrow = a.seg_row + static_cast<size_t>(b) * (a.Kseg + 1);
-  if (k < Kb - 1) {
-    int32_t* map = a.seg_map + (static_cast<size_t>(b) * a.Kseg + k) * a.T_alloc;
-    const int p_in = (k + 1) * a.L;  // column (k+1)L - 1
-    for (int x = threadIdx.x; x < t_b; x += blockDim.x) {
-      map[x] = walk(words, t_b, x, p_in, lo, m0, nullptr, 0);
-    }
-  } else if (threadIdx.x == 0) {
-    // Last segment: path[s-1] = t-1 (backtrack.hpp:23-24).
-    segrow[Kb] = t_b - 1;
-    segrow[Kb - 1] = s_b >= 2 ? walk(words, t_b, t_b - 1, s_b - 1, lo, m0, nullptr, 0) : t_b - 1;
-  }
-
-  // The last CTA of this item to finish chains the maps down to column 0.
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int old = atomicAdd(counters + b, 1);
-    s_last = old == Kb - 1;
-  }
-  __syncthreads();
-  if (s_last && threadIdx.x == 0) {
-    __threadfence();
-    int P = __ldcg(segrow + (Kb - 1));
-    for (int kk = Kb - 2; kk >= 0; --kk) {
-      P = __ldcg(a.seg_map + (static_cast<size_t>(b) * a.Kseg + kk) * a.T_alloc + P);
-      segrow[kk] = P;
-    }
-    counters[b] = 0;  // ready for the next call (stream-ordered)
-  }
-}
-
-template <int VEC>
-__device__ __forceinline__ void store_chunk(uint8_t* dst, const uint8_t* v);
-
-template <>
-__device__ __forceinline__ void store_chunk<16>(uint8_t* dst, const uint8_t* v) {
-  *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
-}
-template <>
-__device__ __forceinline__ void store_chunk<4>(uint8_t* dst, const uint8_t* v) {
-  *reinterpret_cast<uint32_t*>(dst) = *reinterpret_cast<const uint32_t*>(v);
-}
-template <>
-__device__ __forceinline__ void store_chunk<1>(uint8_t* dst, const uint8_t* v) {
-  *dst = *v;
-}
-
-template <int VEC>
-__global__ void __launch_bounds__(kBtThreads) bt_write_kernel(const BtArgs a) {
-  extern __shared__ uint32_t dyn[];
-  __shared__ int s_rlo, s_rhi;
-  const int k = blockIdx.x;
-  const int b = blockIdx.y;
-  const int t_b = static_cast<int>(a.lengths[2 * b]);
-  const int s_b = static_cast<int>(a.lengths[2 * b + 1]);
-  const int c0 = k * a.L;
-  const int ncols = (a.S_cap - c0) < a.L ? (a.S_cap - c0) : a.L;
-  int32_t* path = reinterpret_cast<int32_t*>(dyn);  // [L]
-  uint32_t* words = dyn + a.L;                      // [NW][rows]
-  const bool active = t_b > 0 && s_b > 0 && c0 < s_b;
-
-  if (threadIdx.x == 0) {
-    s_rlo = 1;
-    s_rhi = 0;
-  }
-  for (int j = threadIdx.x; j < a.L; j += blockDim.x) path[j] = -1;
-  __syncthreads();
-
-  if (active) {
-    const int Kb = (s_b + a.L - 1) / a.L;
-    const int32_t* segrow = a.seg_row + static_cast<size_t>(b) * (a.Kseg + 1);
-    const int r_hi = __ldcg(segrow + k + 1);  // row at column (k+1)L, or t-1 at s-1
-    const int r_lo = __ldcg(segrow + k);      // row at column kL
-    const int nrows = r_hi - r_lo + 1;
-    const int NW = a.L / 32 + 1;
-    const int m0 = c0 >> 5;
-    const int nw_avail = (a.M - m0) < NW ? (a.M - m0) : NW;
-    const uint32_t* src = a.dirs + static_cast<size_t>(b) * a.M * a.T_alloc;
-    for (int idx = threadIdx.x; idx < NW * nrows; idx += blockDim.x) {
-      const int wi = idx / nrows;
-      const int y = idx - wi * nrows;
-      words[idx] =
-          wi < nw_avail ? __ldcg(src + static_cast<size_t>(m0 + wi) * a.T_alloc + r_lo + y) : 0u;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      // Walk in tile-local row coordinates (row r_lo maps to 0).  The walk
-      // never leaves [r_lo, r_hi]: the pass-1 maps said it ends at r_lo.
-      const bool last = k == Kb - 1;
-      const int p_in = last ? s_b - 1 : (k + 1) * a.L;
-      const int lo = c0 + 1;
-      if (last) path[s_b - 1 - c0] = r_hi - r_lo;
-      walk(words, nrows, r_hi - r_lo, p_in, lo, m0, path, c0);
-      // Shift back to absolute rows (walk leaves row 0 == r_lo untouched: y > 0 check
-      // is relative; rows below r_lo are never needed since the walk ends at r_lo).
-      s_rlo = r_lo;
-      s_rhi = r_hi;
-    }
-    __syncthreads();
-    const int last_col = (s_b - c0) < a.L ? (s_b - c0) : a.L;
-    for (int j = threadIdx.x; j < last_col; j += blockDim.x) path[j] += s_rlo;
-    __syncthreads();
-  }
-
-  // paths row
-  if (a.paths) {
-    int32_t* prow = a.paths + static_cast<size_t>(b) * a.S_cap + c0;
-    for (int j = threadIdx.x; j < ncols; j += blockDim.x) prow[j] = path[j];
-  }
-  // dense output slice [T_cap][ncols]
-  if (a.out) {
-    const int rlo = s_rlo, rhi = s_rhi;
-    const int nchunk = (ncols + VEC - 1) / VEC;
-    uint8_t* base = a.out + static_cast<size_t>(b) * a.T_cap * a.S_cap + c0;
-    for (int idx = threadIdx.x; idx < a.T_cap * nchunk; idx += blockDim.x) {
-      const int i = idx / nchunk;
-      const int ch = idx - i * nchunk;
-      alignas(16) uint8_t v[VEC];
+  // Column j's bit sits at position p = j + 1; the walk covers p = s-1 .. 1.
+  const int mtop = (s - 1) >> 5;
+  int base[kWinStages];
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) v[e] = 0;
-      if (i >= rlo && i <= rhi) {
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const int j = ch * VEC + e;
-          v[e] = (j < ncols && path[j] == i) ? 1 : 0;
-        }
+  for (int i = 0; i < kWinStages; ++i) {
+    base[i] = cur;
+    prefetch_window(win_smem, (mtop - i) & (kWinStages - 1), src, a.T_alloc, mtop - i, cur, lane);
+  }
+  for (int m = mtop; m >= 0; --m) {
+    const int st = m & (kWinStages - 1);
+    cp_async_wait<kWinStages - 1>();
+    __syncwarp();
+    const int wb = base[0];
+    const int p_top = (m == mtop) ? ((s - 1) & 31) : 31;
+    const int p_min = (m == 0) ? 1 : 0;
+    uint32_t ex = 0;
+    int y = cur;
+    if (lane == 0 && y > 0 && p_top >= p_min) {
+      const uint32_t* w_st = win + st * kWinRows + wb;  // row y at w_st[-y]
+      const uint32_t lo_mask = (m == 0) ? ~1u : ~0u;
+      int p = p_top;
+      uint32_t w = w_st[-y];
+      while (true) {
+        const uint32_t w_next = w_st[-(y - 1)];  // lookahead: the next row is always y-1
+        const uint32_t hit = w & lo_mask & (0xffffffffu >> (31 - p));
+        if (hit == 0u) break;
+        const int e = 31 - __clz(hit);
+        ex |= 1u << e;
+        --y;
+        p = e - 1;
+        if (y == 0 || p < p_min) break;
+        w = w_next;
       }
-      store_chunk<VEC>(base + static_cast<size_t>(i) * a.S_cap + ch * VEC, v);
+    }
+    ex = __shfl_sync(0xffffffffu, ex, 0);
+    const int cur_top = cur;
+    cur = __shfl_sync(0xffffffffu, y, 0);
+#pragma unroll
+    for (int i = 0; i < kWinStages - 1; ++i) base[i] = base[i + 1];
+    base[kWinStages - 1] = cur;
+    __syncwarp();
+    prefetch_window(win_smem, st, src, a.T_alloc, m - kWinStages, cur, lane);
+    // Expand the block: column 32m + u - 1 (position u) sits at row
+    // cur_top - #exits at positions >= u.
+    const int u = lane;
+    if (u >= p_min && u <= p_top) {
+      const int col = 32 * m + u - 1;
+      const int row = cur_top - __popc(ex >> u);
+      if (path) path[col] = row;
+      if (out) out[static_cast<size_t>(row) * a.S_cap + col] = 1;
     }
   }
 }
@@ -239,7 +145,7 @@ __global__ void bt_serial_kernel(const BtArgs a) {
   if (t <= 0 || s <= 0) return;
   const uint32_t* src = a.dirs + static_cast<size_t>(b) * a.M * a.T_alloc;
   uint8_t* out = a.out ? a.out + static_cast<size_t>(b) * a.T_cap * a.S_cap : nullptr;
-  int32_t* prow = a.paths ? a.paths + static_cast<size_t>(b) * a.S_cap : nullptr;
+  int32_t* prow = a.path ? a.path + static_cast<size_t>(b) * a.S_cap : nullptr;
   int cur = t - 1;
   if (out) out[static_cast<size_t>(cur) * a.S_cap + s - 1] = 1;
   if (prow) prow[s - 1] = cur;
@@ -255,6 +161,7 @@ __global__ void bt_serial_kernel(const BtArgs a) {
 }
 
 __global__ void fill_paths_kernel(int32_t* paths, size_t n) {
+  if (!paths) return;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
     paths[i] = -1;
@@ -313,55 +220,19 @@ cudaError_t launch_backtrack(const BtArgs& a, cudaStream_t stream, int* launches
     const char* e = std::getenv("MAS_BT_SERIAL");
     return e && e[0] == '1';
   }();
-  int n = 0;
   if (serial) {
-    if (a.out) {
-      cudaError_t e = cudaMemsetAsync(a.out, 0, static_cast<size_t>(a.B) * a.T_cap * a.S_cap, stream);
-      if (e != cudaSuccess) return e;
-    }
-    if (a.paths) {
-      fill_paths_kernel<<<grid_for(static_cast<size_t>(a.B) * a.S_cap, 256), 256, 0, stream>>>(
-          a.paths, static_cast<size_t>(a.B) * a.S_cap);
-      ++n;
-    }
+    fill_paths_kernel<<<grid_for(static_cast<size_t>(a.B) * a.S_cap, 256), 256, 0, stream>>>(
+        a.path, static_cast<size_t>(a.B) * a.S_cap);
     bt_serial_kernel<<<(a.B + 63) / 64, 64, 0, stream>>>(a);
-    ++n;
-    if (launches) *launches = n;
+    if (launches) *launches = 2;
     return cudaGetLastError();
   }
-  const int NW = a.L / 32 + 1;
-  // counters live right after seg_row's [B][Kseg+1] block (see mas_abi.cu).
-  int* counters = reinterpret_cast<int*>(a.seg_row + static_cast<size_t>(a.B) * (a.Kseg + 1));
-  const size_t smem1 = static_cast<size_t>(NW) * a.T_alloc * 4;
-  bt_segmap_kernel<<<dim3(a.Kseg, a.B), kBtThreads, smem1, stream>>>(a, counters);
-  ++n;
-  const size_t smem2 = static_cast<size_t>(a.L) * 4 + static_cast<size_t>(NW) * (a.L + 1) * 4;
-  const dim3 grid2(a.Kseg, a.B);
-  if (a.S_cap % 16 == 0)
-    bt_write_kernel<16><<<grid2, kBtThreads, smem2, stream>>>(a);
-  else if (a.S_cap % 4 == 0)
-    bt_write_kernel<4><<<grid2, kBtThreads, smem2, stream>>>(a);
-  else
-    bt_write_kernel<1><<<grid2, kBtThreads, smem2, stream>>>(a);
-  ++n;
-  if (launches) *launches = n;
+  bt_walk_kernel<<<a.B, 32, 0, stream>>>(a);
+  if (launches) *launches = 1;
   return cudaGetLastError();
 }
 
-cudaError_t bt_configure(int T_alloc, int L) {
-  const int NW = L / 32 + 1;
-  const int smem1 = NW * T_alloc * 4;
-  cudaError_t e = cudaFuncSetAttribute(bt_segmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       smem1 > 48 * 1024 ? smem1 : 48 * 1024);
-  if (e != cudaSuccess) return e;
-  const int smem2 = L * 4 + NW * (L + 1) * 4;
-  const int s2 = smem2 > 48 * 1024 ? smem2 : 48 * 1024;
-  e = cudaFuncSetAttribute(bt_write_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(bt_write_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(bt_write_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2);
-}
+cudaError_t bt_configure(int /*T_alloc*/, int /*L*/) { return cudaSuccess; }
 
 cudaError_t launch_locate_nonfinite(const float* q, int64_t row_pitch, int T_pad, int b, int t,
                                     int s, unsigned long long* d_result, cudaStream_t stream) {

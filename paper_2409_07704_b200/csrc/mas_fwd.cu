@@ -33,17 +33,22 @@ namespace mas {
 namespace {
 
 struct SmemLayout {
-  uint32_t ring, bars, fifo, head, tail, total;
+  uint32_t ring, bars, full, empty, fifo, zero, total;
 };
 
+// Per CTA: W rings of N TMA stages, the TMA mbarriers, and per warp a
+// kFifoSlots-deep boundary-row FIFO with its "full" barriers (completed by
+// the producer's st.async bytes) and the "empty" barriers of the FIFO this
+// warp feeds (arrived remotely by its consumer).
 __host__ __device__ inline SmemLayout smem_layout(int W, int N) {
   SmemLayout L;
   L.ring = 0;
   L.bars = static_cast<uint32_t>(W * N * kStageBytes);
-  L.fifo = L.bars + static_cast<uint32_t>(((W * N * 8) + 127) & ~127);
-  L.head = L.fifo + static_cast<uint32_t>(W * kFifoSlots * 32 * 4);
-  L.tail = L.head + 128u;
-  L.total = L.tail + 128u;
+  L.full = L.bars + static_cast<uint32_t>(W * N * 8);
+  L.empty = L.full + static_cast<uint32_t>(W * kFifoSlots * 8);
+  L.fifo = (L.empty + static_cast<uint32_t>(W * kFifoSlots * 8) + 127u) & ~127u;
+  L.zero = L.fifo + static_cast<uint32_t>(W * kFifoSlots * 32 * 4);
+  L.total = L.zero + static_cast<uint32_t>(kRowsPerWarp * 32);
   return L;
 }
 
@@ -78,8 +83,8 @@ __device__ __forceinline__ void fwd_block(const uint8_t* __restrict__ stage,
       const float bnd = (u == 0) ? vprev : v[u - 1];
       const float send = is31 ? bnd : o1;
       const float up = __shfl_sync(0xffffffffu, send, srclane);
-      const bool p0 = up > o0;  // bit(row0, c-1)
-      const bool p1 = o0 > o1;  // bit(row1, c-1)
+      const uint32_t p0 = gt_mask(up, o0);  // bit(row0, c-1)
+      const uint32_t p1 = gt_mask(o0, o1);  // bit(row1, c-1)
       float n0 = q0 + fmaxf(up, o0);
       float n1 = q1 + fmaxf(o0, o1);
       if (GENERIC) {
@@ -93,8 +98,8 @@ __device__ __forceinline__ void fwd_block(const uint8_t* __restrict__ stage,
           n1 = mnv;
         }
       }
-      w0 |= static_cast<uint32_t>(p0) << u;
-      w1 |= static_cast<uint32_t>(p1) << u;
+      w0 |= p0 & (1u << u);
+      w1 |= p1 & (1u << u);
       fold_abs_max_nan(acc, q0, q1);
       ex[u] = n1;
       o0 = n0;
@@ -106,7 +111,7 @@ __device__ __forceinline__ void fwd_block(const uint8_t* __restrict__ stage,
 template <int MODE>
 __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
     mas_fwd_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
-                   const FwdArgs a) {
+                   const __grid_constant__ CUtensorMap tm_out, const FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_addr(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -125,13 +130,19 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
   const int s_b = static_cast<int>(a.lengths[2 * b + 1]);
 
   const uint32_t bar0 = base + L.bars + static_cast<uint32_t>(warp * N * 8);
-  const uint32_t my_head = base + L.head + static_cast<uint32_t>(warp * 4);
-  const uint32_t my_tail = base + L.tail + static_cast<uint32_t>(warp * 4);
+  const uint32_t my_full = base + L.full + static_cast<uint32_t>(warp * kFifoSlots * 8);
+  const uint32_t my_empty = base + L.empty + static_cast<uint32_t>(warp * kFifoSlots * 8);
   if (lane == 0) {
     for (int s = 0; s < N; ++s) mbar_init(bar0 + 8u * s, 1u);
-    *reinterpret_cast<volatile uint32_t*>(sbase + L.head + warp * 4) = 0u;
-    *reinterpret_cast<volatile uint32_t*>(sbase + L.tail + warp * 4) = 0u;
+    for (int s = 0; s < kFifoSlots; ++s) {
+      mbar_init(my_full + 8u * s, 1u);
+      mbar_init(my_empty + 8u * s, 1u);
+    }
   }
+  // A zeroed 64 x 32-byte tile, the TMA-store source of the fused output fill.
+  for (int k = threadIdx.x; k < kRowsPerWarp * 32 / 16; k += blockDim.x)
+    reinterpret_cast<uint4*>(sbase + L.zero)[k] = make_uint4(0u, 0u, 0u, 0u);
+  fence_proxy_async_smem();
   fence_mbar_init();
   cluster_sync_all();  // every CTA's FIFO state exists before any remote access
 
@@ -149,10 +160,14 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
       pw = W - 1;
       pr = crank - 1;
     }
+    // FIFO endpoints: my consumer's slots + "full" barriers, my producer's
+    // "empty" barriers (addresses in the cluster shared window).
     const uint32_t next_fifo =
         has_out ? mapa(base + L.fifo + static_cast<uint32_t>(nw * kFifoSlots * 128), nr) : 0u;
-    const uint32_t next_head = has_out ? mapa(base + L.head + static_cast<uint32_t>(nw * 4), nr) : 0u;
-    const uint32_t prev_tail = has_in ? mapa(base + L.tail + static_cast<uint32_t>(pw * 4), pr) : 0u;
+    const uint32_t next_full =
+        has_out ? mapa(base + L.full + static_cast<uint32_t>(nw * kFifoSlots * 8), nr) : 0u;
+    const uint32_t prev_empty =
+        has_in ? mapa(base + L.empty + static_cast<uint32_t>(pw * kFifoSlots * 8), pr) : 0u;
     const uint8_t* my_fifo = sbase + L.fifo + warp * kFifoSlots * 128;
 
     const uint32_t ring = base + L.ring + static_cast<uint32_t>(warp * N * kStageBytes);
@@ -163,7 +178,11 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
 
     const int nblk = (s_b + kStageCols - 1) / kStageCols;
     const int row_pair = (b * a.T_pad + i0) / 2;
-    uint64_t pol_q = 0, pol_dir = policy_evict_last();
+    const int out_row = b * a.T_cap + i0;
+    const uint32_t zero_tile = base + L.zero;
+    const bool zero_fill = a.zero_fill != 0;
+    uint64_t pol_q = 0;
+    const uint64_t pol_dir = policy_evict_last();
     if (lane == 0) {
       prefetch_tensormap(&tm0);
       prefetch_tensormap(&tm1);
@@ -192,10 +211,16 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
       v[u] = a.row0_up;
       ex[u] = 0.0f;
     }
-    uint32_t* dirs_lane = a.dirs + static_cast<size_t>(b) * a.M * a.T_alloc + i0 + 2 * lane;
+    uint32_t* dirs_ptr = a.dirs + static_cast<size_t>(b) * a.M * a.T_alloc + i0 + 2 * lane;
 
+    // Ring position of block m (slot, parity) and of the block refilled at
+    // its start (m + N - 1 goes into the slot block m - 1 used).
+    int slot = 0;
+    uint32_t par = 0;
+    int free_slot = N - 1;
     for (int m = 0; m < nblk; ++m) {
-      const int slot = m % N;
+      const int fs = m & (kFifoSlots - 1);
+      const uint32_t fpar = static_cast<uint32_t>(m >> 3) & 1u;
       if (m + N - 1 < nblk) {
         __syncwarp();
         if (lane == 0) {
@@ -203,20 +228,20 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
           // (generic proxy); order those reads before the async-proxy write.
           fence_proxy_async_smem();
           const int blk = m + N - 1;
-          const int s2 = blk % N;
-          const uint32_t bar = bar0 + 8u * s2;
-          const uint32_t dst = ring + static_cast<uint32_t>(s2 * kStageBytes);
+          const uint32_t bar = bar0 + 8u * free_slot;
+          const uint32_t dst = ring + static_cast<uint32_t>(free_slot * kStageBytes);
           mbar_arrive_expect_tx(bar, kStageBytes);
           tma_load_2d(dst, &tm0, blk * kStageCols, row_pair, bar, pol_q);
           tma_load_2d(dst + 4096u, &tm1, blk * kStageCols, row_pair, bar, pol_q);
         }
       }
-      mbar_wait(bar0 + 8u * slot, static_cast<uint32_t>((m / N) & 1));
+      mbar_wait(bar0 + 8u * slot, par);
 
       if (has_in) {
-        while (static_cast<int>(ld_acquire_cluster(my_head)) < m + 1) {
-        }
-        const float4* f = reinterpret_cast<const float4*>(my_fifo + (m % kFifoSlots) * 128);
+        // Producer's block m arrives as 128 bytes of st.async on full[fs].
+        if (lane == 0) mbar_arrive_expect_tx(my_full + 8u * fs, 128u);
+        mbar_wait(my_full + 8u * fs, fpar);
+        const float4* f = reinterpret_cast<const float4*>(my_fifo + fs * 128);
 #pragma unroll
         for (int q4 = 0; q4 < 8; ++q4) {
           const float4 x = f[q4];
@@ -225,8 +250,6 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
           v[4 * q4 + 2] = x.z;
           v[4 * q4 + 3] = x.w;
         }
-        __syncwarp();
-        if (lane == 0) st_release_cluster(prev_tail, static_cast<uint32_t>(m + 1));
       }
 
       const uint8_t* stage = ring_ptr + slot * kStageBytes;
@@ -243,20 +266,37 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
                                c_base, kStageCols, row0, mnv, row0_is_zero);
       }
       vprev = v[31];
+      if (has_in) {
+        // Every value read from slot fs has been consumed by the block above.
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote_relaxed(prev_empty + 8u * fs);
+      }
 
-      st_global_v2_evict_last(dirs_lane + static_cast<size_t>(m) * a.T_alloc, w0, w1, pol_dir);
+      st_global_v2_evict_last(dirs_ptr, w0, w1, pol_dir);
+      dirs_ptr += a.T_alloc;
 
       if (has_out && is31) {
-        while (static_cast<int>(ld_acquire_cluster(my_tail)) < m + 1 - kFifoSlots) {
-        }
-        const uint32_t dst = next_fifo + static_cast<uint32_t>((m % kFifoSlots) * 128);
+        // Slot fs of the consumer is free once it released block m - F.
+        if (m >= kFifoSlots) mbar_wait(my_empty + 8u * fs, fpar ^ 1u);
+        const uint32_t dst = next_fifo + static_cast<uint32_t>(fs * 128);
+        const uint32_t fbar = next_full + 8u * fs;
 #pragma unroll
         for (int q4 = 0; q4 < 8; ++q4)
-          st_cluster_v4(dst + 16u * q4, ex[4 * q4], ex[4 * q4 + 1], ex[4 * q4 + 2],
-                        ex[4 * q4 + 3]);
-        st_release_cluster(next_head, static_cast<uint32_t>(m + 1));
+          st_async_v4(dst + 16u * q4, ex[4 * q4], ex[4 * q4 + 1], ex[4 * q4 + 2], ex[4 * q4 + 3],
+                      fbar);
       }
+      if (zero_fill && lane == 0) {
+        // Fused zero fill of the output tile this warp covers (the backtrack
+        // scatters the ones later): one asynchronous TMA store of a zero
+        // tile, rows [i0, i0+64) x columns [32m, 32m+32), clipped by TMA.
+        tma_store_2d(&tm_out, zero_tile, c_base, out_row);
+      }
+
+      slot = slot + 1 == N ? 0 : slot + 1;
+      par ^= slot == 0 ? 1u : 0u;
+      free_slot = free_slot + 1 == N ? 0 : free_slot + 1;
     }
+    if (zero_fill && lane == 0) bulk_store_drain();
     __syncwarp();
 
     const bool bad = row0 < t_b && !(acc < INFINITY);
@@ -315,12 +355,12 @@ int fwd_max_active_clusters(int W, int N, int K, int mode) {
   return n;
 }
 
-cudaError_t launch_fwd(int mode, const CUtensorMap& tm0, const CUtensorMap& tm1, const FwdArgs& a,
-                       int B, cudaStream_t stream) {
+cudaError_t launch_fwd(int mode, const CUtensorMap& tm0, const CUtensorMap& tm1,
+                       const CUtensorMap& tm_out, const FwdArgs& a, int B, cudaStream_t stream) {
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = fwd_launch_config(B, a.K, a.W, a.N, stream, attr);
-  if (mode == 0) return cudaLaunchKernelEx(&cfg, mas_fwd_kernel<0>, tm0, tm1, a);
-  return cudaLaunchKernelEx(&cfg, mas_fwd_kernel<1>, tm0, tm1, a);
+  if (mode == 0) return cudaLaunchKernelEx(&cfg, mas_fwd_kernel<0>, tm0, tm1, tm_out, a);
+  return cudaLaunchKernelEx(&cfg, mas_fwd_kernel<1>, tm0, tm1, tm_out, a);
 }
 
 }  // namespace mas

@@ -31,23 +31,21 @@ struct FwdArgs {
   int N;                    // TMA stages per warp
   float mnv;                // max_neg_val
   float row0_up;            // value above row 0: mnv (parallel) / -inf (reference)
+  int zero_fill;            // 1: TMA-store zero tiles of the output (tm_out) as we go
+  int T_cap, S_cap;         // output shape
 };
 
 struct BtArgs {
   const uint32_t* lengths;  // [B][2]
   const uint32_t* dirs;     // [B][M][T_alloc]
-  int32_t* seg_map;         // [B][Kseg][T_alloc] pass-1 maps (row at segment start)
-  int32_t* seg_row;         // [B][Kseg + 1] pass-2 path rows at segment starts
-  uint8_t* out;             // [B][T_cap][S_cap] or null
-  int32_t* paths;           // [B][S_cap] or null
+  int32_t* path;            // [B][S_cap] int32 path rows, -1 past s_b, or null
+  uint8_t* out;             // [B][T_cap][S_cap] (already zero-filled) or null
   int B, T_cap, S_cap, M, T_alloc;
-  int L;                    // segment length in columns (multiple of 32)
-  int Kseg;                 // ceil(S_cap / L)
 };
 
 size_t fwd_smem_bytes(int W, int N);
-cudaError_t launch_fwd(int mode, const CUtensorMap& tm0, const CUtensorMap& tm1, const FwdArgs& a,
-                       int B, cudaStream_t stream);
+cudaError_t launch_fwd(int mode, const CUtensorMap& tm0, const CUtensorMap& tm1,
+                       const CUtensorMap& tm_out, const FwdArgs& a, int B, cudaStream_t stream);
 cudaError_t launch_backtrack(const BtArgs& a, cudaStream_t stream, int* launches);
 cudaError_t launch_locate_nonfinite(const float* q, int64_t row_pitch, int T_pad, int b, int t,
                                     int s, unsigned long long* d_result, cudaStream_t stream);

@@ -61,6 +61,20 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(policy)
       : "memory");
 }
+// 2-D tile store shared -> global (bulk-group completion), no L2 hint.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(c0), "r"(c1)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// Wait until every bulk store of this thread has finished reading shared
+// memory (the CTA may not exit before that).
+__device__ __forceinline__ void bulk_store_drain() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -86,16 +100,33 @@ __device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, f
                "f"(c), "f"(d)
                : "memory");
 }
-__device__ __forceinline__ void st_release_cluster(uint32_t addr, uint32_t v) {
-  asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+// Asynchronous 16-byte store into a (possibly remote) CTA's shared memory
+// that completes 16 bytes of transaction count on that CTA's mbarrier --
+// the boundary-row FIFO's data path (SASS: STAS.128).
+__device__ __forceinline__ void st_async_v4(uint32_t addr, float a, float b, float c, float d,
+                                            uint32_t remote_bar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+      "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(__float_as_uint(c)),
+      "r"(__float_as_uint(d)), "r"(remote_bar)
+      : "memory");
 }
-__device__ __forceinline__ uint32_t ld_acquire_cluster(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.acquire.cluster.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-  return v;
+// Relaxed arrive on a (possibly remote) mbarrier: no membar is emitted
+// (a .release.cluster arrive costs MEMBAR.ALL.GPU).  Callers issue it only
+// after every value read from the released buffer has been consumed.
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar)
+               : "memory");
 }
 
 // ---- misc -----------------------------------------------------------------
+// a > b as an all-ones / zero mask (FSET), so a bit can be merged into a
+// word with a single LOP3.
+__device__ __forceinline__ uint32_t gt_mask(float a, float b) {
+  uint32_t d;
+  asm("set.gt.u32.f32 %0, %1, %2;" : "=r"(d) : "f"(a), "f"(b));
+  return d;
+}
 // max.NaN over |a|, |b| folded into acc: acc turns NaN / +inf as soon as any
 // folded value is non-finite (one FMNMX3.NAN per two values on sm_100a).
 __device__ __forceinline__ void fold_abs_max_nan(float& acc, float a, float b) {
