@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libmonoalign_b200.so")
+LIB_PATH = os.environ.get("MAS_LIB_PATH") or os.path.join(_HERE, "_lib", "libmonoalign_b200.so")
 
 MAS_OK = 0
 MAS_E_VALIDATION = 1

@@ -182,19 +182,14 @@ bool encode_out_map(uint8_t* out, int64_t rows, int64_t S, CUtensorMap* m) {
   if (!enc) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(S)};
-  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(mas::kRowsPerWarp)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(mas::kStageCols),
+                             static_cast<cuuint32_t>(mas::kRowsPerWarp)};
   const cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, out, dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int num_sms() {
-  int dev = 0, n = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n;
-}
 
 struct Geometry {
   int W = 1, K = 1, N = 2, L = 256, Kseg = 1, T_alloc = 64, M = 1;
@@ -202,20 +197,22 @@ struct Geometry {
 
 bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
   const int warps = std::max(1, (t_max + mas::kRowsPerWarp - 1) / mas::kRowsPerWarp);
+  // One warp per SM sub-partition (4 per CTA), clusters of up to 16 CTAs;
+  // 6 warps x 2 stages for the longest texts.
+  const size_t budget = 220 * 1024;
   if (warps <= 4) {
     g->K = 1;
     g->W = warps;
-  } else if (warps <= 32) {
+  } else if (warps <= 4 * mas::kMaxClusterCtas) {
     g->W = 4;
     g->K = (warps + 3) / 4;
-  } else if (warps <= 8 * mas::kMaxClusterCtas) {
-    g->W = 8;
-    g->K = (warps + 7) / 8;
+  } else if (warps <= 6 * mas::kMaxClusterCtas) {
+    g->W = 6;
+    g->K = (warps + 5) / 6;
   } else {
     return false;
   }
-  const int sms = num_sms();
-  const size_t budget = (static_cast<int64_t>(B) * g->K <= sms) ? 220 * 1024 : 110 * 1024;
+  (void)B;
   int N = 8;
   while (N > 2 && mas::fwd_smem_bytes(g->W, N) > budget) --N;
   g->N = N;
@@ -328,7 +325,7 @@ int mas_plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t
   if (!choose_geometry(batch, std::max(t_max, 1), speech_cap, &p->geo)) {
     delete p;
     return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
-                     "text length above 8192 rows is not supported by the device path");
+                     "text length above 6144 rows is not supported by the device path");
   }
   const Geometry& g = p->geo;
   auto fail = [&](cudaError_t e, const char* what) {
@@ -406,6 +403,8 @@ int mas_plan_enqueue(mas_plan_t* p, const float* d_values, uint8_t* d_out, int32
   if (fused_zero && !encode_out_map(d_out, static_cast<int64_t>(p->B) * p->T, p->S, &tm_out))
     return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled(out) failed");
   fa.zero_fill = fused_zero ? 1 : 0;
+  fa.one = 1u;
+  fa.zero = 0.0f;
   fa.T_cap = p->T;
   fa.S_cap = p->S;
   MAS_CUDA(mas::launch_fwd(p->mode, tm0, tm1, tm_out, fa, p->B, stream), "launch mas_fwd");

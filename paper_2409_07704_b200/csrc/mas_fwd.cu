@@ -13,18 +13,26 @@
 //   * one thread-block cluster of K CTAs per item; CTA rank c, warp w owns
 //     the 64 text rows [64 g, 64 g + 64), g = c * W + w; lane k owns rows
 //     64 g + 2k and 64 g + 2k + 1 in registers (the running column);
-//   * speech columns are walked in order; the row above a lane's first row
-//     arrives by __shfl_sync from lane k-1, and for lane 0 from the previous
-//     warp through a 32-column-block FIFO in shared memory (DSMEM when the
-//     previous warp lives in another CTA of the cluster);
-//   * q is streamed per warp with TMA into an N-stage ring of 64 x 32 fp32
-//     tiles (128-byte swizzle, rows de-interleaved by parity so every
-//     LDS.128 is conflict-free), L2 evict_first; nothing else is read;
+//   * speech columns are walked in order, 64 per iteration; the row above a
+//     lane's first row arrives by __shfl_sync from lane k-1, and for lane 0
+//     from the previous warp through a FIFO of 64-column slots in shared
+//     memory, filled by the producer with st.async (DSMEM when the producer
+//     lives in another CTA of the cluster) and tracked by mbarriers;
+//   * q is streamed per warp with TMA into an N-stage ring of 64-row x
+//     64-column fp32 tiles (128-byte swizzle, rows de-interleaved by parity
+//     so every LDS.128 is conflict-free), L2 evict_first; nothing else is
+//     read;
 //   * direction words (one u32 per row per 32 columns) are written with
-//     L2 evict_last so the backtrack finds them in L2;
-//   * NonFinite validation (types.cpp:107-115) is fused: max.NaN over |q|
-//     per lane, one FMNMX3 per two cells; a flagged item is re-scanned
-//     exactly by the locator kernel on the error path only.
+//     L2 evict_last so the backtrack finds them in L2; the output's zero
+//     fill is issued alongside as asynchronous TMA stores of a zero tile;
+//   * NonFinite validation (types.cpp:107-115) is fused: an FFMA per cell
+//     folds q * 0 into a per-lane accumulator (NaN iff some q is inf/NaN);
+//     a flagged item is re-scanned exactly by the locator kernel on the
+//     error path only;
+//   * per step the ALU pipe (the bottleneck, 2 cycles per warp instruction
+//     per SM sub-partition) carries only FMNMX x2, FSETP x2 and the shuffle
+//     select; bit packing (predicated IMAD) and the NonFinite fold (FFMA) run
+//     on the FMA pipe next to the FADDs.
 #include "mas_kernels.h"
 #include "mas_ptx.cuh"
 
@@ -32,80 +40,158 @@ namespace mas {
 
 namespace {
 
+constexpr int kSubCols = 32;                            // columns per TMA box / dirs word
+constexpr int kSubBytes = kRowsPerWarp * kSubCols * 4;  // 8 KiB: [parity][32 rows][32 cols]
+constexpr int kSlotBytes = kStageCols * 4;              // one FIFO slot (64 floats)
+#ifndef MAS_L2_AHEAD
+#define MAS_L2_AHEAD 0
+#endif
+constexpr int kL2Ahead = MAS_L2_AHEAD;  // iterations of L2 prefetch beyond the smem ring
+
 struct SmemLayout {
-  uint32_t ring, bars, full, empty, fifo, zero, total;
+  uint32_t ring, bars, full, empty, sink, fifo, zero, total;
 };
 
 // Per CTA: W rings of N TMA stages, the TMA mbarriers, and per warp a
 // kFifoSlots-deep boundary-row FIFO with its "full" barriers (completed by
 // the producer's st.async bytes) and the "empty" barriers of the FIFO this
-// warp feeds (arrived remotely by its consumer).
+// warp feeds (arrived remotely by its consumer); plus one zero tile.
 __host__ __device__ inline SmemLayout smem_layout(int W, int N) {
   SmemLayout L;
   L.ring = 0;
   L.bars = static_cast<uint32_t>(W * N * kStageBytes);
   L.full = L.bars + static_cast<uint32_t>(W * N * 8);
   L.empty = L.full + static_cast<uint32_t>(W * kFifoSlots * 8);
-  L.fifo = (L.empty + static_cast<uint32_t>(W * kFifoSlots * 8) + 127u) & ~127u;
-  L.zero = L.fifo + static_cast<uint32_t>(W * kFifoSlots * 32 * 4);
-  L.total = L.zero + static_cast<uint32_t>(kRowsPerWarp * 32);
+  L.sink = L.empty + static_cast<uint32_t>(W * kFifoSlots * 8);  // st.async target of releases
+  L.fifo = (L.sink + static_cast<uint32_t>(W * 16) + 127u) & ~127u;
+  L.zero = L.fifo + static_cast<uint32_t>(W * kFifoSlots * kSlotBytes);
+  L.total = L.zero + static_cast<uint32_t>(kRowsPerWarp * kStageCols);
   return L;
 }
 
-// One 32-column block of the DP for one warp.  GENERIC handles column 0,
-// reference-engine masking (cells with c < i stay exactly max_neg_val,
-// reference.cpp:12-17, :30) and a partial last block; the steady-state
-// instantiation has none of those checks.
-template <int MODE, bool GENERIC>
-__device__ __forceinline__ void fwd_block(const uint8_t* __restrict__ stage,
-                                          const uint32_t (&coff)[8], const float (&v)[32],
-                                          float vprev, float (&ex)[32], float& o0, float& o1,
-                                          uint32_t& w0, uint32_t& w1, float& acc, bool is31,
-                                          int srclane, int c_base, int nvalid, int row0,
-                                          float mnv, bool row0_is_zero) {
+// Per-warp state of the running column.
+struct Lane {
+  float o0, o1;  // Q of the lane's two rows at the previous column
+  float acc;     // sum of q * 0: NaN iff a non-finite q was seen
+  float vlast;   // producer's bottom row at the previous column
+};
+
+// Four steps (one LDS.128 per row parity) of the DP for one warp.
+template <int MODE, bool GENERIC, int SUB, int A4>
+__device__ __forceinline__ bool fwd_group(const uint8_t* __restrict__ tile, const uint32_t (&coff)[8],
+                                         const float4* __restrict__ slot, float (&ex)[kStageCols],
+                                         Lane& L, uint32_t& w0, uint32_t& w1, bool is31,
+                                         int srclane, int c_base, int nvalid, int row0, float mnv,
+                                         bool row0_is_zero, uint32_t one, float zero) {
+  constexpr int ug = SUB * 32 + A4 * 4;  // step index within the iteration
+  if (GENERIC && ug >= nvalid) return false;
+  const float4 qa = *reinterpret_cast<const float4*>(tile + coff[A4]);
+  const float4 qb = *reinterpret_cast<const float4*>(tile + 4096 + coff[A4]);
+  const float4 vv = slot[ug / 4];  // producer's bottom row, columns c-1 .. c+2
+  const float qs0[4] = {qa.x, qa.y, qa.z, qa.w};
+  const float qs1[4] = {qb.x, qb.y, qb.z, qb.w};
+  const float bnds[4] = {L.vlast, vv.x, vv.y, vv.z};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (GENERIC && ug + e >= nvalid) return false;
+    const float q0 = qs0[e];
+    const float q1 = qs1[e];
+    // Lane 31 forwards the previous warp's bottom row (column c-1) to lane
+    // 0; every other lane forwards its own bottom row to lane k+1.
+    const float send = is31 ? bnds[e] : L.o1;
+    const float up = __shfl_sync(0xffffffffu, send, srclane);
+    switch (A4 * 4 + e) {  // compile-time bit position
+#define MAS_BITS(U)                          \
+  case U:                                    \
+    set_bit_if_gt<U>(w0, up, L.o0, one);     \
+    set_bit_if_gt<U>(w1, L.o0, L.o1, one);   \
+    break;
+      MAS_BITS(0) MAS_BITS(1) MAS_BITS(2) MAS_BITS(3) MAS_BITS(4) MAS_BITS(5) MAS_BITS(6)
+      MAS_BITS(7) MAS_BITS(8) MAS_BITS(9) MAS_BITS(10) MAS_BITS(11) MAS_BITS(12) MAS_BITS(13)
+      MAS_BITS(14) MAS_BITS(15) MAS_BITS(16) MAS_BITS(17) MAS_BITS(18) MAS_BITS(19)
+      MAS_BITS(20) MAS_BITS(21) MAS_BITS(22) MAS_BITS(23) MAS_BITS(24) MAS_BITS(25)
+      MAS_BITS(26) MAS_BITS(27) MAS_BITS(28) MAS_BITS(29) MAS_BITS(30) MAS_BITS(31)
+#undef MAS_BITS
+    }
+    float n0 = q0 + fmaxf(up, L.o0);  // bit(row0, c-1) = up > o0 above
+    float n1 = q1 + fmaxf(L.o0, L.o1);
+    if (GENERIC) {
+      const int c = c_base + ug + e;
+      if (MODE == 1) {
+        if (c < row0) n0 = mnv;
+        if (c < row0 + 1) n1 = mnv;
+      }
+      if (c == 0) {  // first column: parallel.cpp:73-75 / reference.cpp:16-24
+        n0 = row0_is_zero ? q0 : mnv;
+        n1 = mnv;
+      }
+    }
+    fold_nonfinite(L.acc, q0, zero);
+    fold_nonfinite(L.acc, q1, zero);
+    ex[ug + e] = n1;
+    L.o0 = n0;
+    L.o1 = n1;
+  }
+  L.vlast = vv.w;
+  return true;
+}
+
+// 32 columns (one TMA box, one direction word per row) of the DP for one
+// warp.  GENERIC handles column 0, reference-engine masking (cells with
+// c < i stay exactly max_neg_val, reference.cpp:12-17, :30) and a partial
+// last iteration; the steady-state instantiation has none of those checks.
+// Per step the ALU pipe carries FMNMX x2, FSETP x2 and the shuffle select,
+// the FMA pipe FADD x2, the bit IMADs and the NonFinite FFMAs.
+template <int MODE, bool GENERIC, int SUB>
+__device__ __forceinline__ void fwd_sub(const uint8_t* __restrict__ tile, const uint32_t (&coff)[8],
+                                        const float4* __restrict__ slot, float (&ex)[kStageCols],
+                                        Lane& L, uint32_t& w0, uint32_t& w1, bool is31,
+                                        int srclane, int c_base, int nvalid, int row0, float mnv,
+                                        bool row0_is_zero, uint32_t one, float zero) {
   w0 = 0u;
   w1 = 0u;
-#pragma unroll
-  for (int a4 = 0; a4 < 8; ++a4) {
-    if (GENERIC && a4 * 4 >= nvalid) return;
-    const float4 qa = *reinterpret_cast<const float4*>(stage + coff[a4]);
-    const float4 qb = *reinterpret_cast<const float4*>(stage + 4096 + coff[a4]);
-    const float qs0[4] = {qa.x, qa.y, qa.z, qa.w};
-    const float qs1[4] = {qb.x, qb.y, qb.z, qb.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int u = a4 * 4 + e;
-      if (GENERIC && u >= nvalid) return;
-      const float q0 = qs0[e];
-      const float q1 = qs1[e];
-      // Lane 31 forwards the previous warp's bottom row (column c-1) to lane
-      // 0; every other lane forwards its own bottom row to lane k+1.
-      const float bnd = (u == 0) ? vprev : v[u - 1];
-      const float send = is31 ? bnd : o1;
-      const float up = __shfl_sync(0xffffffffu, send, srclane);
-      const uint32_t p0 = gt_mask(up, o0);  // bit(row0, c-1)
-      const uint32_t p1 = gt_mask(o0, o1);  // bit(row1, c-1)
-      float n0 = q0 + fmaxf(up, o0);
-      float n1 = q1 + fmaxf(o0, o1);
-      if (GENERIC) {
-        const int c = c_base + u;
-        if (MODE == 1) {
-          if (c < row0) n0 = mnv;
-          if (c < row0 + 1) n1 = mnv;
-        }
-        if (c == 0) {  // first column: parallel.cpp:73-75 / reference.cpp:16-24
-          n0 = row0_is_zero ? q0 : mnv;
-          n1 = mnv;
-        }
-      }
-      w0 |= p0 & (1u << u);
-      w1 |= p1 & (1u << u);
-      fold_abs_max_nan(acc, q0, q1);
-      ex[u] = n1;
-      o0 = n0;
-      o1 = n1;
-    }
-  }
+#define MAS_GROUP(A)                                                                              \
+  if (!fwd_group<MODE, GENERIC, SUB, A>(tile, coff, slot, ex, L, w0, w1, is31, srclane, c_base, \
+                                        nvalid, row0, mnv, row0_is_zero, one, zero))            \
+    return;
+  MAS_GROUP(0) MAS_GROUP(1) MAS_GROUP(2) MAS_GROUP(3) MAS_GROUP(4) MAS_GROUP(5) MAS_GROUP(6)
+  MAS_GROUP(7)
+#undef MAS_GROUP
+}
+
+template <int MODE, bool GENERIC>
+__device__ __forceinline__ void fwd_iter(const uint8_t* stage, const uint32_t (&coff)[8],
+                                         const float4* slot, float (&ex)[kStageCols], Lane& L,
+                                         uint32_t (&w)[4], bool is31, int srclane, int c_base,
+                                         int nvalid, int row0, float mnv, bool row0_is_zero,
+                                         uint32_t one, float zero) {
+  w[2] = 0u;
+  w[3] = 0u;
+  fwd_sub<MODE, GENERIC, 0>(stage, coff, slot, ex, L, w[0], w[1], is31, srclane, c_base, nvalid,
+                            row0, mnv, row0_is_zero, one, zero);
+  fwd_sub<MODE, GENERIC, 1>(stage + kSubBytes, coff, slot, ex, L, w[2], w[3], is31, srclane,
+                            c_base, nvalid, row0, mnv, row0_is_zero, one, zero);
+}
+
+// L2 prefetch of a whole stage (no shared memory, no completion): issued
+// kL2Ahead iterations before the stage's TMA load so DRAM latency jitter is
+// absorbed by L2 instead of stalling the warp chain.
+__device__ __forceinline__ void prefetch_stage(const CUtensorMap* tm0, const CUtensorMap* tm1,
+                                               int col, int row_pair) {
+  tma_prefetch_2d(tm0, col, row_pair);
+  tma_prefetch_2d(tm1, col, row_pair);
+  tma_prefetch_2d(tm0, col + kSubCols, row_pair);
+  tma_prefetch_2d(tm1, col + kSubCols, row_pair);
+}
+
+__device__ __forceinline__ void issue_stage(uint32_t dst, uint32_t bar, const CUtensorMap* tm0,
+                                            const CUtensorMap* tm1, int col, int row_pair,
+                                            uint64_t pol) {
+  mbar_arrive_expect_tx(bar, kStageBytes);
+  tma_load_2d(dst, tm0, col, row_pair, bar, pol);
+  tma_load_2d(dst + 4096u, tm1, col, row_pair, bar, pol);
+  tma_load_2d(dst + kSubBytes, tm0, col + kSubCols, row_pair, bar, pol);
+  tma_load_2d(dst + kSubBytes + 4096u, tm1, col + kSubCols, row_pair, bar, pol);
 }
 
 template <int MODE>
@@ -118,7 +204,7 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
   uint8_t* const sbase = smem_raw + (base - raw);
   const int W = a.W;
   const int N = a.N;
-  const SmemLayout L = smem_layout(W, N);
+  const SmemLayout SL = smem_layout(W, N);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -128,10 +214,12 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
   const int i0 = g * kRowsPerWarp;
   const int t_b = static_cast<int>(a.lengths[2 * b]);
   const int s_b = static_cast<int>(a.lengths[2 * b + 1]);
+  const bool has_in = g > 0;
 
-  const uint32_t bar0 = base + L.bars + static_cast<uint32_t>(warp * N * 8);
-  const uint32_t my_full = base + L.full + static_cast<uint32_t>(warp * kFifoSlots * 8);
-  const uint32_t my_empty = base + L.empty + static_cast<uint32_t>(warp * kFifoSlots * 8);
+  const uint32_t bar0 = base + SL.bars + static_cast<uint32_t>(warp * N * 8);
+  const uint32_t my_full = base + SL.full + static_cast<uint32_t>(warp * kFifoSlots * 8);
+  const uint32_t my_empty = base + SL.empty + static_cast<uint32_t>(warp * kFifoSlots * 8);
+  uint8_t* const my_fifo = sbase + SL.fifo + warp * kFifoSlots * kSlotBytes;
   if (lane == 0) {
     for (int s = 0; s < N; ++s) mbar_init(bar0 + 8u * s, 1u);
     for (int s = 0; s < kFifoSlots; ++s) {
@@ -139,16 +227,21 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
       mbar_init(my_empty + 8u * s, 1u);
     }
   }
-  // A zeroed 64 x 32-byte tile, the TMA-store source of the fused output fill.
-  for (int k = threadIdx.x; k < kRowsPerWarp * 32 / 16; k += blockDim.x)
-    reinterpret_cast<uint4*>(sbase + L.zero)[k] = make_uint4(0u, 0u, 0u, 0u);
+  if (!has_in) {
+    // The first warp of an item has no producer: its FIFO permanently holds
+    // the value above row 0 (max_neg_val, or -inf for reference.cpp:20-24).
+    for (int k = lane; k < kFifoSlots * kStageCols; k += 32)
+      reinterpret_cast<float*>(my_fifo)[k] = a.row0_up;
+  }
+  // A zeroed 64 x 64-byte tile, the TMA-store source of the fused output fill.
+  for (int k = threadIdx.x; k < kRowsPerWarp * kStageCols / 16; k += blockDim.x)
+    reinterpret_cast<uint4*>(sbase + SL.zero)[k] = make_uint4(0u, 0u, 0u, 0u);
   fence_proxy_async_smem();
   fence_mbar_init();
   cluster_sync_all();  // every CTA's FIFO state exists before any remote access
 
   const bool live = i0 < t_b && s_b > 0;
   if (live) {
-    const bool has_in = g > 0;
     const bool has_out = i0 + kRowsPerWarp < t_b;
     int nw = warp + 1, nr = crank;
     if (nw == W) {
@@ -163,23 +256,24 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
     // FIFO endpoints: my consumer's slots + "full" barriers, my producer's
     // "empty" barriers (addresses in the cluster shared window).
     const uint32_t next_fifo =
-        has_out ? mapa(base + L.fifo + static_cast<uint32_t>(nw * kFifoSlots * 128), nr) : 0u;
+        has_out ? mapa(base + SL.fifo + static_cast<uint32_t>(nw * kFifoSlots * kSlotBytes), nr)
+                : 0u;
     const uint32_t next_full =
-        has_out ? mapa(base + L.full + static_cast<uint32_t>(nw * kFifoSlots * 8), nr) : 0u;
+        has_out ? mapa(base + SL.full + static_cast<uint32_t>(nw * kFifoSlots * 8), nr) : 0u;
     const uint32_t prev_empty =
-        has_in ? mapa(base + L.empty + static_cast<uint32_t>(pw * kFifoSlots * 8), pr) : 0u;
-    const uint8_t* my_fifo = sbase + L.fifo + warp * kFifoSlots * 128;
+        has_in ? mapa(base + SL.empty + static_cast<uint32_t>(pw * kFifoSlots * 8), pr) : 0u;
+    const uint32_t prev_sink = has_in ? mapa(base + SL.sink + static_cast<uint32_t>(pw * 16), pr) : 0u;
 
-    const uint32_t ring = base + L.ring + static_cast<uint32_t>(warp * N * kStageBytes);
-    const uint8_t* ring_ptr = sbase + L.ring + warp * N * kStageBytes;
+    const uint32_t ring = base + SL.ring + static_cast<uint32_t>(warp * N * kStageBytes);
+    const uint8_t* ring_ptr = sbase + SL.ring + warp * N * kStageBytes;
     uint32_t coff[8];
 #pragma unroll
     for (int a4 = 0; a4 < 8; ++a4) coff[a4] = lane * 128u + ((a4 ^ (lane & 7)) << 4);
 
-    const int nblk = (s_b + kStageCols - 1) / kStageCols;
+    const int nit = (s_b + kStageCols - 1) / kStageCols;
     const int row_pair = (b * a.T_pad + i0) / 2;
     const int out_row = b * a.T_cap + i0;
-    const uint32_t zero_tile = base + L.zero;
+    const uint32_t zero_tile = base + SL.zero;
     const bool zero_fill = a.zero_fill != 0;
     uint64_t pol_q = 0;
     const uint64_t pol_dir = policy_evict_last();
@@ -187,14 +281,12 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
       prefetch_tensormap(&tm0);
       prefetch_tensormap(&tm1);
       pol_q = policy_evict_first();
-      const int pro = nblk < N - 1 ? nblk : N - 1;
-      for (int blk = 0; blk < pro; ++blk) {
-        const uint32_t bar = bar0 + 8u * blk;
-        const uint32_t dst = ring + static_cast<uint32_t>(blk * kStageBytes);
-        mbar_arrive_expect_tx(bar, kStageBytes);
-        tma_load_2d(dst, &tm0, blk * kStageCols, row_pair, bar, pol_q);
-        tma_load_2d(dst + 4096u, &tm1, blk * kStageCols, row_pair, bar, pol_q);
-      }
+      const int pro = nit < N - 1 ? nit : N - 1;
+      for (int it = 0; it < pro; ++it)
+        issue_stage(ring + static_cast<uint32_t>(it * kStageBytes), bar0 + 8u * it, &tm0, &tm1,
+                    it * kStageCols, row_pair, pol_q);
+      const int pre = nit < N - 1 + kL2Ahead ? nit : N - 1 + kL2Ahead;
+      for (int it = pro; it < pre; ++it) prefetch_stage(&tm0, &tm1, it * kStageCols, row_pair);
     }
 
     const bool is31 = lane == 31;
@@ -202,93 +294,94 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
     const int row0 = i0 + 2 * lane;
     const bool row0_is_zero = row0 == 0;
     const float mnv = a.mnv;
-    float o0 = 0.0f, o1 = 0.0f, acc = 0.0f;
-    float vprev = a.row0_up;
-    float v[32];
-    float ex[32];
+    const uint32_t one = a.one;  // opaque constants (see set_bit_if_gt / fold_nonfinite)
+    const float zero = a.zero;
+    Lane L;
+    L.o0 = 0.0f;
+    L.o1 = 0.0f;
+    L.acc = 0.0f;
+    L.vlast = a.row0_up;
+    float ex[kStageCols];
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      v[u] = a.row0_up;
-      ex[u] = 0.0f;
-    }
+    for (int u = 0; u < kStageCols; ++u) ex[u] = 0.0f;
     uint32_t* dirs_ptr = a.dirs + static_cast<size_t>(b) * a.M * a.T_alloc + i0 + 2 * lane;
 
-    // Ring position of block m (slot, parity) and of the block refilled at
-    // its start (m + N - 1 goes into the slot block m - 1 used).
+    // Ring position of iteration m (slot, parity) and the slot refilled at
+    // its start (iteration m + N - 1 goes where iteration m - 1 was).
     int slot = 0;
     uint32_t par = 0;
     int free_slot = N - 1;
-    for (int m = 0; m < nblk; ++m) {
+    for (int m = 0; m < nit; ++m) {
       const int fs = m & (kFifoSlots - 1);
-      const uint32_t fpar = static_cast<uint32_t>(m >> 3) & 1u;
-      if (m + N - 1 < nblk) {
+      const uint32_t fpar = static_cast<uint32_t>(m / kFifoSlots) & 1u;
+      if (m + N - 1 < nit) {
         __syncwarp();
         if (lane == 0) {
-          // The slot being refilled was last read in block m-1 by every lane
-          // (generic proxy); order those reads before the async-proxy write.
+          // The slot being refilled was last read in iteration m-1 by every
+          // lane (generic proxy); order those reads before the async write.
           fence_proxy_async_smem();
-          const int blk = m + N - 1;
-          const uint32_t bar = bar0 + 8u * free_slot;
-          const uint32_t dst = ring + static_cast<uint32_t>(free_slot * kStageBytes);
-          mbar_arrive_expect_tx(bar, kStageBytes);
-          tma_load_2d(dst, &tm0, blk * kStageCols, row_pair, bar, pol_q);
-          tma_load_2d(dst + 4096u, &tm1, blk * kStageCols, row_pair, bar, pol_q);
+          issue_stage(ring + static_cast<uint32_t>(free_slot * kStageBytes), bar0 + 8u * free_slot,
+                      &tm0, &tm1, (m + N - 1) * kStageCols, row_pair, pol_q);
+          if (m + N - 1 + kL2Ahead < nit)
+            prefetch_stage(&tm0, &tm1, (m + N - 1 + kL2Ahead) * kStageCols, row_pair);
         }
+      }
+      if (has_in && lane == 0) {
+        // Producer's iteration m arrives as 256 bytes of st.async on full[fs].
+        mbar_arrive_expect_tx(my_full + 8u * fs, kSlotBytes);
       }
       mbar_wait(bar0 + 8u * slot, par);
-
-      if (has_in) {
-        // Producer's block m arrives as 128 bytes of st.async on full[fs].
-        if (lane == 0) mbar_arrive_expect_tx(my_full + 8u * fs, 128u);
-        mbar_wait(my_full + 8u * fs, fpar);
-        const float4* f = reinterpret_cast<const float4*>(my_fifo + fs * 128);
-#pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4) {
-          const float4 x = f[q4];
-          v[4 * q4 + 0] = x.x;
-          v[4 * q4 + 1] = x.y;
-          v[4 * q4 + 2] = x.z;
-          v[4 * q4 + 3] = x.w;
-        }
-      }
+      if (has_in) mbar_wait(my_full + 8u * fs, fpar);
 
       const uint8_t* stage = ring_ptr + slot * kStageBytes;
+      const float4* fslot = reinterpret_cast<const float4*>(my_fifo + fs * kSlotBytes);
       const int c_base = m * kStageCols;
       const int nvalid = s_b - c_base < kStageCols ? s_b - c_base : kStageCols;
-      uint32_t w0, w1;
+      uint32_t w[4];
       const bool generic =
           m == 0 || nvalid < kStageCols || (MODE == 1 && c_base < i0 + kRowsPerWarp - 1);
       if (generic) {
-        fwd_block<MODE, true>(stage, coff, v, vprev, ex, o0, o1, w0, w1, acc, is31, srclane,
-                              c_base, nvalid, row0, mnv, row0_is_zero);
+        fwd_iter<MODE, true>(stage, coff, fslot, ex, L, w, is31, srclane, c_base, nvalid, row0,
+                             mnv, row0_is_zero, one, zero);
       } else {
-        fwd_block<MODE, false>(stage, coff, v, vprev, ex, o0, o1, w0, w1, acc, is31, srclane,
-                               c_base, kStageCols, row0, mnv, row0_is_zero);
+        fwd_iter<MODE, false>(stage, coff, fslot, ex, L, w, is31, srclane, c_base, kStageCols,
+                              row0, mnv, row0_is_zero, one, zero);
       }
-      vprev = v[31];
       if (has_in) {
-        // Every value read from slot fs has been consumed by the block above.
+        // Every value read from slot fs has been consumed above.
         __syncwarp();
+#ifdef MAS_EMPTY_RELAXED
         if (lane == 0) mbar_arrive_remote_relaxed(prev_empty + 8u * fs);
+#else
+        // Release the slot with a 4-byte st.async that completes the
+        // producer's "empty" transaction (prompt, fence-free signalling).
+        if (lane == 0) st_async_b32(prev_sink, static_cast<uint32_t>(m), prev_empty + 8u * fs);
+#endif
       }
 
-      st_global_v2_evict_last(dirs_ptr, w0, w1, pol_dir);
-      dirs_ptr += a.T_alloc;
+      st_global_v2_evict_last(dirs_ptr, w[0], w[1], pol_dir);
+      if (2 * m + 1 < a.M) st_global_v2_evict_last(dirs_ptr + a.T_alloc, w[2], w[3], pol_dir);
+      dirs_ptr += 2 * static_cast<size_t>(a.T_alloc);
 
       if (has_out && is31) {
-        // Slot fs of the consumer is free once it released block m - F.
-        if (m >= kFifoSlots) mbar_wait(my_empty + 8u * fs, fpar ^ 1u);
-        const uint32_t dst = next_fifo + static_cast<uint32_t>(fs * 128);
+        // Slot fs of the consumer is free once it released iteration m - F.
+        if (m >= kFifoSlots) {
+#ifndef MAS_EMPTY_RELAXED
+          mbar_arrive_expect_tx(my_empty + 8u * fs, 4u);
+#endif
+          mbar_wait(my_empty + 8u * fs, fpar ^ 1u);
+        }
+        const uint32_t dst = next_fifo + static_cast<uint32_t>(fs * kSlotBytes);
         const uint32_t fbar = next_full + 8u * fs;
 #pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4)
+        for (int q4 = 0; q4 < kStageCols / 4; ++q4)
           st_async_v4(dst + 16u * q4, ex[4 * q4], ex[4 * q4 + 1], ex[4 * q4 + 2], ex[4 * q4 + 3],
                       fbar);
       }
       if (zero_fill && lane == 0) {
         // Fused zero fill of the output tile this warp covers (the backtrack
-        // scatters the ones later): one asynchronous TMA store of a zero
-        // tile, rows [i0, i0+64) x columns [32m, 32m+32), clipped by TMA.
+        // scatters the ones later): one asynchronous TMA store of the zero
+        // tile, rows [i0, i0+64) x columns [64m, 64m+64), clipped by TMA.
         tma_store_2d(&tm_out, zero_tile, c_base, out_row);
       }
 
@@ -299,7 +392,7 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
     if (zero_fill && lane == 0) bulk_store_drain();
     __syncwarp();
 
-    const bool bad = row0 < t_b && !(acc < INFINITY);
+    const bool bad = row0 < t_b && !(L.acc < INFINITY);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flags + b, 1);
   }
   __syncwarp();

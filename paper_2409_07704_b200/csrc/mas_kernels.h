@@ -13,9 +13,12 @@ namespace mas {
 // columns.
 constexpr int kRowsPerLane = 2;
 constexpr int kRowsPerWarp = 32 * kRowsPerLane;  // 64
-constexpr int kStageCols = 32;
-constexpr int kStageBytes = kRowsPerWarp * kStageCols * 4;  // 8 KiB
-constexpr int kFifoSlots = 8;  // boundary-row FIFO depth, in 32-column blocks
+constexpr int kStageCols = 64;                              // columns per iteration / TMA stage
+constexpr int kStageBytes = kRowsPerWarp * kStageCols * 4;  // 16 KiB
+#ifndef MAS_FIFO_SLOTS
+#define MAS_FIFO_SLOTS 8
+#endif
+constexpr int kFifoSlots = MAS_FIFO_SLOTS;  // boundary-row FIFO depth, in 64-column iterations
 constexpr int kMaxWarpsPerCta = 8;
 constexpr int kMaxClusterCtas = 16;
 
@@ -33,6 +36,8 @@ struct FwdArgs {
   float row0_up;            // value above row 0: mnv (parallel) / -inf (reference)
   int zero_fill;            // 1: TMA-store zero tiles of the output (tm_out) as we go
   int T_cap, S_cap;         // output shape
+  uint32_t one;             // 1 and 0.0f passed at run time so ptxas keeps the
+  float zero;               //   bit IMADs / NonFinite FFMAs on the FMA pipe
 };
 
 struct BtArgs {

@@ -75,6 +75,13 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
 __device__ __forceinline__ void bulk_store_drain() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+// TMA L2 prefetch of one box (no shared-memory destination).
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -111,11 +118,22 @@ __device__ __forceinline__ void st_async_v4(uint32_t addr, float a, float b, flo
       "r"(__float_as_uint(d)), "r"(remote_bar)
       : "memory");
 }
+__device__ __forceinline__ void st_async_b32(uint32_t addr, uint32_t v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                   addr),
+               "r"(v), "r"(remote_bar)
+               : "memory");
+}
 // Relaxed arrive on a (possibly remote) mbarrier: no membar is emitted
 // (a .release.cluster arrive costs MEMBAR.ALL.GPU).  Callers issue it only
 // after every value read from the released buffer has been consumed.
 __device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t remote_bar) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_remote_release(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar)
                : "memory");
 }
 
@@ -126,6 +144,20 @@ __device__ __forceinline__ uint32_t gt_mask(float a, float b) {
   uint32_t d;
   asm("set.gt.u32.f32 %0, %1, %2;" : "=r"(d) : "f"(a), "f"(b));
   return d;
+}
+// if (a > b) w += (1 << BIT), as a predicated IMAD so the bit packing runs on
+// the FMA pipe (the ALU pipe is the DP's bottleneck: FMNMX + FSETP).  `one`
+// must be an opaque register holding 1 (else ptxas turns it into IADD3).
+template <int BIT>
+__device__ __forceinline__ void set_bit_if_gt(uint32_t& w, float a, float b, uint32_t one) {
+  asm("{\n\t.reg .pred q;\n\tsetp.gt.f32 q, %1, %2;\n\t@q mad.lo.u32 %0, %3, %4, %0;\n\t}"
+      : "+r"(w)
+      : "f"(a), "f"(b), "r"(one), "n"(1u << BIT));
+}
+// acc = q * zero + acc on the FMA pipe (`zero` an opaque 0.0f): acc turns
+// NaN as soon as a folded q is inf or NaN (inf * 0 = NaN).
+__device__ __forceinline__ void fold_nonfinite(float& acc, float q, float zero) {
+  asm("fma.rn.f32 %0, %1, %2, %0;" : "+f"(acc) : "f"(q), "f"(zero));
 }
 // max.NaN over |a|, |b| folded into acc: acc turns NaN / +inf as soon as any
 // folded value is non-finite (one FMNMX3.NAN per two values on sm_100a).
