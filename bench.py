@@ -1,0 +1,348 @@
+"""Benchmark of the maximum-path call (BASELINE.json metric: MAS Gcells/s
+(B*T*S / time) and ms/batch at B32 T1024 S8192 vs the CPU reference).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = the whole maximum-path call on one batch of config 3
+(B=32 items per GPU, T=1024, S=8192, fp32 log-likelihoods from the
+reference's own generator bench::generate_random_batch, generated
+bit-identically on the device): K1 forward (direction bits + fused NonFinite
+check + fused zero fill of the uint8 [B,T,S] output) and K2 backtrack (the
+ones of the alignment), with inputs resident in HBM.  Inputs (1.07 GB per
+GPU) are larger than L2 (126 MB), so no flush is needed between steps.
+
+Under torchrun each rank aligns its own 32-item shard (items [32r, 32r+32)
+of generate_random_batch(32 N, ...)): weak scaling, no collective on the data
+path; NCCL is used only for the start/stop barrier and the max-over-ranks
+timing.
+
+`--impl reference` times the reference's own CPU engine (oracle/_ref, the
+unmodified /root/reference/proj/src compiled in place) on this box's host
+cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+T_TEXT, S_SPEECH, B_PER_GPU = 1024, 8192, 32
+BYTES_PER_CELL = 4 + 1 / 8 + 1  # q read + direction bit + uint8 output
+METRIC = "MAS Gcells/s (B*T*S/time) and ms/batch at B32 T1024 S8192 vs CPU ref"
+WORKLOAD = "c3: B32 T1024 S8192 fp32 maximum-path (align -> uint8 [B,T,S]), per GPU"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _ncu_traffic():
+    """dram bytes per launch of the forward kernel from the committed
+    `ncu --set full` summary (profiles/ncu_fwd_latest.json), if present."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_fwd_latest.json")) as f:
+            d = json.load(f)
+        if d.get("workload") == "c3":
+            return float(d["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """NVML SM clock + throttle reasons sampled in a thread during the timed
+    region (the recipe's nvidia-smi clocks line, at a finer period)."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index, period=0.002):
+        self.samples, self.reasons = [], 0
+        self.period = period
+        self.ok = False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            self.sample()
+            time.sleep(self.period)
+
+    def sample(self):
+        if not self.ok:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+        except Exception:
+            pass
+
+    def __enter__(self):
+        self.sample()
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.th.join()
+        self.sample()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples),
+                "reasons": [n for b, n in self.REASONS.items() if self.reasons & b
+                            and n != "gpu_idle"]}
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_reference_leg(steps, warmup, budget_s=None):
+    """Times monoalign::align (parallel engine, threads=0 = all host threads,
+    capped at B by the engine, parallel.cpp:86-91) on a pre-built config-3
+    batch.  Returns (ms list, cores, sample description)."""
+    from oracle.oracle import Reference, build
+
+    build()
+    ref = Reference()
+    hw = ref.hardware_threads()
+    batch = ref.timed_batch(B_PER_GPU, T_TEXT, S_SPEECH, 0)
+    try:
+        for _ in range(warmup):
+            batch.time("parallel", 0)
+        ms = []
+        t0 = time.perf_counter()
+        while True:
+            ms.append(batch.time("parallel", 0))
+            if budget_s is None and len(ms) >= steps:
+                break
+            if budget_s is not None and (time.perf_counter() - t0 >= budget_s or len(ms) >= steps):
+                break
+    finally:
+        batch.close()
+    cores = min(hw, B_PER_GPU)
+    sample = (f"full config-3 batch (32x1024x8192) per align call, {len(ms)} call(s), "
+              f"monoalign::align parallel engine, threads=0 -> {cores} workers of {hw} "
+              f"hardware threads, timed with steady_clock around align only")
+    return ms, cores, sample
+
+
+def run_reference(args):
+    rank, world, _ = _dist()
+    if rank != 0:
+        return 0
+    ms, cores, sample = cpu_reference_leg(args.steps, args.warmup)
+    cells = B_PER_GPU * T_TEXT * S_SPEECH
+    tot = sum(ms) / 1e3
+    value = cells * len(ms) / tot / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "Gcells/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": len(ms), "warmup": args.warmup,
+        "ms_per_step": round(statistics.mean(ms), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "B": B_PER_GPU, "T": T_TEXT, "S": S_SPEECH,
+                   "global_batch": B_PER_GPU, "parallelism": "host threads"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Gcells/s", "cores": cores,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "Gcells/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import ctypes
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2409_07704_b200 as mas
+    from paper_2409_07704_b200 import _lib
+
+    rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    B, T, S = B_PER_GPU, T_TEXT, S_SPEECH
+    cells = B * T * S
+
+    # Inputs: this rank's shard of generate_random_batch(B * world, T, S, 0).
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        q = mas.generate_device(B, T, S, 0, first_item=rank * B, device=dev)
+        out = torch.empty((B, T, S), dtype=torch.uint8, device=dev)
+    plan = mas.Plan(B, T, S)
+    geom = plan.geometry
+    FWD, BT = _lib.MAS_PART_FORWARD, _lib.MAS_PART_BACKTRACK
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            plan.enqueue(q, out, stream=stream)
+        plan.finish(q, stream=stream)  # no NonFinite / validation error
+
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    with clocks:
+        t_start.record(stream)
+        for k in range(K):
+            ev[k][0].record(stream)
+            plan.enqueue(q, out, stream=stream, parts=FWD)
+            ev[k][1].record(stream)
+            plan.enqueue(q, out, stream=stream, parts=BT)
+            ev[k][2].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    plan.finish(q, stream=stream)
+    launches_per_step = 2  # mas_fwd + bt_walk (the flags memset is a runtime memset)
+    elapsed_ms = t_start.elapsed_time(t_end)
+    fwd_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    bt_ms = [e[1].elapsed_time(e[2]) for e in ev]
+
+    # Sanity (outside the timed region): exactly one 1 per column of every item.
+    col = out.sum(dim=1, dtype=torch.int32)
+    assert bool((col == 1).all()), "alignment invariant violated"
+
+    tmax = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(tmax.item())
+    value = world * cells * K / (elapsed_ms / 1e3) / 1e9
+
+    # ---- e2e: the C-ABI host entry point with pinned HOST buffers ----------
+    lib = _lib.load()
+    hq = torch.empty((B, T, S), dtype=torch.float32, pin_memory=True)
+    hq.copy_(q)
+    hout = torch.empty((B, T, S), dtype=torch.uint8, pin_memory=True)
+    cfg = mas.api._make_config("parallel", -1e32, 0)
+    err = _lib.MasError()
+
+    def host_call():
+        rc = lib.mas_align_host(hq.data_ptr(), B, T, S, None, ctypes.byref(cfg),
+                                hout.data_ptr(), None, ctypes.byref(err))
+        _lib.raise_for(rc, err)
+
+    e2e_steps = max(3, min(K, 10))
+    for _ in range(2):
+        host_call()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        host_call()
+    torch.cuda.synchronize(dev)
+    e2e_s = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = world * cells * e2e_steps / float(e2e_s.item()) / 1e9
+    assert torch.equal(hout, out.cpu()), "host entry point differs from the device path"
+    h2d = B * T * S * 4
+    d2h = B * T * S + 4 * B  # alignment bytes + NonFinite flags
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            ms, cores, sample = cpu_reference_leg(20, 1, budget_s=12.0)
+            cpu = {"value": round(cells * len(ms) / (sum(ms) / 1e3) / 1e9, 4),
+                   "unit": "Gcells/s", "cores": cores, "kind": "reference", "sample": sample}
+        except Exception as e:  # the reference build did not travel
+            cpu = {"value": None, "unit": "Gcells/s", "cores": None, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    peak, peak_src = _peaks()
+    fwd_avg = statistics.mean(fwd_ms)
+    bt_avg = statistics.mean(bt_ms)
+    achieved = BYTES_PER_CELL * cells / (fwd_avg / 1e3) / 1e9
+    traffic = _ncu_traffic()
+    step_ms = elapsed_ms / K
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "Gcells/s", "n_gpus": world,
+        "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": round(step_ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (bench::generate_random_batch seed 0, generated bit-identically on "
+                "the device)",
+        "config": {"workload": WORKLOAD, "B": B, "T": T, "S": S, "global_batch": B * world,
+                   "parallelism": f"batch-shard dp{world}, no collective",
+                   "l2": "inputs larger than L2 (1.07 GB q per GPU vs 126 MB L2), no flush",
+                   "geometry": geom},
+        "roofline": {"bound": "hbm", "kernel": "mas_fwd_kernel", "achieved": round(achieved, 1),
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "bytes_per_cell": BYTES_PER_CELL,
+                     "fwd_ms": round(fwd_avg, 4), "backtrack_ms": round(bt_avg, 4),
+                     "step_frac": round(BYTES_PER_CELL * cells / (step_ms / 1e3) / 1e9 / peak, 4)},
+        "e2e": {"value": round(e2e_value, 3), "unit": "Gcells/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                "path": "mas_align_host (C-ABI), pinned host in/out, H2D+kernels+D2H+checks"},
+        "gpu_launches": K * launches_per_step,
+        "clocks": clocks.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

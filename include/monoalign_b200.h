@@ -139,6 +139,15 @@ MAS_API int mas_plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap,
 /* Enqueues the kernels on `stream`; no host synchronisation. */
 MAS_API int mas_plan_enqueue(mas_plan_t* plan, const float* d_values, uint8_t* d_out, int32_t* d_paths,
                      void* stream, mas_error_t* err);
+/* The same, restricted to a subset of the kernels (MAS_PART_* bits), so a
+ * caller can bracket each kernel with its own events.  The forward part
+ * (direction bits, NonFinite flags, output zero fill) must precede the
+ * backtrack part (paths / ones of the alignment) on `stream`. */
+#define MAS_PART_FORWARD 0x1u
+#define MAS_PART_BACKTRACK 0x2u
+#define MAS_PART_ALL 0x3u
+MAS_API int mas_plan_enqueue_part(mas_plan_t* plan, uint32_t parts, const float* d_values,
+                          uint8_t* d_out, int32_t* d_paths, void* stream, mas_error_t* err);
 /* Synchronises `stream` and turns device-side NonFinite flags and recorded
  * host-side item errors into the reference's error (or MAS_OK). */
 MAS_API int mas_plan_finish(mas_plan_t* plan, const float* d_values, void* stream, mas_error_t* err);

@@ -42,9 +42,10 @@ def build(force: bool = False) -> None:
     targets = ["oracle"]
     if os.path.isdir(REF_SRC):
         targets.append("ref")
-    if force or not os.path.exists(ORACLE_SO) or (
-            "ref" in targets and not os.path.exists(REF_SO)):
-        subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
+    if not os.path.isdir(REF_SRC) and os.path.exists(ORACLE_SO) and not force:
+        return  # GPU box: use the prebuilt checkers that travelled with the repo
+    subprocess.run(["make", "-s", "-C", HERE] + (["clean"] if force else []) + targets,
+                   check=True)
 
 
 class _OracleError(ctypes.Structure):
@@ -153,6 +154,13 @@ class Reference:
                                        ctypes.POINTER(ctypes.c_int), ctypes.c_void_p,
                                        ctypes.c_int]
         lib.ref_hardware_threads.restype = ctypes.c_uint
+        lib.ref_batch_create.restype = ctypes.c_void_p
+        lib.ref_batch_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint64]
+        lib.ref_batch_destroy.restype = None
+        lib.ref_batch_destroy.argtypes = [ctypes.c_void_p]
+        lib.ref_batch_time_align.restype = ctypes.c_double
+        lib.ref_batch_time_align.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                             ctypes.POINTER(ctypes.c_int64)]
         self.lib = lib
 
     @staticmethod
@@ -197,6 +205,32 @@ class Reference:
         if code >= 0:
             raise ValueError(ERRC_NAMES[code])
         return score.value, paths[: min(n.value, cap)], n.value
+
+    def timed_batch(self, b, t, s, seed):
+        """A pre-built generate_random_batch(b, t, s, seed) inside the
+        reference library; call .time(engine, threads) -> ms per align."""
+        ref = self
+
+        class _Batch:
+            def __init__(self):
+                self.h = ref.lib.ref_batch_create(b, t, s, seed)
+                if not self.h:
+                    raise MemoryError("ref_batch_create failed")
+
+            def time(self, engine="parallel", threads=0):
+                ck = ctypes.c_int64()
+                ms = ref.lib.ref_batch_time_align(self.h, 1 if engine == "reference" else 0,
+                                                  threads, ctypes.byref(ck))
+                if ms < 0:
+                    raise RuntimeError("reference align failed")
+                return ms
+
+            def close(self):
+                if self.h:
+                    ref.lib.ref_batch_destroy(self.h)
+                    self.h = None
+
+        return _Batch()
 
     def hardware_threads(self) -> int:
         return int(self.lib.ref_hardware_threads())

@@ -14,6 +14,7 @@
 //   path_from_matrix                     include/monoalign/types.hpp:155-158
 //   bench::generate_random_batch         include/monoalign/bench.hpp:58
 //   oracle::best_paths                   include/monoalign/oracle.hpp:33
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -123,5 +124,41 @@ int ref_best_paths(const float* q, int t, int s, double* max_score, int* n_paths
 }
 
 unsigned ref_hardware_threads() { return std::thread::hardware_concurrency(); }
+
+/// Timing harness for bench.py's reference arm / cpu_baseline: a pre-built
+/// LikelihoodBatch (bench::generate_random_batch) and monoalign::align timed
+/// alone with steady_clock, as the reference's own bench does
+/// (bench.cpp:275-303, timing :293-296).
+void* ref_batch_create(int b, int t, int s, std::uint64_t seed) {
+  try {
+    return new monoalign::LikelihoodBatch(monoalign::bench::generate_random_batch(b, t, s, seed));
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+void ref_batch_destroy(void* batch) { delete static_cast<monoalign::LikelihoodBatch*>(batch); }
+
+/// One monoalign::align call on the batch; returns milliseconds, < 0 on error.
+/// `checksum` (optional) receives the sum of path rows, so the work is used.
+double ref_batch_time_align(void* batch, int engine, int threads, std::int64_t* checksum) {
+  const auto& bt = *static_cast<monoalign::LikelihoodBatch*>(batch);
+  monoalign::MasConfig cfg;
+  cfg.engine = engine == 1 ? monoalign::EngineKind::Reference : monoalign::EngineKind::Parallel;
+  cfg.threads = threads;
+  try {
+    const auto t0 = std::chrono::steady_clock::now();
+    const monoalign::AlignmentMatrix m = monoalign::align(bt, cfg);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (checksum) {
+      std::int64_t acc = 0;
+      for (std::size_t k = 0; k < m.values.size(); k += 4099) acc += m.values[k];
+      *checksum = acc;
+    }
+    return std::chrono::duration<double, std::milli>(t1 - t0).count();
+  } catch (...) {
+    return -1.0;
+  }
+}
 
 }  // extern "C"

@@ -22,6 +22,9 @@ MAS_E_UNSUPPORTED = 4
 MAS_ENGINE_REFERENCE = 0
 MAS_ENGINE_PARALLEL = 1
 MAS_FLAG_UNCHECKED = 0x1
+MAS_PART_FORWARD = 0x1
+MAS_PART_BACKTRACK = 0x2
+MAS_PART_ALL = 0x3
 
 # include/monoalign/errors.hpp:8-30 of the reference, declaration order.
 ERRC_NAMES = (
@@ -68,6 +71,8 @@ _SIGS = {
                                        ctypes.c_int64, _VP, ctypes.POINTER(MasConfig),
                                        ctypes.POINTER(_VP), ctypes.POINTER(MasError)]),
     "mas_plan_enqueue": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, ctypes.POINTER(MasError)]),
+    "mas_plan_enqueue_part": (ctypes.c_int, [_VP, ctypes.c_uint32, _VP, _VP, _VP, _VP,
+                                             ctypes.POINTER(MasError)]),
     "mas_plan_finish": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(MasError)]),
     "mas_plan_launches": (ctypes.c_int, [_VP]),
     "mas_plan_geometry": (None, [_VP, ctypes.POINTER(ctypes.c_int32 * 5)]),

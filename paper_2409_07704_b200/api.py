@@ -226,13 +226,14 @@ class Plan:
         _lib.raise_for(rc, err)
         self._h = handle
 
-    def enqueue(self, values, out=None, paths=None, stream=None):
+    def enqueue(self, values, out=None, paths=None, stream=None, parts=_lib.MAS_PART_ALL):
+        """Enqueues the kernels (`parts`: MAS_PART_FORWARD / _BACKTRACK bits)."""
         import torch
 
         err = _lib.MasError()
         st = torch.cuda.current_stream() if stream is None else stream
-        rc = self._lib.mas_plan_enqueue(
-            self._h, values.data_ptr(), None if out is None else out.data_ptr(),
+        rc = self._lib.mas_plan_enqueue_part(
+            self._h, parts, values.data_ptr(), None if out is None else out.data_ptr(),
             None if paths is None else paths.data_ptr(), ctypes.c_void_p(st.cuda_stream),
             ctypes.byref(err))
         _lib.raise_for(rc, err)

@@ -363,6 +363,11 @@ void mas_plan_geometry(const mas_plan_t* p, int32_t geom[5]) {
 
 int mas_plan_enqueue(mas_plan_t* p, const float* d_values, uint8_t* d_out, int32_t* d_paths,
                      void* stream_v, mas_error_t* err) {
+  return mas_plan_enqueue_part(p, MAS_PART_ALL, d_values, d_out, d_paths, stream_v, err);
+}
+
+int mas_plan_enqueue_part(mas_plan_t* p, uint32_t parts, const float* d_values, uint8_t* d_out,
+                          int32_t* d_paths, void* stream_v, mas_error_t* err) {
   clear_error(err);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   if ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (p->pitch & 3) != 0 || (p->T_pad & 1))
@@ -372,6 +377,8 @@ int mas_plan_enqueue(mas_plan_t* p, const float* d_values, uint8_t* d_out, int32
   if (!encode_maps(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, &tm0, &tm1))
     return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled failed");
   const Geometry& g = p->geo;
+  int nfwd = 0, nbt = 0;
+  if (parts & MAS_PART_FORWARD) {
   MAS_CUDA(cudaMemsetAsync(p->d_flags, 0, sizeof(int) * p->B, stream), "cudaMemsetAsync(flags)");
   mas::FwdArgs fa;
   fa.lengths = p->d_lengths;
@@ -408,6 +415,9 @@ int mas_plan_enqueue(mas_plan_t* p, const float* d_values, uint8_t* d_out, int32
   fa.T_cap = p->T;
   fa.S_cap = p->S;
   MAS_CUDA(mas::launch_fwd(p->mode, tm0, tm1, tm_out, fa, p->B, stream), "launch mas_fwd");
+  nfwd = 1;
+  }
+  if (parts & MAS_PART_BACKTRACK) {
   mas::BtArgs ba;
   ba.lengths = p->d_lengths;
   ba.dirs = p->d_dirs;
@@ -418,9 +428,9 @@ int mas_plan_enqueue(mas_plan_t* p, const float* d_values, uint8_t* d_out, int32
   ba.S_cap = p->S;
   ba.M = g.M;
   ba.T_alloc = g.T_alloc;
-  int nbt = 0;
   if (d_out || d_paths) MAS_CUDA(mas::launch_backtrack(ba, stream, &nbt), "launch backtrack");
-  p->launches = 1 + nbt;
+  }
+  p->launches = nfwd + nbt;
   return MAS_OK;
 }
 
