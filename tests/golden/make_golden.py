@@ -195,7 +195,7 @@ def main():
     err("nonfinite_last", late)
     G["err_infeasible/q"] = np.zeros((1, 3, 2), np.float32)
     err("infeasible", G["err_infeasible/q"])
-    G["err_ragged/lengths"] = np.array([[40, 100], [0, 5], [50, 60]], np.int64)
+    G["err_ragged/lengths"] = np.array([[40, 100], [0, 5], [30, 60]], np.int64)
     err("ragged", base, G["err_ragged/lengths"])
     G["err_ragged2/lengths"] = np.array([[40, 100], [30, 20], [5, 0]], np.int64)
     err("ragged2", base, G["err_ragged2/lengths"])
