@@ -36,24 +36,26 @@ def _stale() -> bool:
     return any(os.path.exists(d) and os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Compiles the library (``out``; ``defines`` are extra -D macros for
+    experiment variants built next to the product library)."""
+    if out == LIB and not defines and not force and not _stale():
+        return out
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     cmd = [
         NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
         "-ccbin", HOST_CXX, "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC,
         "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
-        "-o", LIB,
-    ] + [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
+        "-o", out,
+    ] + [f"-D{d}" for d in defines] + [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc build of libmonoalign_b200.so failed")
     if verbose:
         sys.stderr.write(res.stderr)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

@@ -243,6 +243,7 @@ struct mas_plan {
   unsigned long long* d_locate = nullptr;
   int launches = 0;
   int device = 0;
+  int bt_rows = 64;       // backtrack window rows
 };
 
 extern "C" {
@@ -343,6 +344,11 @@ int mas_plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t
     return fail(e, "cudaMemcpy(lengths)");
   if ((e = cudaMalloc(&p->d_dirs, nB * g.M * g.T_alloc * sizeof(uint32_t))) != cudaSuccess)
     return fail(e, "cudaMalloc(dirs)");
+  static const int bt_rows_cap = [] {
+    const char* e = std::getenv("MAS_BT_ROWS");  // experiment override
+    return e ? std::max(16, std::min(256, std::atoi(e))) & ~15 : 256;
+  }();
+  p->bt_rows = std::min(bt_rows_cap, g.T_alloc);
   if ((e = cudaMalloc(&p->d_flags, nB * sizeof(int))) != cudaSuccess)
     return fail(e, "cudaMalloc(flags)");
   if ((e = cudaMalloc(&p->d_locate, sizeof(unsigned long long))) != cudaSuccess)
@@ -428,7 +434,9 @@ int mas_plan_enqueue_part(mas_plan_t* p, uint32_t parts, const float* d_values, 
   ba.S_cap = p->S;
   ba.M = g.M;
   ba.T_alloc = g.T_alloc;
-  if (d_out || d_paths) MAS_CUDA(mas::launch_backtrack(ba, stream, &nbt), "launch backtrack");
+  ba.R = p->bt_rows;
+  if (d_out || d_paths)
+    MAS_CUDA(mas::launch_backtrack(ba, stream, &nbt), "launch backtrack");
   }
   p->launches = nfwd + nbt;
   return MAS_OK;

@@ -7,136 +7,280 @@
 // followed by write_path (src/types.cpp:181-185) into a zeroed [T][S] byte
 // matrix (types.cpp:40-47).  Here the walk reads the forward kernel's
 // direction bits, bit(i, j) == (Q[i-1][j] > Q[i][j]), stored as one u32 per
-// row per 32 columns (word m of row i holds columns 32m-1 .. 32m+30).  The
+// row per 32 columns (word m of row i holds columns 32m-1 .. 32m+30, the
+// column at position p = column + 1 - 32m as bit 31 - p).  The
 // zero fill of the output happens in the forward kernel (or a memset for
 // ragged shapes), so this kernel only walks and scatters the ones:
 //
 //   one warp per item walks row to row rather than column to column --
-//   inside a 32-column word the next step down is a find-last-set-bit, so
-//   an item costs ~(t + s/32) dependent steps instead of s.  The window of
-//   direction words the walk can reach in a block (at most 32 rows per
-//   block) is prefetched kWinStages blocks ahead with cp.async; lane 0 walks
-//   with a one-row load lookahead; each finished 32-column block is expanded
-//   by the whole warp (popc of the exit mask) into path[] and the ones of
-//   the alignment matrix.
+//   inside a 32-column word the next step up is a find-last-set-bit, so an
+//   item costs ~(t + s/32) dependent steps instead of s.  Windows of
+//   direction words (8 words x up to 256 rows) are bulk-copied (TMA engine,
+//   cp.async.bulk) four stages ahead; lane 0 walks out of a register queue; each finished 256-column
+//   stage is expanded by the whole warp (popc of the exit masks) into
+//   path[] and the ones of the alignment matrix.
 #include <cstdio>
 #include <cstdlib>
 
 #include "mas_kernels.h"
+#include "mas_ptx.cuh"
 
 namespace mas {
 
 namespace {
 
-constexpr int kWinStages = 8;                      // blocks prefetched ahead
-constexpr int kWinWords = 9;                       // words per lane per stage
-constexpr int kWinRows = 32 * kWinWords;           // >= 32 * kWinStages + 1 rows
+constexpr int kBtStages = 4;   // ring depth (stages of direction words in flight)
+constexpr int kBtWords = 8;    // direction words per stage = 256 speech positions
+constexpr int kBtMaxRows = 256;  // rows per window (TMA box limit)
 
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
-               "r"(valid ? 4 : 0)
+// Window load of stage n: words [8n, 8n + 8) (those < M) of rows
+// [row0, row0 + R), as one bulk copy per word (a word's rows are contiguous
+// in the [B][M][T_alloc] layout), completing on `bar`.
+__device__ __forceinline__ void bt_issue(uint32_t dst, uint32_t bar, const uint32_t* item_dirs,
+                                         int row0, int n, int M, int T_alloc, int R) {
+  const int words = min(kBtWords, M - kBtWords * n);
+  const uint32_t wbytes = static_cast<uint32_t>(R * 4);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+               "r"(wbytes * static_cast<uint32_t>(words))
                : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// Prefetch block m's direction words for rows [base - kWinRows + 1, base]
-// into stage `st`: lane l copies rows base - l - 32 i.
-__device__ __forceinline__ void prefetch_window(uint32_t win_smem, int st, const uint32_t* src,
-                                                int T_alloc, int m, int base, int lane) {
-  if (m >= 0) {
-    const uint32_t* col = src + static_cast<size_t>(m) * T_alloc;
-#pragma unroll
-    for (int i = 0; i < kWinWords; ++i) {
-      const int idx = lane + 32 * i;
-      const int row = base - idx;
-      cp_async4(win_smem + static_cast<uint32_t>((st * kWinRows + idx) * 4),
-                col + (row >= 0 ? row : 0), row >= 0);
-    }
+  for (int k = 0; k < words; ++k) {
+    const uint32_t* src = item_dirs + static_cast<size_t>(kBtWords * n + k) * T_alloc + row0;
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            dst + static_cast<uint32_t>(k) * wbytes),
+        "l"(src), "r"(wbytes), "r"(bar)
+        : "memory");
   }
-  cp_async_commit();
+}
+// First row of a window that must contain row y and as many rows below it
+// as possible: 16-byte aligned source (rounded up, so y stays inside),
+// within [0, T_alloc - R].
+__device__ __forceinline__ int bt_row0(int y, int R, int T_alloc) {
+  return min((max(y - R + 1, 0) + 3) & ~3, T_alloc - R);
 }
 
-__global__ void __launch_bounds__(32) bt_walk_kernel(const BtArgs a) {
-  __shared__ uint32_t win[kWinStages * kWinRows];
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// K2: one CTA of two warps per item.
+//
+// Warp 0, lane 0 walks (backtrack.hpp:21-32, restated on direction bits).
+// Stage n covers direction words [8n, 8n+8), i.e. speech positions
+// [256n, 256n+256) (position P = column + 1); its words are bulk-copied
+// (cp.async.bulk) kBtStages ahead into a shared-memory ring, as a window of
+// R rows ending at the row the walk had reached when the copy was issued
+// (the walk only moves up).  Words are bit-reversed (position p is bit
+// 31 - p), so in word M at row y with allowed bits `lim` the last column
+// the path spends on row y is the lowest set bit h = x & -x of
+// x = w & lim: the step is LOP3 -> IADD -> LOP3 -> IMAD on the critical
+// path, no bit scan.  If there is none the walk moves on to word M - 1 on
+// the same row.  The words of rows y-1 .. y-3 are held in a register
+// queue (loaded three steps ahead); a word change exposes one load.  Per
+// word the walker records the row it entered on and the exit mask.
+//
+// Warp 1 expands finished stages from those records while the walk goes
+// on: the row of column j = P - 1 is the word's entry row minus the exits
+// at positions >= P, written to path[] (int32) and as the one of
+// out[b][row][j] (the zeros were written by the forward kernel's fused
+// fill or a memset; types.cpp:40-47 / :181-185).
+//
+// A window miss (the walk descending more than ~R - 35 rows within four
+// stages) re-centres the window with a synchronous reload.
+__global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
+  // Guard words in front: the queue may read up to 4 rows below row 0 and
+  // the next-word load one word (R rows) before the stage's first word.
+  constexpr int kGuard = kBtMaxRows + 32;
+  __shared__ alignas(128) uint32_t win_raw[kGuard + kBtStages * kBtWords * kBtMaxRows];
+  __shared__ alignas(8) uint64_t bars[3 * kBtStages];  // full | done | free
+  __shared__ int rec_y[kBtStages][kBtWords];
+  __shared__ uint32_t rec_ex[kBtStages][kBtWords];
+  __shared__ int s_ylo[kBtStages];
   const int b = blockIdx.x;
-  const int lane = threadIdx.x;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int t = static_cast<int>(a.lengths[2 * b]);
   const int s = static_cast<int>(a.lengths[2 * b + 1]);
+  const int R = a.R;
+  const int M = a.M, T_alloc = a.T_alloc;
+  const uint32_t win_s = static_cast<uint32_t>(__cvta_generic_to_shared(win_raw + kGuard));
+  const uint32_t full_s = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+  const uint32_t done_s = full_s + 8u * kBtStages;
+  const uint32_t free_s = done_s + 8u * kBtStages;
+  constexpr uint32_t kSlotBytes = kBtWords * kBtMaxRows * 4;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 3 * kBtStages; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full_s + 8u * k) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // Everything below reads the forward kernel's direction bits or writes
+  // after its zero fill (programmatic dependent launch).
+#ifndef MAS_BT_NO_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+  if (t <= 0 || s <= 0) {
+    int32_t* path = a.path ? a.path + static_cast<size_t>(b) * a.S_cap : nullptr;
+    if (path)
+      for (int j = threadIdx.x; j < a.S_cap; j += 64) path[j] = -1;
+    return;
+  }
+  const int n_top = (s - 1) >> 8;
+
+  if (warp == 0) {
+    if (lane != 0 || s == 1) return;
+    const uint32_t* dirs = a.dirs + static_cast<size_t>(b) * M * T_alloc;
+    const uint32_t wstride = static_cast<uint32_t>(R * 4);  // next word, same row
+    int y = t - 1;
+    int Mg = (s - 1) >> 5;  // current word
+    // allowed (bit-reversed) bits of the current word: positions <= P
+    uint32_t lim = 0xffffffffu << (31 - ((s - 1) & 31));
+    if (Mg == 0) lim &= 0x7fffffffu;  // position 0 of word 0 is column -1
+    uint32_t ph_full = 0, ph_free = 0, pend = 0;
+    for (int k = 0; k < kBtStages && n_top - k >= 0; ++k) {
+      const int n = n_top - k, slot = n & (kBtStages - 1);
+      s_ylo[slot] = bt_row0(y, R, T_alloc);
+      bt_issue(win_s + slot * kSlotBytes, full_s + 8u * slot, dirs, s_ylo[slot], n, M, T_alloc,
+               R);
+      pend |= 1u << slot;
+    }
+    for (int n = n_top; n >= 0; --n) {
+      const int slot = n & (kBtStages - 1);
+      if (n + kBtStages <= n_top) {  // records of stage n + kBtStages expanded?
+        mbar_wait(free_s + 8u * slot, (ph_free >> slot) & 1u);
+        ph_free ^= 1u << slot;
+      }
+      int ml = Mg - kBtWords * n;  // first word of this stage to walk
+      for (int k = kBtWords - 1; k > ml; --k) {  // above the item's last column
+        rec_y[slot][k] = y;
+        rec_ex[slot][k] = 0u;
+      }
+      if (y > 0) {
+        if (pend & (1u << slot)) {
+          mbar_wait(full_s + 8u * slot, (ph_full >> slot) & 1u);
+          ph_full ^= 1u << slot;
+          pend &= ~(1u << slot);
+        }
+        const uint32_t slot_base = win_s + slot * kSlotBytes;
+        int ylo = s_ylo[slot];
+        // pw: address of (word ml, row y); p1: (word ml, row 1)
+        uint32_t pw = slot_base + static_cast<uint32_t>((ml * R + (y - ylo)) * 4);
+        uint32_t p1 = pw - static_cast<uint32_t>((y - 1) * 4);
+        uint32_t c0 = lds32(pw);
+        while (true) {  // one direction word per pass; c0 = word at (ml, y)
+          // The window must hold rows y-35 .. y: a word has at most 32
+          // exits and the queue reads three rows ahead.
+          if (y - 35 < ylo && ylo > 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            ylo = bt_row0(y, R, T_alloc);
+            s_ylo[slot] = ylo;
+            bt_issue(slot_base, full_s + 8u * slot, dirs, ylo, n, M, T_alloc, R);
+            mbar_wait(full_s + 8u * slot, (ph_full >> slot) & 1u);
+            ph_full ^= 1u << slot;
+            pw = slot_base + static_cast<uint32_t>((ml * R + (y - ylo)) * 4);
+            p1 = pw - static_cast<uint32_t>((y - 1) * 4);
+            c0 = lds32(pw);
+          }
+          rec_y[slot][ml] = y;
+          uint32_t c1 = lds32(pw - 4), c2 = lds32(pw - 8), c3 = lds32(pw - 12);
+          uint32_t exw = 0u;
+          const uint32_t pw_entry = pw;
+          uint32_t h;
+#define MAS_BT_STEP(C)                                   \
+  {                                                      \
+    const uint32_t x = (C) & lim;                        \
+    h = x & (0u - x);                                    \
+    if (static_cast<int>(h) <= 0 || pw == p1) break;     \
+    exw |= h;                                            \
+    lim = h * 0xfffffffeu; /* bits above h */            \
+    pw -= 4u;                                            \
+    (C) = lds32(pw - 12u);                               \
+  }
+          while (true) {
+            MAS_BT_STEP(c0) MAS_BT_STEP(c1) MAS_BT_STEP(c2) MAS_BT_STEP(c3)
+          }
+#undef MAS_BT_STEP
+          y -= static_cast<int>((pw_entry - pw) >> 2);
+          pw -= wstride;
+          p1 -= wstride;
+          if (h != 0u) {  // exit at the word's first position, or at row 1
+            exw |= h;
+            --y;
+            pw -= 4u;
+          }
+          c0 = lds32(pw);
+          rec_ex[slot][ml] = exw;
+          --Mg;
+          lim = Mg == 0 ? 0x7fffffffu : 0xffffffffu;
+          --ml;
+          if (y == 0 || ml < 0) break;
+        }
+      }
+      for (; ml >= 0; --ml) {  // the walk reached row 0: the rest stays there
+        rec_y[slot][ml] = 0;
+        rec_ex[slot][ml] = 0u;
+      }
+      Mg = kBtWords * n - 1;  // next stage starts at its top word
+      mbar_arrive_local(done_s + 8u * slot);
+      if (n - kBtStages >= 0 && y > 0) {
+        // the slot's words were consumed above: refill it with stage
+        // n - kBtStages, windowed at the walk's current row
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        s_ylo[slot] = bt_row0(y, R, T_alloc);
+        bt_issue(win_s + slot * kSlotBytes, full_s + 8u * slot, dirs, s_ylo[slot], n - kBtStages,
+                 M, T_alloc, R);
+        pend |= 1u << slot;
+      }
+    }
+    for (int k = 0; k < kBtStages; ++k)  // no copy may still be writing our smem
+      if (pend & (1u << k)) mbar_wait(full_s + 8u * k, (ph_full >> k) & 1u);
+    return;
+  }
+
+  // ---- warp 1: expansion ----------------------------------------------------
   int32_t* path = a.path ? a.path + static_cast<size_t>(b) * a.S_cap : nullptr;
   uint8_t* out = a.out ? a.out + static_cast<size_t>(b) * a.T_cap * a.S_cap : nullptr;
   if (path)
-    for (int j = (s > 0 ? s : 0) + lane; j < a.S_cap; j += 32) path[j] = -1;
-  if (t <= 0 || s <= 0) return;
-  const uint32_t* src = a.dirs + static_cast<size_t>(b) * a.M * a.T_alloc;
-  const uint32_t win_smem = static_cast<uint32_t>(__cvta_generic_to_shared(win));
-
-  int cur = t - 1;
+    for (int j = s + lane; j < a.S_cap; j += 32) path[j] = -1;
   if (lane == 0) {  // backtrack.hpp:23-24
-    if (path) path[s - 1] = cur;
-    if (out) out[static_cast<size_t>(cur) * a.S_cap + s - 1] = 1;
+    if (path) path[s - 1] = t - 1;
+    if (out) out[static_cast<size_t>(t - 1) * a.S_cap + s - 1] = 1;
   }
-  // Column j's bit sits at position p = j + 1; the walk covers p = s-1 .. 1.
-  const int mtop = (s - 1) >> 5;
-  int base[kWinStages];
+  if (s == 1) return;
+  uint32_t ph_done = 0;
+  for (int n = n_top; n >= 0; --n) {
+    const int slot = n & (kBtStages - 1);
+    mbar_wait(done_s + 8u * slot, (ph_done >> slot) & 1u);
+    ph_done ^= 1u << slot;
+    int ry[kBtWords];
+    uint32_t rx[kBtWords];
 #pragma unroll
-  for (int i = 0; i < kWinStages; ++i) {
-    base[i] = cur;
-    prefetch_window(win_smem, (mtop - i) & (kWinStages - 1), src, a.T_alloc, mtop - i, cur, lane);
-  }
-  for (int m = mtop; m >= 0; --m) {
-    const int st = m & (kWinStages - 1);
-    cp_async_wait<kWinStages - 1>();
-    __syncwarp();
-    const int wb = base[0];
-    const int p_top = (m == mtop) ? ((s - 1) & 31) : 31;
-    const int p_min = (m == 0) ? 1 : 0;
-    uint32_t ex = 0;
-    int y = cur;
-    if (lane == 0 && y > 0 && p_top >= p_min) {
-      const uint32_t* w_st = win + st * kWinRows + wb;  // row y at w_st[-y]
-      const uint32_t lo_mask = (m == 0) ? ~1u : ~0u;
-      int p = p_top;
-      uint32_t w = w_st[-y];
-      while (true) {
-        const uint32_t w_next = w_st[-(y - 1)];  // lookahead: the next row is always y-1
-        const uint32_t hit = w & lo_mask & (0xffffffffu >> (31 - p));
-        if (hit == 0u) break;
-        const int e = 31 - __clz(hit);
-        ex |= 1u << e;
-        --y;
-        p = e - 1;
-        if (y == 0 || p < p_min) break;
-        w = w_next;
-      }
+    for (int i = 0; i < kBtWords; ++i) {
+      ry[i] = rec_y[slot][i];
+      rx[i] = rec_ex[slot][i];
     }
-    ex = __shfl_sync(0xffffffffu, ex, 0);
-    const int cur_top = cur;
-    cur = __shfl_sync(0xffffffffu, y, 0);
-#pragma unroll
-    for (int i = 0; i < kWinStages - 1; ++i) base[i] = base[i + 1];
-    base[kWinStages - 1] = cur;
     __syncwarp();
-    prefetch_window(win_smem, st, src, a.T_alloc, m - kWinStages, cur, lane);
-    // Expand the block: column 32m + u - 1 (position u) sits at row
-    // cur_top - #exits at positions >= u.
-    const int u = lane;
-    if (u >= p_min && u <= p_top) {
-      const int col = 32 * m + u - 1;
-      const int row = cur_top - __popc(ex >> u);
-      if (path) path[col] = row;
-      if (out) out[static_cast<size_t>(row) * a.S_cap + col] = 1;
+    if (lane == 0) mbar_arrive_local(free_s + 8u * slot);
+#pragma unroll
+    for (int i = 0; i < kBtWords; ++i) {
+      const int j = 256 * n + 32 * i + lane - 1;
+      if (j >= 0 && j <= s - 2) {
+        // exits at positions >= lane are bits <= 31 - lane
+        const int row = ry[i] - __popc(rx[i] << lane);
+        if (path) path[j] = row;
+        if (out) out[static_cast<size_t>(row) * a.S_cap + j] = 1;
+      }
     }
   }
 }
 
 // Reference-order serial walk, one thread per item -- kept as a
-// cross-check (MAS_BT_SERIAL=1) for the segmented kernels.
+// cross-check (MAS_BT_SERIAL=1) for the windowed walker.
 __global__ void bt_serial_kernel(const BtArgs a) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.B) return;
@@ -153,7 +297,7 @@ __global__ void bt_serial_kernel(const BtArgs a) {
     if (cur > 0) {
       const int p = j + 1;
       const uint32_t w = src[static_cast<size_t>(p >> 5) * a.T_alloc + cur];
-      if ((w >> (p & 31)) & 1u) --cur;
+      if ((w >> (31 - (p & 31))) & 1u) --cur;
     }
     if (out) out[static_cast<size_t>(cur) * a.S_cap + j] = 1;
     if (prow) prow[j] = cur;
@@ -227,9 +371,24 @@ cudaError_t launch_backtrack(const BtArgs& a, cudaStream_t stream, int* launches
     if (launches) *launches = 2;
     return cudaGetLastError();
   }
-  bt_walk_kernel<<<a.B, 32, 0, stream>>>(a);
+  // Programmatic dependent launch: the walkers' prologue overlaps the tail
+  // of the forward kernel; griddepcontrol.wait orders every data access.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(a.B), 1, 1);
+  cfg.blockDim = dim3(64, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+#ifdef MAS_BT_NO_PDL
+  cfg.numAttrs = 0;
+#else
+  cfg.numAttrs = 1;
+#endif
   if (launches) *launches = 1;
-  return cudaGetLastError();
+  return cudaLaunchKernelEx(&cfg, bt_walk_kernel, a);
 }
 
 cudaError_t bt_configure(int /*T_alloc*/, int /*L*/) { return cudaSuccess; }

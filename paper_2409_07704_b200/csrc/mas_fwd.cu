@@ -22,7 +22,8 @@
 //     64-column fp32 tiles (128-byte swizzle, rows de-interleaved by parity
 //     so every LDS.128 is conflict-free), L2 evict_first; nothing else is
 //     read;
-//   * direction words (one u32 per row per 32 columns) are written with
+//   * direction words (one u32 per row per 32 columns, bit-reversed: the
+//     bit of column 32m + p - 1 is bit 31 - p of word m) are written with
 //     L2 evict_last so the backtrack finds them in L2; the output's zero
 //     fill is issued alongside as asynchronous TMA stores of a zero tile;
 //   * NonFinite validation (types.cpp:107-115) is fused: an FFMA per cell
@@ -103,8 +104,8 @@ __device__ __forceinline__ bool fwd_group(const uint8_t* __restrict__ tile, cons
     switch (A4 * 4 + e) {  // compile-time bit position
 #define MAS_BITS(U)                          \
   case U:                                    \
-    set_bit_if_gt<U>(w0, up, L.o0, one);     \
-    set_bit_if_gt<U>(w1, L.o0, L.o1, one);   \
+    set_bit_if_gt<31 - U>(w0, up, L.o0, one); \
+    set_bit_if_gt<31 - U>(w1, L.o0, L.o1, one); \
     break;
       MAS_BITS(0) MAS_BITS(1) MAS_BITS(2) MAS_BITS(3) MAS_BITS(4) MAS_BITS(5) MAS_BITS(6)
       MAS_BITS(7) MAS_BITS(8) MAS_BITS(9) MAS_BITS(10) MAS_BITS(11) MAS_BITS(12) MAS_BITS(13)
@@ -239,6 +240,10 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
   fence_proxy_async_smem();
   fence_mbar_init();
   cluster_sync_all();  // every CTA's FIFO state exists before any remote access
+  // Let the backtrack grid (programmatic dependent launch) get resident on
+  // the SMs this grid leaves idle; it waits for our completion before it
+  // touches any data (griddepcontrol.wait).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   const bool live = i0 < t_b && s_b > 0;
   if (live) {

@@ -46,6 +46,7 @@ struct BtArgs {
   int32_t* path;            // [B][S_cap] int32 path rows, -1 past s_b, or null
   uint8_t* out;             // [B][T_cap][S_cap] (already zero-filled) or null
   int B, T_cap, S_cap, M, T_alloc;
+  int R;                    // rows per backtrack window (<= 256, <= T_alloc)
 };
 
 size_t fwd_smem_bytes(int W, int N);
