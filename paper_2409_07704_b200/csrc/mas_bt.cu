@@ -64,6 +64,14 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
   return v;
 }
+// A shared load ptxas keeps in program order (ld.volatile): the walker's
+// queue loads must be issued where they are written, three steps before
+// their use, not sunk to the loop back-edge.
+__device__ __forceinline__ uint32_t lds32_v(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
 __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -76,13 +84,16 @@ __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
 // (cp.async.bulk) kBtStages ahead into a shared-memory ring, as a window of
 // R rows ending at the row the walk had reached when the copy was issued
 // (the walk only moves up).  Words are bit-reversed (position p is bit
-// 31 - p), so in word M at row y with allowed bits `lim` the last column
-// the path spends on row y is the lowest set bit h = x & -x of
-// x = w & lim: the step is LOP3 -> IADD -> LOP3 -> IMAD on the critical
-// path, no bit scan.  If there is none the walk moves on to word M - 1 on
-// the same row.  The words of rows y-1 .. y-3 are held in a register
-// queue (loaded three steps ahead); a word change exposes one load.  Per
-// word the walker records the row it entered on and the exit mask.
+// 31 - p), so in word M at row y, with x = the row's word restricted to
+// the positions the walk may still take, the last column the path spends
+// on row y is the lowest set bit of x.  With d = x - 1 the next row's x is
+// next & ~(x ^ d): a step is IADD -> LOP3 on the critical path, no bit
+// scan and no branch -- once x has no bit left it stays 0, and an exit at
+// position 0 leaves x = 0 too -- so steps run in branch-free blocks of
+// four, the rows come from a four-deep register queue, and the row the
+// walk reaches is y - popc(exits).  The forward kernel stores row 0 and
+// column -1 as zero bits, so the walk needs no bounds checks.  Per word the
+// walker records the row it entered on and the exit mask.
 //
 // Warp 1 expands finished stages from those records while the walk goes
 // on: the row of column j = P - 1 is the word's entry row minus the exits
@@ -93,14 +104,14 @@ __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
 // A window miss (the walk descending more than ~R - 35 rows within four
 // stages) re-centres the window with a synchronous reload.
 __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
-  // Guard words in front: the queue may read up to 4 rows below row 0 and
-  // the next-word load one word (R rows) before the stage's first word.
-  constexpr int kGuard = kBtMaxRows + 32;
+  // Guard words in front: a block may read up to 8 rows below row 0.
+  constexpr int kGuard = 32;
   __shared__ alignas(128) uint32_t win_raw[kGuard + kBtStages * kBtWords * kBtMaxRows];
   __shared__ alignas(8) uint64_t bars[3 * kBtStages];  // full | done | free
   __shared__ int rec_y[kBtStages][kBtWords];
   __shared__ uint32_t rec_ex[kBtStages][kBtWords];
   __shared__ int s_ylo[kBtStages];
+  __shared__ int rec_yend[kBtStages];
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -132,16 +143,23 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
   }
   const int n_top = (s - 1) >> 8;
 
+  const uint32_t* dirs = a.dirs + static_cast<size_t>(b) * M * T_alloc;
   if (warp == 0) {
     if (lane != 0 || s == 1) return;
-    const uint32_t* dirs = a.dirs + static_cast<size_t>(b) * M * T_alloc;
     const uint32_t wstride = static_cast<uint32_t>(R * 4);  // next word, same row
     int y = t - 1;
     int Mg = (s - 1) >> 5;  // current word
-    // allowed (bit-reversed) bits of the current word: positions <= P
+    // allowed (bit-reversed) bits of the item's last word: positions <= P
     uint32_t lim = 0xffffffffu << (31 - ((s - 1) & 31));
-    if (Mg == 0) lim &= 0x7fffffffu;  // position 0 of word 0 is column -1
     uint32_t ph_full = 0, ph_free = 0, pend = 0;
+#ifdef MAS_BT_PROFILE
+    long long pr_t0 = clock64(), pr_free = 0, pr_full = 0, pr_recenter = 0, pr_words = 0;
+    __shared__ unsigned pr_ts[300];
+    __shared__ unsigned char pr_ex[300];
+#define PR_T(v) long long v = clock64()
+#else
+#define PR_T(v)
+#endif
     for (int k = 0; k < kBtStages && n_top - k >= 0; ++k) {
       const int n = n_top - k, slot = n & (kBtStages - 1);
       s_ylo[slot] = bt_row0(y, R, T_alloc);
@@ -152,8 +170,12 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
     for (int n = n_top; n >= 0; --n) {
       const int slot = n & (kBtStages - 1);
       if (n + kBtStages <= n_top) {  // records of stage n + kBtStages expanded?
+        PR_T(a0);
         mbar_wait(free_s + 8u * slot, (ph_free >> slot) & 1u);
         ph_free ^= 1u << slot;
+#ifdef MAS_BT_PROFILE
+        pr_free += clock64() - a0;
+#endif
       }
       int ml = Mg - kBtWords * n;  // first word of this stage to walk
       for (int k = kBtWords - 1; k > ml; --k) {  // above the item's last column
@@ -162,63 +184,83 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
       }
       if (y > 0) {
         if (pend & (1u << slot)) {
+          PR_T(a1);
           mbar_wait(full_s + 8u * slot, (ph_full >> slot) & 1u);
           ph_full ^= 1u << slot;
           pend &= ~(1u << slot);
+#ifdef MAS_BT_PROFILE
+          pr_full += clock64() - a1;
+#endif
         }
         const uint32_t slot_base = win_s + slot * kSlotBytes;
         int ylo = s_ylo[slot];
-        // pw: address of (word ml, row y); p1: (word ml, row 1)
+        auto recenter = [&]() {
+#ifdef MAS_BT_PROFILE
+          ++pr_recenter;
+#endif
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          ylo = bt_row0(y, R, T_alloc);
+          s_ylo[slot] = ylo;
+          bt_issue(slot_base, full_s + 8u * slot, dirs, ylo, n, M, T_alloc, R);
+          mbar_wait(full_s + 8u * slot, (ph_full >> slot) & 1u);
+          ph_full ^= 1u << slot;
+        };
+        // The window must hold rows y-40 .. y: a word has at most 32 exits
+        // and a block reads eight rows ahead.
+        if (y - 40 < ylo && ylo > 0) recenter();
+        rec_y[slot][ml] = y;
+        // pw: shared address of (word ml, row y)
         uint32_t pw = slot_base + static_cast<uint32_t>((ml * R + (y - ylo)) * 4);
-        uint32_t p1 = pw - static_cast<uint32_t>((y - 1) * 4);
-        uint32_t c0 = lds32(pw);
-        while (true) {  // one direction word per pass; c0 = word at (ml, y)
-          // The window must hold rows y-35 .. y: a word has at most 32
-          // exits and the queue reads three rows ahead.
-          if (y - 35 < ylo && ylo > 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            ylo = bt_row0(y, R, T_alloc);
-            s_ylo[slot] = ylo;
-            bt_issue(slot_base, full_s + 8u * slot, dirs, ylo, n, M, T_alloc, R);
-            mbar_wait(full_s + 8u * slot, (ph_full >> slot) & 1u);
-            ph_full ^= 1u << slot;
-            pw = slot_base + static_cast<uint32_t>((ml * R + (y - ylo)) * 4);
-            p1 = pw - static_cast<uint32_t>((y - 1) * 4);
-            c0 = lds32(pw);
-          }
-          rec_y[slot][ml] = y;
-          uint32_t c1 = lds32(pw - 4), c2 = lds32(pw - 8), c3 = lds32(pw - 12);
+        // x: the current row's word, restricted to positions the walk may
+        // still take
+        uint32_t x = lds32(pw) & lim;
+        lim = 0xffffffffu;
+        while (true) {  // one direction word per pass; pw = (word ml, row y)
+          // q1..q4: rows y-1 .. y-4 of the word
+          uint32_t q1 = lds32(pw - 4), q2 = lds32(pw - 8), q3 = lds32(pw - 12),
+                   q4 = lds32(pw - 16);
+          uint32_t pb = pw, ps = pw;
           uint32_t exw = 0u;
-          const uint32_t pw_entry = pw;
-          uint32_t h;
-#define MAS_BT_STEP(C)                                   \
-  {                                                      \
-    const uint32_t x = (C) & lim;                        \
-    h = x & (0u - x);                                    \
-    if (static_cast<int>(h) <= 0 || pw == p1) break;     \
-    exw |= h;                                            \
-    lim = h * 0xfffffffeu; /* bits above h */            \
-    pw -= 4u;                                            \
-    (C) = lds32(pw - 12u);                               \
+          // A step: the lowest set bit of x (bit-reversed: the last column
+          // on this row) is an exit; with d = x - 1, x & ~d is that bit and
+          // ~(x ^ d) the positions left of it, so the next row's x is one
+          // LOP3 after the IADD.  The step is self-terminating: once x has
+          // no bit it stays 0, and an exit at position 0 (bit 31) is
+          // recorded and leaves x = 0.  So four steps run without a branch,
+          // and the row reached is y - popc(exits).
+// ps steps down one row per exit (x != 0), so the next word's address is
+// known when the block ends, without waiting for a popc.
+#define MAS_BT_STEP(Q, OFF)                    \
+  {                                            \
+    const uint32_t d = x - 1u;                 \
+    exw |= x & ~d;                             \
+    ps -= x != 0u ? 4u : 0u;                   \
+    x = (Q) & ~(x ^ d);                        \
+    (Q) = lds32(pb - (OFF));                   \
   }
           while (true) {
-            MAS_BT_STEP(c0) MAS_BT_STEP(c1) MAS_BT_STEP(c2) MAS_BT_STEP(c3)
+            MAS_BT_STEP(q1, 20u) MAS_BT_STEP(q2, 24u) MAS_BT_STEP(q3, 28u) MAS_BT_STEP(q4, 32u)
+            pb -= 16u;
+            if ((x & 0x7fffffffu) == 0u) break;
           }
 #undef MAS_BT_STEP
-          y -= static_cast<int>((pw_entry - pw) >> 2);
-          pw -= wstride;
-          p1 -= wstride;
-          if (h != 0u) {  // exit at the word's first position, or at row 1
-            exw |= h;
-            --y;
-            pw -= 4u;
-          }
-          c0 = lds32(pw);
+          exw |= x;  // a pending exit at position 0
+          ps -= x != 0u ? 4u : 0u;
           rec_ex[slot][ml] = exw;
-          --Mg;
-          lim = Mg == 0 ? 0x7fffffffu : 0xffffffffu;
+#ifdef MAS_BT_PROFILE
+          if (pr_words < 300) { pr_ts[pr_words] = static_cast<unsigned>(clock64() - pr_t0); pr_ex[pr_words] = static_cast<unsigned char>(__popc(exw | x)); }
+          ++pr_words;
+#endif
+          y -= static_cast<int>((pw - ps) >> 2);
           --ml;
           if (y == 0 || ml < 0) break;
+          pw = ps - wstride;
+          if (y - 40 < ylo && ylo > 0) {
+            recenter();
+            pw = slot_base + static_cast<uint32_t>((ml * R + (y - ylo)) * 4);
+          }
+          rec_y[slot][ml] = y;
+          x = lds32(pw);
         }
       }
       for (; ml >= 0; --ml) {  // the walk reached row 0: the rest stays there
@@ -226,23 +268,26 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
         rec_ex[slot][ml] = 0u;
       }
       Mg = kBtWords * n - 1;  // next stage starts at its top word
+      rec_yend[slot] = y;
       mbar_arrive_local(done_s + 8u * slot);
-      if (n - kBtStages >= 0 && y > 0) {
-        // the slot's words were consumed above: refill it with stage
-        // n - kBtStages, windowed at the walk's current row
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        s_ylo[slot] = bt_row0(y, R, T_alloc);
-        bt_issue(win_s + slot * kSlotBytes, full_s + 8u * slot, dirs, s_ylo[slot], n - kBtStages,
-                 M, T_alloc, R);
-        pend |= 1u << slot;
-      }
+      // the expander refills this slot with stage n - kBtStages when y > 0
+      if (n - kBtStages >= 0 && y > 0) pend |= 1u << slot;
     }
     for (int k = 0; k < kBtStages; ++k)  // no copy may still be writing our smem
       if (pend & (1u << k)) mbar_wait(full_s + 8u * k, (ph_full >> k) & 1u);
+#ifdef MAS_BT_PROFILE
+    if (b < 2) {
+      printf("bt item %d: total %lld cyc, wait free %lld, wait full %lld, recenters %lld, words %lld\n",
+             b, clock64() - pr_t0, pr_free, pr_full, pr_recenter, pr_words);
+      if (b == 0)
+        for (int i = 1; i < 300 && i < pr_words; ++i)
+          printf("word %d t=%u dt=%u ex=%d\n", i, pr_ts[i], pr_ts[i] - pr_ts[i - 1], pr_ex[i]);
+    }
+#endif
     return;
   }
 
-  // ---- warp 1: expansion ----------------------------------------------------
+  // ---- warp 1: expansion and window refills ---------------------------------
   int32_t* path = a.path ? a.path + static_cast<size_t>(b) * a.S_cap : nullptr;
   uint8_t* out = a.out ? a.out + static_cast<size_t>(b) * a.T_cap * a.S_cap : nullptr;
   if (path)
@@ -264,8 +309,20 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
       ry[i] = rec_y[slot][i];
       rx[i] = rec_ex[slot][i];
     }
+    const int yend = rec_yend[slot];
     __syncwarp();
-    if (lane == 0) mbar_arrive_local(free_s + 8u * slot);
+    if (lane == 0) {
+      mbar_arrive_local(free_s + 8u * slot);
+      if (n - kBtStages >= 0 && yend > 0) {
+        // The walker has finished with this slot's words: refill it with
+        // stage n - kBtStages, windowed at the walk's current row.
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const int row0 = bt_row0(yend, R, T_alloc);
+        s_ylo[slot] = row0;
+        bt_issue(win_s + slot * kSlotBytes, full_s + 8u * slot, dirs, row0, n - kBtStages, M,
+                 T_alloc, R);
+      }
+    }
 #pragma unroll
     for (int i = 0; i < kBtWords; ++i) {
       const int j = 256 * n + 32 * i + lane - 1;

@@ -34,6 +34,8 @@
 //     per SM sub-partition) carries only FMNMX x2, FSETP x2 and the shuffle
 //     select; bit packing (predicated IMAD) and the NonFinite fold (FFMA) run
 //     on the FMA pipe next to the FADDs.
+#include <mutex>
+
 #include "mas_kernels.h"
 #include "mas_ptx.cuh"
 
@@ -364,6 +366,16 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
 #endif
       }
 
+      // The backtrack never needs (and must never take) a step above row 0
+      // or at column -1: store those bits as 0.
+      if (m == 0) {
+        w[0] &= 0x7fffffffu;
+        w[1] &= 0x7fffffffu;
+      }
+      if (row0_is_zero) {
+        w[0] = 0u;
+        w[2] = 0u;
+      }
       st_global_v2_evict_last(dirs_ptr, w[0], w[1], pol_dir);
       if (2 * m + 1 < a.M) st_global_v2_evict_last(dirs_ptr + a.T_alloc, w[2], w[3], pol_dir);
       dirs_ptr += 2 * static_cast<size_t>(a.T_alloc);
@@ -408,20 +420,37 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
 
 size_t fwd_smem_bytes(int W, int N) { return smem_layout(W, N).total + 1024u; }
 
+// Kernel attributes are per function, not per launch, so concurrent plans
+// with different geometries must not race on them: once per device, allow
+// the largest dynamic shared memory the device offers and non-portable
+// cluster sizes (each launch still requests only what it needs).
 cudaError_t fwd_configure(int W, int N, int K) {
-  const int smem = static_cast<int>(fwd_smem_bytes(W, N));
-  cudaError_t e;
-  for (int mode = 0; mode < 2; ++mode) {
-    const void* fn = mode == 0 ? reinterpret_cast<const void*>(&mas_fwd_kernel<0>)
-                               : reinterpret_cast<const void*>(&mas_fwd_kernel<1>);
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    if (K > 8) {
-      e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
+  (void)K;
+  constexpr int kMaxDevices = 64;
+  static std::once_flag once[kMaxDevices];
+  static cudaError_t status[kMaxDevices];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::call_once(once[dev], [dev] {
+    int smem_max = 0;
+    cudaError_t r = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    for (int mode = 0; mode < 2 && r == cudaSuccess; ++mode) {
+      const void* fn = mode == 0 ? reinterpret_cast<const void*>(&mas_fwd_kernel<0>)
+                                 : reinterpret_cast<const void*>(&mas_fwd_kernel<1>);
+      r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+      if (r == cudaSuccess)
+        r = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     }
-  }
-  return cudaSuccess;
+    status[dev] = r;
+  });
+  if (status[dev] != cudaSuccess) return status[dev];
+  int smem_max = 0;
+  e = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  return static_cast<int>(fwd_smem_bytes(W, N)) <= smem_max ? cudaSuccess
+                                                            : cudaErrorInvalidConfiguration;
 }
 
 static cudaLaunchConfig_t fwd_launch_config(int B, int K, int W, int N, cudaStream_t stream,
