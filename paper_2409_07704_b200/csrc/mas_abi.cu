@@ -226,6 +226,24 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
 
 }  // namespace
 
+// Device memory comes from the device's default stream-ordered pool, with
+// the release threshold raised once so repeated calls reuse it instead of
+// re-mapping pages (and cudaFree's device-wide synchronisation is avoided).
+cudaError_t pool_setup(int dev) {
+  constexpr int kMaxDevices = 64;
+  static std::once_flag once[kMaxDevices];
+  static cudaError_t status[kMaxDevices];
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::call_once(once[dev], [dev] {
+    cudaMemPool_t pool;
+    cudaError_t r = cudaDeviceGetDefaultMemPool(&pool, dev);
+    uint64_t keep = ~0ull;
+    if (r == cudaSuccess) r = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    status[dev] = r;
+  });
+  return status[dev];
+}
+
 struct mas_plan {
   int32_t B = 0, T = 0, S = 0;
   int64_t pitch = 0;
@@ -244,6 +262,7 @@ struct mas_plan {
   int launches = 0;
   int device = 0;
   int bt_rows = 64;       // backtrack window rows
+  bool internal = false;  // created by mas_align_host / _device, which order the frees
 };
 
 extern "C" {
@@ -269,10 +288,14 @@ void mas_plan_destroy(mas_plan_t* p) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
-  cudaFree(p->d_lengths);
-  cudaFree(p->d_dirs);
-  cudaFree(p->d_flags);
-  cudaFree(p->d_locate);
+  // A caller-held plan may still have kernels in flight on the caller's
+  // stream: finish them before the workspace goes back to the pool.
+  if (!p->internal) cudaDeviceSynchronize();
+  cudaStream_t st = cudaStreamPerThread;
+  cudaFreeAsync(p->d_lengths, st);
+  cudaFreeAsync(p->d_dirs, st);
+  cudaFreeAsync(p->d_flags, st);
+  cudaFreeAsync(p->d_locate, st);
   cudaSetDevice(prev);
   delete p;
 }
@@ -336,23 +359,32 @@ int mas_plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t
   cudaError_t e;
   if ((e = mas::fwd_configure(g.W, g.N, g.K)) != cudaSuccess) return fail(e, "fwd_configure");
   if ((e = mas::bt_configure(g.T_alloc, g.L)) != cudaSuccess) return fail(e, "bt_configure");
+  if ((e = pool_setup(p->device)) != cudaSuccess) return fail(e, "memory pool setup");
+  // Workspace from the stream-ordered pool on this thread's default stream;
+  // synchronised below, so it is valid on any stream afterwards.
+  cudaStream_t st = cudaStreamPerThread;
   const size_t nB = static_cast<size_t>(batch);
-  if ((e = cudaMalloc(&p->d_lengths, nB * 2 * sizeof(uint32_t))) != cudaSuccess)
-    return fail(e, "cudaMalloc(lengths)");
-  if ((e = cudaMemcpy(p->d_lengths, p->lengths.data(), nB * 2 * sizeof(uint32_t),
-                      cudaMemcpyHostToDevice)) != cudaSuccess)
-    return fail(e, "cudaMemcpy(lengths)");
-  if ((e = cudaMalloc(&p->d_dirs, nB * g.M * g.T_alloc * sizeof(uint32_t))) != cudaSuccess)
-    return fail(e, "cudaMalloc(dirs)");
+  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_lengths), nB * 2 * sizeof(uint32_t),
+                           st)) != cudaSuccess)
+    return fail(e, "cudaMallocAsync(lengths)");
+  if ((e = cudaMemcpyAsync(p->d_lengths, p->lengths.data(), nB * 2 * sizeof(uint32_t),
+                           cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return fail(e, "cudaMemcpyAsync(lengths)");
+  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_dirs),
+                           nB * g.M * g.T_alloc * sizeof(uint32_t), st)) != cudaSuccess)
+    return fail(e, "cudaMallocAsync(dirs)");
   static const int bt_rows_cap = [] {
     const char* e = std::getenv("MAS_BT_ROWS");  // experiment override
     return e ? std::max(16, std::min(256, std::atoi(e))) & ~15 : 256;
   }();
   p->bt_rows = std::min(bt_rows_cap, g.T_alloc);
-  if ((e = cudaMalloc(&p->d_flags, nB * sizeof(int))) != cudaSuccess)
-    return fail(e, "cudaMalloc(flags)");
-  if ((e = cudaMalloc(&p->d_locate, sizeof(unsigned long long))) != cudaSuccess)
-    return fail(e, "cudaMalloc(locate)");
+  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_flags), nB * sizeof(int), st)) !=
+      cudaSuccess)
+    return fail(e, "cudaMallocAsync(flags)");
+  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_locate), sizeof(unsigned long long),
+                           st)) != cudaSuccess)
+    return fail(e, "cudaMallocAsync(locate)");
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail(e, "plan workspace");
   *plan_out = p;
   return MAS_OK;
 }
@@ -367,6 +399,87 @@ void mas_plan_geometry(const mas_plan_t* p, int32_t geom[5]) {
   geom[4] = p->geo.L;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Enqueues the kernels (MAS_PART_* bits) for items [b0, b0 + nb) of the
+// plan's batch.  d_values / d_out / d_paths are the whole batch's buffers.
+int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_values,
+                  uint8_t* d_out, int32_t* d_paths, cudaStream_t stream, mas_error_t* err) {
+  if ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (p->pitch & 3) != 0 || (p->T_pad & 1))
+    return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
+                     "device layout needs 16-byte base, pitch % 4 == 0 and even text_cap");
+  const Geometry& g = p->geo;
+  int nfwd = 0, nbt = 0;
+  if (parts & MAS_PART_FORWARD) {
+    CUtensorMap tm0, tm1;
+    if (!encode_maps(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, &tm0, &tm1))
+      return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled failed");
+    MAS_CUDA(cudaMemsetAsync(p->d_flags + b0, 0, sizeof(int) * nb, stream),
+             "cudaMemsetAsync(flags)");
+    mas::FwdArgs fa;
+    fa.b0 = b0;
+    fa.lengths = p->d_lengths;
+    fa.dirs = p->d_dirs;
+    fa.flags = p->d_flags;
+    fa.T_pad = p->T_pad;
+    fa.M = g.M;
+    fa.T_alloc = g.T_alloc;
+    fa.K = g.K;
+    fa.W = g.W;
+    fa.N = g.N;
+    fa.mnv = p->mnv;
+    fa.row0_up = p->mode == 1 ? -std::numeric_limits<float>::infinity() : p->mnv;
+    // The output's zero fill rides along with the forward pass when every
+    // item is full length (its warps then cover every row and column);
+    // ragged batches get a stream-ordered memset instead.
+    static const bool no_fuse = [] {
+      const char* e = std::getenv("MAS_NO_FUSED_ZERO");
+      return e && e[0] == '1';
+    }();
+    const bool fused_zero = d_out && !no_fuse && p->all_full && (p->S % 16) == 0 &&
+                            (reinterpret_cast<uintptr_t>(d_out) & 15u) == 0;
+    const size_t item_bytes = static_cast<size_t>(p->T) * p->S;
+    if (d_out && !fused_zero) {
+      MAS_CUDA(cudaMemsetAsync(d_out + b0 * item_bytes, 0, nb * item_bytes, stream),
+               "cudaMemsetAsync(out)");
+    }
+    CUtensorMap tm_out;
+    std::memset(&tm_out, 0, sizeof(tm_out));
+    if (fused_zero && !encode_out_map(d_out, static_cast<int64_t>(p->B) * p->T, p->S, &tm_out))
+      return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled(out) failed");
+    fa.zero_fill = fused_zero ? 1 : 0;
+    fa.one = 1u;
+    fa.zero = 0.0f;
+    fa.T_cap = p->T;
+    fa.S_cap = p->S;
+    MAS_CUDA(mas::launch_fwd(p->mode, tm0, tm1, tm_out, fa, nb, stream), "launch mas_fwd");
+    nfwd = 1;
+  }
+  if ((parts & MAS_PART_BACKTRACK) && (d_out || d_paths)) {
+    mas::BtArgs ba;
+    ba.b0 = b0;
+    ba.lengths = p->d_lengths;
+    ba.dirs = p->d_dirs;
+    ba.path = d_paths;
+    ba.out = d_out;
+    ba.B = nb;
+    ba.T_cap = p->T;
+    ba.S_cap = p->S;
+    ba.M = g.M;
+    ba.T_alloc = g.T_alloc;
+    ba.R = p->bt_rows;
+    MAS_CUDA(mas::launch_backtrack(ba, stream, &nbt), "launch backtrack");
+  }
+  p->launches = nfwd + nbt;
+  return MAS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int mas_plan_enqueue(mas_plan_t* p, const float* d_values, uint8_t* d_out, int32_t* d_paths,
                      void* stream_v, mas_error_t* err) {
   return mas_plan_enqueue_part(p, MAS_PART_ALL, d_values, d_out, d_paths, stream_v, err);
@@ -375,71 +488,8 @@ int mas_plan_enqueue(mas_plan_t* p, const float* d_values, uint8_t* d_out, int32
 int mas_plan_enqueue_part(mas_plan_t* p, uint32_t parts, const float* d_values, uint8_t* d_out,
                           int32_t* d_paths, void* stream_v, mas_error_t* err) {
   clear_error(err);
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
-  if ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (p->pitch & 3) != 0 || (p->T_pad & 1))
-    return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
-                     "device layout needs 16-byte base, pitch % 4 == 0 and even text_cap");
-  CUtensorMap tm0, tm1;
-  if (!encode_maps(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, &tm0, &tm1))
-    return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled failed");
-  const Geometry& g = p->geo;
-  int nfwd = 0, nbt = 0;
-  if (parts & MAS_PART_FORWARD) {
-  MAS_CUDA(cudaMemsetAsync(p->d_flags, 0, sizeof(int) * p->B, stream), "cudaMemsetAsync(flags)");
-  mas::FwdArgs fa;
-  fa.lengths = p->d_lengths;
-  fa.dirs = p->d_dirs;
-  fa.flags = p->d_flags;
-  fa.T_pad = p->T_pad;
-  fa.M = g.M;
-  fa.T_alloc = g.T_alloc;
-  fa.K = g.K;
-  fa.W = g.W;
-  fa.N = g.N;
-  fa.mnv = p->mnv;
-  fa.row0_up = p->mode == 1 ? -std::numeric_limits<float>::infinity() : p->mnv;
-  // The output's zero fill rides along with the forward pass when every
-  // item is full length (its warps then cover every row and column); ragged
-  // batches get a stream-ordered memset instead.
-  static const bool no_fuse = [] {
-    const char* e = std::getenv("MAS_NO_FUSED_ZERO");
-    return e && e[0] == '1';
-  }();
-  const bool fused_zero = d_out && !no_fuse && p->all_full && (p->S % 16) == 0 &&
-                          (reinterpret_cast<uintptr_t>(d_out) & 15u) == 0;
-  if (d_out && !fused_zero) {
-    MAS_CUDA(cudaMemsetAsync(d_out, 0, static_cast<size_t>(p->B) * p->T * p->S, stream),
-             "cudaMemsetAsync(out)");
-  }
-  CUtensorMap tm_out;
-  std::memset(&tm_out, 0, sizeof(tm_out));
-  if (fused_zero && !encode_out_map(d_out, static_cast<int64_t>(p->B) * p->T, p->S, &tm_out))
-    return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled(out) failed");
-  fa.zero_fill = fused_zero ? 1 : 0;
-  fa.one = 1u;
-  fa.zero = 0.0f;
-  fa.T_cap = p->T;
-  fa.S_cap = p->S;
-  MAS_CUDA(mas::launch_fwd(p->mode, tm0, tm1, tm_out, fa, p->B, stream), "launch mas_fwd");
-  nfwd = 1;
-  }
-  if (parts & MAS_PART_BACKTRACK) {
-  mas::BtArgs ba;
-  ba.lengths = p->d_lengths;
-  ba.dirs = p->d_dirs;
-  ba.path = d_paths;
-  ba.out = d_out;
-  ba.B = p->B;
-  ba.T_cap = p->T;
-  ba.S_cap = p->S;
-  ba.M = g.M;
-  ba.T_alloc = g.T_alloc;
-  ba.R = p->bt_rows;
-  if (d_out || d_paths)
-    MAS_CUDA(mas::launch_backtrack(ba, stream, &nbt), "launch backtrack");
-  }
-  p->launches = nfwd + nbt;
-  return MAS_OK;
+  return enqueue_items(p, parts, 0, p->B, d_values, d_out, d_paths,
+                       static_cast<cudaStream_t>(stream_v), err);
 }
 
 int mas_plan_finish(mas_plan_t* p, const float* d_values, void* stream_v, mas_error_t* err) {
@@ -447,8 +497,10 @@ int mas_plan_finish(mas_plan_t* p, const float* d_values, void* stream_v, mas_er
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   MAS_CUDA(cudaStreamSynchronize(stream), "kernel execution");
   std::vector<int> flags(p->B);
-  MAS_CUDA(cudaMemcpy(flags.data(), p->d_flags, sizeof(int) * p->B, cudaMemcpyDeviceToHost),
-           "cudaMemcpy(flags)");
+  MAS_CUDA(cudaMemcpyAsync(flags.data(), p->d_flags, sizeof(int) * p->B, cudaMemcpyDeviceToHost,
+                           stream),
+           "cudaMemcpyAsync(flags)");
+  MAS_CUDA(cudaStreamSynchronize(stream), "flags readback");
   const int limit = p->first_host_error.item >= 0 ? p->first_host_error.item : p->B;
   for (int b = 0; b < limit; ++b) {
     if (!flags[b]) continue;
@@ -488,6 +540,7 @@ int mas_align_device(const float* d_values, int64_t row_pitch, int32_t batch, in
   mas_plan_t* plan = nullptr;
   int rc = mas_plan_create(batch, text_cap, speech_cap, row_pitch, lengths, cfg, &plan, err);
   if (rc) return rc;
+  plan->internal = true;
   const float* q = d_values;
   float* scratch = nullptr;
   if ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (row_pitch & 3) != 0 ||
@@ -539,54 +592,82 @@ int mas_align_host(const float* values, int32_t batch, int32_t text_cap, int32_t
     rc = validate_dims(batch, text_cap, speech_cap, err);
     if (rc) return rc;
   }
-  cudaStream_t stream = cudaStreamPerThread;
   const int T_pad = (text_cap + 1) & ~1;
   const int64_t pitch = (static_cast<int64_t>(speech_cap) + 3) & ~int64_t(3);
-  const size_t q_bytes = static_cast<size_t>(batch) * T_pad * pitch * 4;
-  const size_t o_bytes = static_cast<size_t>(batch) * text_cap * speech_cap;
-  const size_t p_bytes = static_cast<size_t>(batch) * speech_cap * 4;
+  const size_t q_item = static_cast<size_t>(T_pad) * pitch;  // floats per item on the device
+  const size_t o_item = static_cast<size_t>(text_cap) * speech_cap;
   mas_plan_t* plan = nullptr;
   int rc = mas_plan_create(batch, text_cap, speech_cap, pitch, lengths, cfg, &plan, err);
   if (rc) return rc;
+  plan->internal = true;
   plan->T_pad = T_pad;
+
+  // Items are processed in chunks on two streams, so the host->device copy
+  // of chunk c+1 runs while chunk c computes and copies its alignment back
+  // (PCIe is full duplex): the call costs about one pass over the input on
+  // the bus instead of input + output + compute in sequence.
+  const int nchunk = std::min(batch, 4);
+  const int per = (batch + nchunk - 1) / nchunk;
+  cudaStream_t st[2] = {nullptr, nullptr};
   float* d_q = nullptr;
   uint8_t* d_out = nullptr;
   int32_t* d_paths = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_q), q_bytes, stream);
-  if (e == cudaSuccess && out) e = cudaMallocAsync(reinterpret_cast<void**>(&d_out), o_bytes, stream);
+  cudaError_t e = cudaSuccess;
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k)
+    e = cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
+  if (e == cudaSuccess)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&d_q), batch * q_item * sizeof(float), st[0]);
+  if (e == cudaSuccess && out)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&d_out), batch * o_item, st[0]);
   if (e == cudaSuccess && paths)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&d_paths), p_bytes, stream);
-  if (e == cudaSuccess) {
-    if (T_pad == text_cap) {
-      e = cudaMemcpy2DAsync(d_q, pitch * 4, values, static_cast<size_t>(speech_cap) * 4,
+    e = cudaMallocAsync(reinterpret_cast<void**>(&d_paths),
+                        static_cast<size_t>(batch) * speech_cap * sizeof(int32_t), st[0]);
+  cudaEvent_t ready = nullptr;
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ready, st[0]);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st[1], ready, 0);
+  if (e != cudaSuccess) rc = cuda_error(err, e, "host path setup");
+  for (int c = 0; c < nchunk && rc == MAS_OK; ++c) {
+    const int b0 = c * per;
+    const int nb = std::min(per, batch - b0);
+    if (nb <= 0) break;
+    cudaStream_t s = st[c & 1];
+    for (int b = b0; b < b0 + nb && e == cudaSuccess; ++b)
+      e = cudaMemcpy2DAsync(d_q + b * q_item, pitch * 4, values + b * o_item,
                             static_cast<size_t>(speech_cap) * 4,
-                            static_cast<size_t>(batch) * text_cap, cudaMemcpyHostToDevice, stream);
-    } else {
-      for (int b = 0; b < batch && e == cudaSuccess; ++b)
-        e = cudaMemcpy2DAsync(d_q + static_cast<size_t>(b) * T_pad * pitch, pitch * 4,
-                              values + static_cast<size_t>(b) * text_cap * speech_cap,
-                              static_cast<size_t>(speech_cap) * 4,
-                              static_cast<size_t>(speech_cap) * 4, text_cap,
-                              cudaMemcpyHostToDevice, stream);
+                            static_cast<size_t>(speech_cap) * 4, text_cap, cudaMemcpyHostToDevice,
+                            s);
+    if (e != cudaSuccess) {
+      rc = cuda_error(err, e, "host->device staging");
+      break;
     }
+    rc = enqueue_items(plan, MAS_PART_ALL, b0, nb, d_q, d_out, d_paths, s, err);
+    if (rc != MAS_OK) break;
+    if (out &&
+        (e = cudaMemcpyAsync(out + b0 * o_item, d_out + b0 * o_item, nb * o_item,
+                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      rc = cuda_error(err, e, "device->host out");
+    if (rc == MAS_OK && paths &&
+        (e = cudaMemcpyAsync(paths + static_cast<size_t>(b0) * speech_cap,
+                             d_paths + static_cast<size_t>(b0) * speech_cap,
+                             static_cast<size_t>(nb) * speech_cap * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      rc = cuda_error(err, e, "device->host paths");
   }
-  if (e != cudaSuccess) {
-    rc = cuda_error(err, e, "host->device staging");
-  } else {
-    rc = mas_plan_enqueue(plan, d_q, d_out, d_paths, stream, err);
-    if (rc == MAS_OK && out)
-      if ((e = cudaMemcpyAsync(out, d_out, o_bytes, cudaMemcpyDeviceToHost, stream)) != cudaSuccess)
-        rc = cuda_error(err, e, "device->host out");
-    if (rc == MAS_OK && paths)
-      if ((e = cudaMemcpyAsync(paths, d_paths, p_bytes, cudaMemcpyDeviceToHost, stream)) !=
-          cudaSuccess)
-        rc = cuda_error(err, e, "device->host paths");
-    if (rc == MAS_OK) rc = mas_plan_finish(plan, d_q, stream, err);
+  // Join the second stream into the first; the NonFinite check and the
+  // frees follow on st[0].
+  if (st[1] && ready) {
+    cudaEventRecord(ready, st[1]);
+    cudaStreamWaitEvent(st[0], ready, 0);
   }
-  cudaFreeAsync(d_q, stream);
-  if (d_out) cudaFreeAsync(d_out, stream);
-  if (d_paths) cudaFreeAsync(d_paths, stream);
-  cudaStreamSynchronize(stream);
+  if (rc == MAS_OK) rc = mas_plan_finish(plan, d_q, st[0], err);
+  if (d_q) cudaFreeAsync(d_q, st[0]);
+  if (d_out) cudaFreeAsync(d_out, st[0]);
+  if (d_paths) cudaFreeAsync(d_paths, st[0]);
+  if (st[0]) cudaStreamSynchronize(st[0]);
+  if (ready) cudaEventDestroy(ready);
+  for (int k = 0; k < 2; ++k)
+    if (st[k]) cudaStreamDestroy(st[k]);
   mas_plan_destroy(plan);
   return rc;
 }

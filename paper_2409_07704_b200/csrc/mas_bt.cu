@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
   __shared__ uint32_t rec_ex[kBtStages][kBtWords];
   __shared__ int s_ylo[kBtStages];
   __shared__ int rec_yend[kBtStages];
-  const int b = blockIdx.x;
+  const int b = a.b0 + static_cast<int>(blockIdx.x);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int t = static_cast<int>(a.lengths[2 * b]);
@@ -339,8 +339,9 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
 // Reference-order serial walk, one thread per item -- kept as a
 // cross-check (MAS_BT_SERIAL=1) for the windowed walker.
 __global__ void bt_serial_kernel(const BtArgs a) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= a.B) return;
+  const int bi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bi >= a.B) return;
+  const int b = a.b0 + bi;
   const int t = static_cast<int>(a.lengths[2 * b]);
   const int s = static_cast<int>(a.lengths[2 * b + 1]);
   if (t <= 0 || s <= 0) return;
@@ -423,7 +424,8 @@ cudaError_t launch_backtrack(const BtArgs& a, cudaStream_t stream, int* launches
   }();
   if (serial) {
     fill_paths_kernel<<<grid_for(static_cast<size_t>(a.B) * a.S_cap, 256), 256, 0, stream>>>(
-        a.path, static_cast<size_t>(a.B) * a.S_cap);
+        a.path ? a.path + static_cast<size_t>(a.b0) * a.S_cap : nullptr,
+        static_cast<size_t>(a.B) * a.S_cap);
     bt_serial_kernel<<<(a.B + 63) / 64, 64, 0, stream>>>(a);
     if (launches) *launches = 2;
     return cudaGetLastError();

@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int crank = static_cast<int>(cluster_ctarank());
-  const int b = blockIdx.x / a.K;
+  const int b = a.b0 + static_cast<int>(blockIdx.x) / a.K;
   const int g = crank * W + warp;
   const int i0 = g * kRowsPerWarp;
   const int t_b = static_cast<int>(a.lengths[2 * b]);

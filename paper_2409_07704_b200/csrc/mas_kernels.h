@@ -23,6 +23,7 @@ constexpr int kMaxWarpsPerCta = 8;
 constexpr int kMaxClusterCtas = 16;
 
 struct FwdArgs {
+  int b0;                   // first item of this launch (items b0 .. b0 + grid/K - 1)
   const uint32_t* lengths;  // [B][2] (t, s); t == 0 marks an item not to run
   uint32_t* dirs;           // [B][M][T_alloc] direction words, see DESIGN.md
   int* flags;               // [B] NonFinite candidate flags
@@ -41,6 +42,7 @@ struct FwdArgs {
 };
 
 struct BtArgs {
+  int b0;                   // first item of this launch; B items from there
   const uint32_t* lengths;  // [B][2]
   const uint32_t* dirs;     // [B][M][T_alloc]
   int32_t* path;            // [B][S_cap] int32 path rows, -1 past s_b, or null
