@@ -25,6 +25,10 @@
  *   mas_generate_device  bench::generate_random_batch (bench.hpp:58,
  *                       bench.cpp:164-180), bit-identical, for any item shard.
  *   mas_errc_name     errc_name (types.cpp:8-29).
+ *   mas_validate_config / mas_validate_host
+ *                     validate_config / validate_batch / validate_item
+ *                       (types.cpp:59-130), for the C++ mirror in
+ *                       include/monoalign/.
  *
  * Error convention: every entry returns a mas_status; on MAS_E_VALIDATION
  * `err->errc` holds the reference Errc (errors.hpp:8-30 order) and
@@ -157,6 +161,18 @@ MAS_API int mas_plan_launches(const mas_plan_t* plan);
  * ctas_per_item (cluster size), stages, segment_columns}. */
 MAS_API void mas_plan_geometry(const mas_plan_t* plan, int32_t geom[5]);
 MAS_API void mas_plan_destroy(mas_plan_t* plan);
+
+/* validate_config (types.cpp:59-69): MAS_OK or MAS_E_VALIDATION with the
+ * reference's InvalidConfig text. */
+MAS_API int mas_validate_config(const mas_config_t* cfg, mas_error_t* err);
+
+/* validate_batch / validate_item (types.cpp:81-130) of host data: the
+ * length checks on the host, the NonFinite scan on the device (the forward
+ * kernel runs without outputs).  `item_base` is added to the item index in
+ * messages, so validate_item(batch, b) can pass item b alone. */
+MAS_API int mas_validate_host(const float* values, int32_t batch, int32_t text_cap,
+                      int32_t speech_cap, const uint32_t* lengths, int32_t item_base,
+                      mas_error_t* err);
 
 /* bench::generate_random_batch(batch, text_cap, speech_cap, seed), items
  * [first_item, first_item + batch) of that stream, written pitched into

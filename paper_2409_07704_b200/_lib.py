@@ -80,6 +80,9 @@ _SIGS = {
     "mas_generate_device": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32,
                                            ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, _VP,
                                            _VP]),
+    "mas_validate_config": (ctypes.c_int, [ctypes.POINTER(MasConfig), ctypes.POINTER(MasError)]),
+    "mas_validate_host": (ctypes.c_int, [_VP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _VP,
+                                         ctypes.c_int32, ctypes.POINTER(MasError)]),
     "mas_errc_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "mas_abi_version": (ctypes.c_int, []),
 }

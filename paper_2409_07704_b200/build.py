@@ -43,7 +43,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
         return out
     os.makedirs(os.path.dirname(out), exist_ok=True)
     cmd = [
-        NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+        NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++20",
         "-ccbin", HOST_CXX, "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC,
         "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",

@@ -263,6 +263,7 @@ struct mas_plan {
   int device = 0;
   int bt_rows = 64;       // backtrack window rows
   bool internal = false;  // created by mas_align_host / _device, which order the frees
+  int item_base = 0;      // added to item indices in messages (validate_item of one item)
 };
 
 extern "C" {
@@ -300,9 +301,29 @@ void mas_plan_destroy(mas_plan_t* p) {
   delete p;
 }
 
+}  // extern "C"
+
+namespace {
+int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row_pitch,
+                const uint32_t* lengths, const mas_config_t* cfg_in, int item_base,
+                mas_plan_t** plan_out, mas_error_t* err);
+}  // namespace
+
+extern "C" {
+
 int mas_plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row_pitch,
                     const uint32_t* lengths, const mas_config_t* cfg_in, mas_plan_t** plan_out,
                     mas_error_t* err) {
+  return plan_create(batch, text_cap, speech_cap, row_pitch, lengths, cfg_in, 0, plan_out, err);
+}
+
+}  // extern "C"
+
+namespace {
+
+int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row_pitch,
+                const uint32_t* lengths, const mas_config_t* cfg_in, int item_base,
+                mas_plan_t** plan_out, mas_error_t* err) {
   clear_error(err);
   *plan_out = nullptr;
   mas_config_t cfg;
@@ -320,6 +341,7 @@ int mas_plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t
   auto* p = new (std::nothrow) mas_plan();
   if (!p) return set_error(err, MAS_E_UNSUPPORTED, -1, -1, "out of host memory");
   cudaGetDevice(&p->device);
+  p->item_base = item_base;
   p->B = batch;
   p->T = text_cap;
   p->S = speech_cap;
@@ -333,7 +355,7 @@ int mas_plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t
     const uint32_t t = lengths ? lengths[2 * b] : static_cast<uint32_t>(text_cap);
     const uint32_t s = lengths ? lengths[2 * b + 1] : static_cast<uint32_t>(speech_cap);
     ItemError ie;
-    if (length_error(b, t, s, text_cap, speech_cap, &ie)) {
+    if (length_error(b + item_base, t, s, text_cap, speech_cap, &ie)) {
       if (p->first_host_error.item < 0) p->first_host_error = ie;
       p->lengths[2 * b] = 0;
       p->lengths[2 * b + 1] = 0;
@@ -388,6 +410,10 @@ int mas_plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t
   *plan_out = p;
   return MAS_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 int mas_plan_launches(const mas_plan_t* p) { return p ? p->launches : 0; }
 
@@ -520,7 +546,8 @@ int mas_plan_finish(mas_plan_t* p, const float* d_values, void* stream_v, mas_er
     if (hit != none) {
       const int64_t s = p->lengths[2 * b + 1];
       const int64_t i = static_cast<int64_t>(hit / s), j = static_cast<int64_t>(hit % s);
-      set_error(err, MAS_E_VALIDATION, MAS_ERRC_NON_FINITE, b, nonfinite_message(b, i, j));
+      set_error(err, MAS_E_VALIDATION, MAS_ERRC_NON_FINITE, b + p->item_base,
+                nonfinite_message(b + p->item_base, i, j));
       err->i = i;
       err->j = j;
       return MAS_E_VALIDATION;
@@ -577,9 +604,13 @@ int mas_align_device(const float* d_values, int64_t row_pitch, int32_t batch, in
   return rc;
 }
 
-int mas_align_host(const float* values, int32_t batch, int32_t text_cap, int32_t speech_cap,
-                   const uint32_t* lengths, const mas_config_t* cfg, uint8_t* out, int32_t* paths,
-                   mas_error_t* err) {
+}  // extern "C"
+
+namespace {
+
+int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_t speech_cap,
+                    const uint32_t* lengths, const mas_config_t* cfg, uint8_t* out,
+                    int32_t* paths, int item_base, mas_error_t* err) {
   clear_error(err);
   {
     mas_config_t c;
@@ -597,7 +628,7 @@ int mas_align_host(const float* values, int32_t batch, int32_t text_cap, int32_t
   const size_t q_item = static_cast<size_t>(T_pad) * pitch;  // floats per item on the device
   const size_t o_item = static_cast<size_t>(text_cap) * speech_cap;
   mas_plan_t* plan = nullptr;
-  int rc = mas_plan_create(batch, text_cap, speech_cap, pitch, lengths, cfg, &plan, err);
+  int rc = plan_create(batch, text_cap, speech_cap, pitch, lengths, cfg, item_base, &plan, err);
   if (rc) return rc;
   plan->internal = true;
   plan->T_pad = T_pad;
@@ -670,6 +701,36 @@ int mas_align_host(const float* values, int32_t batch, int32_t text_cap, int32_t
     if (st[k]) cudaStreamDestroy(st[k]);
   mas_plan_destroy(plan);
   return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mas_align_host(const float* values, int32_t batch, int32_t text_cap, int32_t speech_cap,
+                   const uint32_t* lengths, const mas_config_t* cfg, uint8_t* out, int32_t* paths,
+                   mas_error_t* err) {
+  return align_host_impl(values, batch, text_cap, speech_cap, lengths, cfg, out, paths, 0, err);
+}
+
+int mas_validate_config(const mas_config_t* cfg, mas_error_t* err) {
+  clear_error(err);
+  mas_config_t c;
+  if (cfg)
+    c = *cfg;
+  else
+    mas_config_default(&c);
+  c.flags &= ~MAS_FLAG_UNCHECKED;
+  return validate_config(c, err);
+}
+
+int mas_validate_host(const float* values, int32_t batch, int32_t text_cap, int32_t speech_cap,
+                      const uint32_t* lengths, int32_t item_base, mas_error_t* err) {
+  mas_config_t c;
+  mas_config_default(&c);
+  c.flags = MAS_FLAG_UNCHECKED;
+  return align_host_impl(values, batch, text_cap, speech_cap, lengths, &c, nullptr, nullptr,
+                         item_base, err);
 }
 
 int mas_generate_device(uint64_t seed, int32_t batch, int32_t text_cap, int32_t speech_cap,

@@ -1,0 +1,235 @@
+// monoalign_api.cpp -- the reference's C++ API (include/monoalign/*.hpp of
+// /root/reference/proj) over the C-ABI of include/monoalign_b200.h.
+//
+// Host-side only: container construction, the ShapeMismatch container check
+// (parallel.cpp:118-125), exception mapping (errors.hpp:32-53), and the
+// path/matrix helpers of types.cpp:132-185.  Every alignment and the
+// NonFinite validation are computed by the sm_100a kernels behind
+// mas_align_host / mas_validate_host; there is no CPU fallback -- a device
+// failure throws DeviceError.
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "monoalign/align.hpp"
+#include "../../include/monoalign_b200.h"
+
+namespace monoalign {
+
+namespace {
+
+[[noreturn]] void throw_for(int rc, const mas_error_t& err) {
+  const std::string msg(err.message);
+  if (rc == MAS_E_VALIDATION) throw ValidationError(static_cast<Errc>(err.errc), msg);
+  if (rc == MAS_E_IO) throw IoError(static_cast<Errc>(err.errc), msg);
+  throw DeviceError("monoalign device path failed: " + msg);
+}
+
+mas_config_t to_c(const MasConfig& cfg, bool unchecked) {
+  mas_config_t c;
+  mas_config_default(&c);
+  c.engine = cfg.engine == EngineKind::Reference ? MAS_ENGINE_REFERENCE : MAS_ENGINE_PARALLEL;
+  c.max_neg_val = cfg.max_neg_val;
+  c.lane_padding = cfg.lane_padding == LanePadding::NextPowerOfTwo ? 1 : 0;
+  c.threads = cfg.threads;
+  c.flags = unchecked ? MAS_FLAG_UNCHECKED : 0u;
+  return c;
+}
+
+// parallel.cpp:118-125 / types.cpp:119-126
+void check_containers(const LikelihoodBatch& batch) {
+  if (batch.batch < 1 || batch.text_cap < 1 || batch.speech_cap < 1)
+    throw ValidationError(Errc::ZeroDim, "batch and capacities must be at least 1");
+  if (batch.lengths.size() != static_cast<std::size_t>(batch.batch) ||
+      batch.values.size() != static_cast<std::size_t>(batch.batch) * batch.item_stride())
+    throw ValidationError(Errc::ShapeMismatch,
+                          "container sizes do not match the declared dimensions");
+}
+
+std::vector<uint32_t> flat_lengths(const LikelihoodBatch& batch) {
+  std::vector<uint32_t> l(static_cast<std::size_t>(batch.batch) * 2);
+  for (int b = 0; b < batch.batch; ++b) {
+    l[2 * b] = batch.lengths[b].text;
+    l[2 * b + 1] = batch.lengths[b].speech;
+  }
+  return l;
+}
+
+AlignmentMatrix run(const LikelihoodBatch& batch, const MasConfig& cfg, bool unchecked) {
+  const mas_config_t c = to_c(cfg, unchecked);
+  mas_error_t err;
+  if (!unchecked) {
+    const int rc = mas_validate_config(&c, &err);
+    if (rc != MAS_OK) throw_for(rc, err);
+  }
+  check_containers(batch);
+  AlignmentMatrix out(batch.batch, batch.text_cap, batch.speech_cap);
+  out.lengths = batch.lengths;
+  const std::vector<uint32_t> l = flat_lengths(batch);
+  const int rc = mas_align_host(batch.values.data(), batch.batch, batch.text_cap, batch.speech_cap,
+                                l.data(), &c, out.values.data(), nullptr, &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+  return out;
+}
+
+}  // namespace
+
+const char* errc_name(Errc code) { return mas_errc_name(static_cast<int32_t>(code)); }
+
+void validate_config(const MasConfig& cfg) {
+  const mas_config_t c = to_c(cfg, false);
+  mas_error_t err;
+  const int rc = mas_validate_config(&c, &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+}
+
+LikelihoodBatch::LikelihoodBatch(int batch_size, int text_capacity, int speech_capacity)
+    : batch(batch_size),
+      text_cap(text_capacity),
+      speech_cap(speech_capacity),
+      values(static_cast<std::size_t>(batch_size) * text_capacity * speech_capacity, 0.0f),
+      lengths(static_cast<std::size_t>(batch_size),
+              ValidLengths{static_cast<std::uint32_t>(text_capacity),
+                           static_cast<std::uint32_t>(speech_capacity)}) {}
+
+AlignmentMatrix::AlignmentMatrix(int batch_size, int text_capacity, int speech_capacity)
+    : batch(batch_size),
+      text_cap(text_capacity),
+      speech_cap(speech_capacity),
+      values(static_cast<std::size_t>(batch_size) * text_capacity * speech_capacity, 0),
+      lengths(static_cast<std::size_t>(batch_size),
+              ValidLengths{static_cast<std::uint32_t>(text_capacity),
+                           static_cast<std::uint32_t>(speech_capacity)}) {}
+
+LikelihoodView item_view(const LikelihoodBatch& batch, int b) {
+  return {batch.item(b).data(), static_cast<int>(batch.lengths[b].text),
+          static_cast<int>(batch.lengths[b].speech), batch.speech_cap};
+}
+
+MutableLikelihoodView item_view(LikelihoodBatch& batch, int b) {
+  return {batch.item(b).data(), static_cast<int>(batch.lengths[b].text),
+          static_cast<int>(batch.lengths[b].speech), batch.speech_cap};
+}
+
+void validate_batch(const LikelihoodBatch& batch) {
+  check_containers(batch);
+  const std::vector<uint32_t> l = flat_lengths(batch);
+  mas_error_t err;
+  const int rc = mas_validate_host(batch.values.data(), batch.batch, batch.text_cap,
+                                   batch.speech_cap, l.data(), 0, &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+}
+
+void validate_item(const LikelihoodBatch& batch, int b) {
+  check_containers(batch);
+  const uint32_t l[2] = {batch.lengths[b].text, batch.lengths[b].speech};
+  mas_error_t err;
+  const int rc = mas_validate_host(batch.item(b).data(), 1, batch.text_cap, batch.speech_cap, l, b,
+                                   &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+}
+
+void validate_path(const PathVector& path, int t, int s) {
+  if (t < 1 || s < 1 || t > s)
+    throw ValidationError(Errc::InvalidPath, "dimensions do not admit a monotonic path");
+  if (path.size() != static_cast<std::size_t>(s))
+    throw ValidationError(Errc::InvalidPath, "path length does not equal the speech length");
+  if (path.front() != 0 || path.back() != t - 1)
+    throw ValidationError(Errc::InvalidPath, "path must start at 0 and end at t-1");
+  for (int j = 1; j < s; ++j) {
+    const std::int32_t d = path[j] - path[j - 1];
+    if (d == 0 || d == 1) continue;
+    std::ostringstream m;
+    m << "step of " << d << " at frame " << j << "; only 0 and 1 are allowed";
+    throw ValidationError(Errc::InvalidPath, m.str());
+  }
+}
+
+AlignmentMatrix matrix_from_path(const PathVector& path, int t, int s) {
+  validate_path(path, t, s);
+  AlignmentMatrix m(1, t, s);
+  write_path(m, 0, path);
+  return m;
+}
+
+PathVector path_from_matrix(const AlignmentMatrix& m, int b) {
+  const ValidLengths v = m.lengths[b];
+  PathVector path(v.speech, -1);
+  for (std::uint32_t j = 0; j < v.speech; ++j) {
+    int ones = 0;
+    for (std::uint32_t i = 0; i < v.text; ++i)
+      if (m.at(b, static_cast<int>(i), static_cast<int>(j))) {
+        ++ones;
+        path[j] = static_cast<std::int32_t>(i);
+      }
+    if (ones == 1) continue;
+    std::ostringstream msg;
+    msg << "item " << b << ": column " << j << " carries " << ones << " ones, expected 1";
+    throw ValidationError(Errc::InvalidMatrix, msg.str());
+  }
+  return path;
+}
+
+void write_path(AlignmentMatrix& out, int b, const PathVector& path) {
+  for (std::size_t j = 0; j < path.size(); ++j) out.at(b, path[j], static_cast<int>(j)) = 1;
+}
+
+std::vector<PathVector> align_paths(const LikelihoodBatch& batch, const MasConfig& cfg) {
+  const mas_config_t c = to_c(cfg, false);
+  mas_error_t err;
+  int rc = mas_validate_config(&c, &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+  check_containers(batch);
+  const std::vector<uint32_t> l = flat_lengths(batch);
+  std::vector<int32_t> flat(static_cast<std::size_t>(batch.batch) * batch.speech_cap);
+  rc = mas_align_host(batch.values.data(), batch.batch, batch.text_cap, batch.speech_cap, l.data(),
+                      &c, nullptr, flat.data(), &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+  std::vector<PathVector> out(batch.batch);
+  for (int b = 0; b < batch.batch; ++b) {
+    const auto* row = flat.data() + static_cast<std::size_t>(b) * batch.speech_cap;
+    out[b].assign(row, row + batch.lengths[b].speech);
+  }
+  return out;
+}
+
+namespace parallel {
+
+int pad_lanes(int t, LanePadding policy) {
+  if (policy == LanePadding::None || t <= 1) return t;
+  unsigned v = 1;
+  while (v < static_cast<unsigned>(t)) v <<= 1;
+  return static_cast<int>(v);
+}
+
+AlignmentMatrix align_parallel(const LikelihoodBatch& batch, const MasConfig& cfg) {
+  MasConfig c = cfg;
+  c.engine = EngineKind::Parallel;
+  return run(batch, c, false);
+}
+
+AlignmentMatrix detail::align_unchecked(const LikelihoodBatch& batch, const MasConfig& cfg) {
+  MasConfig c = cfg;
+  c.engine = EngineKind::Parallel;
+  return run(batch, c, true);
+}
+
+}  // namespace parallel
+
+namespace reference {
+
+AlignmentMatrix align_reference(const LikelihoodBatch& batch, const MasConfig& cfg) {
+  MasConfig c = cfg;
+  c.engine = EngineKind::Reference;
+  return run(batch, c, false);
+}
+
+AlignmentMatrix detail::align_unchecked(const LikelihoodBatch& batch, const MasConfig& cfg) {
+  MasConfig c = cfg;
+  c.engine = EngineKind::Reference;
+  return run(batch, c, true);
+}
+
+}  // namespace reference
+
+}  // namespace monoalign
