@@ -45,7 +45,8 @@ namespace {
 
 constexpr int kSubCols = 32;                            // columns per TMA box / dirs word
 constexpr int kSubBytes = kRowsPerWarp * kSubCols * 4;  // 8 KiB: [parity][32 rows][32 cols]
-constexpr int kSlotBytes = kStageCols * 4;              // one FIFO slot (64 floats)
+constexpr int kSlotBytes = kQuadCols * 4;               // one FIFO slot (16 floats)
+constexpr int kFifoIters = kFifoSlots / (kStageCols / kQuadCols);  // FIFO depth in iterations
 #ifndef MAS_L2_AHEAD
 #define MAS_L2_AHEAD 0
 #endif
@@ -82,7 +83,7 @@ struct Lane {
 // Four steps (one LDS.128 per row parity) of the DP for one warp.
 template <int MODE, bool GENERIC, int SUB, int A4>
 __device__ __forceinline__ bool fwd_group(const uint8_t* __restrict__ tile, const uint32_t (&coff)[8],
-                                         const float4* __restrict__ slot, float (&ex)[kStageCols],
+                                         const float4* __restrict__ slot, float (&ex)[kQuadCols],
                                          Lane& L, uint32_t& w0, uint32_t& w1, bool is31,
                                          int srclane, int c_base, int nvalid, int row0, float mnv,
                                          bool row0_is_zero, uint32_t one, float zero) {
@@ -90,7 +91,7 @@ __device__ __forceinline__ bool fwd_group(const uint8_t* __restrict__ tile, cons
   if (GENERIC && ug >= nvalid) return false;
   const float4 qa = *reinterpret_cast<const float4*>(tile + coff[A4]);
   const float4 qb = *reinterpret_cast<const float4*>(tile + 4096 + coff[A4]);
-  const float4 vv = slot[ug / 4];  // producer's bottom row, columns c-1 .. c+2
+  const float4 vv = slot[A4 & 3];  // producer's bottom row, columns c-1 .. c+2
   const float qs0[4] = {qa.x, qa.y, qa.z, qa.w};
   const float qs1[4] = {qb.x, qb.y, qb.z, qb.w};
   const float bnds[4] = {L.vlast, vv.x, vv.y, vv.z};
@@ -131,7 +132,7 @@ __device__ __forceinline__ bool fwd_group(const uint8_t* __restrict__ tile, cons
     }
     fold_nonfinite(L.acc, q0, zero);
     fold_nonfinite(L.acc, q1, zero);
-    ex[ug + e] = n1;
+    ex[(A4 & 3) * 4 + e] = n1;
     L.o0 = n0;
     L.o1 = n1;
   }
@@ -139,41 +140,87 @@ __device__ __forceinline__ bool fwd_group(const uint8_t* __restrict__ tile, cons
   return true;
 }
 
-// 32 columns (one TMA box, one direction word per row) of the DP for one
-// warp.  GENERIC handles column 0, reference-engine masking (cells with
-// c < i stay exactly max_neg_val, reference.cpp:12-17, :30) and a partial
-// last iteration; the steady-state instantiation has none of those checks.
-// Per step the ALU pipe carries FMNMX x2, FSETP x2 and the shuffle select,
-// the FMA pipe FADD x2, the bit IMADs and the NonFinite FFMAs.
-template <int MODE, bool GENERIC, int SUB>
-__device__ __forceinline__ void fwd_sub(const uint8_t* __restrict__ tile, const uint32_t (&coff)[8],
-                                        const float4* __restrict__ slot, float (&ex)[kStageCols],
-                                        Lane& L, uint32_t& w0, uint32_t& w1, bool is31,
-                                        int srclane, int c_base, int nvalid, int row0, float mnv,
-                                        bool row0_is_zero, uint32_t one, float zero) {
-  w0 = 0u;
-  w1 = 0u;
-#define MAS_GROUP(A)                                                                              \
-  if (!fwd_group<MODE, GENERIC, SUB, A>(tile, coff, slot, ex, L, w0, w1, is31, srclane, c_base, \
-                                        nvalid, row0, mnv, row0_is_zero, one, zero))            \
-    return;
-  MAS_GROUP(0) MAS_GROUP(1) MAS_GROUP(2) MAS_GROUP(3) MAS_GROUP(4) MAS_GROUP(5) MAS_GROUP(6)
-  MAS_GROUP(7)
+// Endpoints of a warp's boundary-row FIFOs: the one it consumes (its
+// producer is the warp above) and the one it feeds (in the warp below,
+// possibly in another CTA of the cluster: cluster shared-window addresses).
+struct Fifo {
+  uint32_t full, empty;            // my FIFO's "full" barriers, my "empty" barriers
+  uint32_t next_fifo, next_full;   // consumer's slots and "full" barriers
+  uint32_t prev_empty, prev_sink;  // producer's "empty" barriers and release sink
+  const uint8_t* buf;              // my FIFO's slots (generic pointer)
+  bool has_in, has_out;
+};
+
+// One quad = 16 columns = 4 groups, with the FIFO hand-off around it: wait
+// for the producer's 16 bottom-row values, compute, release the slot, and
+// (lane 31) pass this warp's own 16 bottom-row values on.  Handing off per
+// 16 columns keeps each warp only ~16 columns behind the warp above, so the
+// wavefront across an item's warps fills and drains 4x faster than with
+// whole-iteration hand-offs.  GENERIC handles column 0, reference-engine
+// masking (cells with c < i stay exactly max_neg_val, reference.cpp:12-17,
+// :30) and a partial last iteration; the steady-state instantiation has
+// none of those checks.  Per step the ALU pipe carries FMNMX x2, FSETP x2
+// and the shuffle select, the FMA pipe FADD x2, the bit IMADs and the
+// NonFinite FFMAs.
+template <int MODE, bool GENERIC, int K>
+__device__ __forceinline__ bool fwd_quad(const uint8_t* stage, const uint32_t (&coff)[8],
+                                        const Fifo& F, float (&ex)[kQuadCols], Lane& L,
+                                        uint32_t (&w)[4], bool& ready, bool more, bool is31,
+                                        int lane, int srclane, int q, int c_base, int nvalid,
+                                        int row0, float mnv, bool row0_is_zero, uint32_t one,
+                                        float zero) {
+  constexpr int SUB = K / 2;
+  if (GENERIC && K * kQuadCols >= nvalid) return false;
+  const int fs = q & (kFifoSlots - 1);
+  // The producer's 16 values arrive as 64 bytes of st.async on full[fs]
+  // (armed with expect_tx one quad earlier).  Usually the look-ahead probe
+  // made during the previous quad already saw them land; otherwise block.
+  if (F.has_in && !ready) mbar_wait(F.full + 8u * fs, static_cast<uint32_t>(q / kFifoSlots) & 1u);
+  // Arm and probe the next quad's slot now, in straight-line code so the
+  // probe's result is only consumed after this quad's 16 columns.  (A warp
+  // without a producer probes its own never-armed barrier: harmless.)
+  const bool next = K < 3 ? (!GENERIC || (K + 1) * kQuadCols < nvalid) : more;
+  const int q1 = q + 1;
+  const uint32_t bar1 = F.full + 8u * (q1 & (kFifoSlots - 1));
+  if (lane == 0 && next && F.has_in) mbar_arrive_expect_tx(bar1, kSlotBytes);
+  const bool probe = mbar_test_wait(bar1, static_cast<uint32_t>(q1 / kFifoSlots) & 1u);
+  const uint8_t* tile = stage + SUB * kSubBytes;
+  const float4* slot = reinterpret_cast<const float4*>(F.buf + fs * kSlotBytes);
+  bool ok = true;
+#define MAS_GROUP(A)                                                                             \
+  if (ok)                                                                                        \
+    ok = fwd_group<MODE, GENERIC, SUB, A>(tile, coff, slot, ex, L, w[2 * SUB], w[2 * SUB + 1], \
+                                          is31, srclane, c_base, nvalid, row0, mnv,            \
+                                          row0_is_zero, one, zero);
+  MAS_GROUP((K & 1) * 4 + 0) MAS_GROUP((K & 1) * 4 + 1) MAS_GROUP((K & 1) * 4 + 2)
+  MAS_GROUP((K & 1) * 4 + 3)
 #undef MAS_GROUP
+  ready = probe;
+  if (F.has_out && is31) {
+    // The consumer's slot is free: checked once per iteration (fwd loop).
+    const uint32_t dst = F.next_fifo + static_cast<uint32_t>(fs * kSlotBytes);
+    const uint32_t fbar = F.next_full + 8u * fs;
+#pragma unroll
+    for (int q4 = 0; q4 < kQuadCols / 4; ++q4)
+      st_async_v4(dst + 16u * q4, ex[4 * q4], ex[4 * q4 + 1], ex[4 * q4 + 2], ex[4 * q4 + 3], fbar);
+  }
+  return ok;
 }
 
+// One iteration: 64 columns = one TMA stage = two direction words per row.
 template <int MODE, bool GENERIC>
 __device__ __forceinline__ void fwd_iter(const uint8_t* stage, const uint32_t (&coff)[8],
-                                         const float4* slot, float (&ex)[kStageCols], Lane& L,
-                                         uint32_t (&w)[4], bool is31, int srclane, int c_base,
-                                         int nvalid, int row0, float mnv, bool row0_is_zero,
-                                         uint32_t one, float zero) {
-  w[2] = 0u;
-  w[3] = 0u;
-  fwd_sub<MODE, GENERIC, 0>(stage, coff, slot, ex, L, w[0], w[1], is31, srclane, c_base, nvalid,
-                            row0, mnv, row0_is_zero, one, zero);
-  fwd_sub<MODE, GENERIC, 1>(stage + kSubBytes, coff, slot, ex, L, w[2], w[3], is31, srclane,
-                            c_base, nvalid, row0, mnv, row0_is_zero, one, zero);
+                                         const Fifo& F, float (&ex)[kQuadCols], Lane& L,
+                                         uint32_t (&w)[4], bool& ready, bool more, bool is31,
+                                         int lane, int srclane, int q0, int c_base, int nvalid,
+                                         int row0, float mnv, bool row0_is_zero, uint32_t one,
+                                         float zero) {
+#define MAS_QUAD(K)                                                                              \
+  if (!fwd_quad<MODE, GENERIC, K>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,   \
+                                  q0 + K, c_base, nvalid, row0, mnv, row0_is_zero, one, zero)) \
+    return;
+  MAS_QUAD(0) MAS_QUAD(1) MAS_QUAD(2) MAS_QUAD(3)
+#undef MAS_QUAD
 }
 
 // L2 prefetch of a whole stage (no shared memory, no completion): issued
@@ -233,7 +280,7 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
   if (!has_in) {
     // The first warp of an item has no producer: its FIFO permanently holds
     // the value above row 0 (max_neg_val, or -inf for reference.cpp:20-24).
-    for (int k = lane; k < kFifoSlots * kStageCols; k += 32)
+    for (int k = lane; k < kFifoSlots * kQuadCols; k += 32)
       reinterpret_cast<float*>(my_fifo)[k] = a.row0_up;
   }
   // A zeroed 64 x 64-byte tile, the TMA-store source of the fused output fill.
@@ -308,10 +355,24 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
     L.o1 = 0.0f;
     L.acc = 0.0f;
     L.vlast = a.row0_up;
-    float ex[kStageCols];
+    float ex[kQuadCols];
 #pragma unroll
-    for (int u = 0; u < kStageCols; ++u) ex[u] = 0.0f;
+    for (int u = 0; u < kQuadCols; ++u) ex[u] = 0.0f;
     uint32_t* dirs_ptr = a.dirs + static_cast<size_t>(b) * a.M * a.T_alloc + i0 + 2 * lane;
+    Fifo F;
+    F.full = my_full;
+    F.empty = my_empty;
+    F.next_fifo = next_fifo;
+    F.next_full = next_full;
+    F.prev_empty = prev_empty;
+    F.prev_sink = prev_sink;
+    F.buf = my_fifo;
+    F.has_in = has_in;
+    F.has_out = has_out;
+
+    // Quad 0's slot is armed here; every later one by the quad before it.
+    bool ready = false;
+    if (has_in && lane == 0) mbar_arrive_expect_tx(my_full, kSlotBytes);
 
     // Ring position of iteration m (slot, parity) and the slot refilled at
     // its start (iteration m + N - 1 goes where iteration m - 1 was).
@@ -319,8 +380,6 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
     uint32_t par = 0;
     int free_slot = N - 1;
     for (int m = 0; m < nit; ++m) {
-      const int fs = m & (kFifoSlots - 1);
-      const uint32_t fpar = static_cast<uint32_t>(m / kFifoSlots) & 1u;
       if (m + N - 1 < nit) {
         __syncwarp();
         if (lane == 0) {
@@ -333,37 +392,37 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
             prefetch_stage(&tm0, &tm1, (m + N - 1 + kL2Ahead) * kStageCols, row_pair);
         }
       }
-      if (has_in && lane == 0) {
-        // Producer's iteration m arrives as 256 bytes of st.async on full[fs].
-        mbar_arrive_expect_tx(my_full + 8u * fs, kSlotBytes);
-      }
       mbar_wait(bar0 + 8u * slot, par);
-      if (has_in) mbar_wait(my_full + 8u * fs, fpar);
 
       const uint8_t* stage = ring_ptr + slot * kStageBytes;
-      const float4* fslot = reinterpret_cast<const float4*>(my_fifo + fs * kSlotBytes);
       const int c_base = m * kStageCols;
       const int nvalid = s_b - c_base < kStageCols ? s_b - c_base : kStageCols;
-      uint32_t w[4];
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
       const bool generic =
           m == 0 || nvalid < kStageCols || (MODE == 1 && c_base < i0 + kRowsPerWarp - 1);
+      if (has_out && is31 && m >= kFifoIters) {
+        // This iteration's slots are free once the consumer released
+        // iteration m - kFifoIters (4-byte st.async on empty[m % kFifoIters]).
+        const uint32_t eb = my_empty + 8u * static_cast<uint32_t>(m % kFifoIters);
+        mbar_arrive_expect_tx(eb, 4u);
+        mbar_wait(eb, (static_cast<uint32_t>(m / kFifoIters) & 1u) ^ 1u);
+      }
+      const bool more = m + 1 < nit;
       if (generic) {
-        fwd_iter<MODE, true>(stage, coff, fslot, ex, L, w, is31, srclane, c_base, nvalid, row0,
-                             mnv, row0_is_zero, one, zero);
+        fwd_iter<MODE, true>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane, 4 * m,
+                             c_base, nvalid, row0, mnv, row0_is_zero, one, zero);
       } else {
-        fwd_iter<MODE, false>(stage, coff, fslot, ex, L, w, is31, srclane, c_base, kStageCols,
-                              row0, mnv, row0_is_zero, one, zero);
+        fwd_iter<MODE, false>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane, 4 * m,
+                              c_base, kStageCols, row0, mnv, row0_is_zero, one, zero);
       }
       if (has_in) {
-        // Every value read from slot fs has been consumed above.
+        // Every value of this iteration's slots has been consumed above:
+        // release them with a 4-byte st.async completing the producer's
+        // "empty" transaction (prompt, fence-free signalling).
         __syncwarp();
-#ifdef MAS_EMPTY_RELAXED
-        if (lane == 0) mbar_arrive_remote_relaxed(prev_empty + 8u * fs);
-#else
-        // Release the slot with a 4-byte st.async that completes the
-        // producer's "empty" transaction (prompt, fence-free signalling).
-        if (lane == 0) st_async_b32(prev_sink, static_cast<uint32_t>(m), prev_empty + 8u * fs);
-#endif
+        if (lane == 0)
+          st_async_b32(prev_sink, static_cast<uint32_t>(m),
+                       prev_empty + 8u * static_cast<uint32_t>(m % kFifoIters));
       }
 
       // The backtrack never needs (and must never take) a step above row 0
@@ -380,21 +439,6 @@ __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
       if (2 * m + 1 < a.M) st_global_v2_evict_last(dirs_ptr + a.T_alloc, w[2], w[3], pol_dir);
       dirs_ptr += 2 * static_cast<size_t>(a.T_alloc);
 
-      if (has_out && is31) {
-        // Slot fs of the consumer is free once it released iteration m - F.
-        if (m >= kFifoSlots) {
-#ifndef MAS_EMPTY_RELAXED
-          mbar_arrive_expect_tx(my_empty + 8u * fs, 4u);
-#endif
-          mbar_wait(my_empty + 8u * fs, fpar ^ 1u);
-        }
-        const uint32_t dst = next_fifo + static_cast<uint32_t>(fs * kSlotBytes);
-        const uint32_t fbar = next_full + 8u * fs;
-#pragma unroll
-        for (int q4 = 0; q4 < kStageCols / 4; ++q4)
-          st_async_v4(dst + 16u * q4, ex[4 * q4], ex[4 * q4 + 1], ex[4 * q4 + 2], ex[4 * q4 + 3],
-                      fbar);
-      }
       if (zero_fill && lane == 0) {
         // Fused zero fill of the output tile this warp covers (the backtrack
         // scatters the ones later): one asynchronous TMA store of the zero

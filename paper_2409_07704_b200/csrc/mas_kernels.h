@@ -15,10 +15,11 @@ constexpr int kRowsPerLane = 2;
 constexpr int kRowsPerWarp = 32 * kRowsPerLane;  // 64
 constexpr int kStageCols = 64;                              // columns per iteration / TMA stage
 constexpr int kStageBytes = kRowsPerWarp * kStageCols * 4;  // 16 KiB
+constexpr int kQuadCols = 16;  // columns per boundary-row FIFO hand-off
 #ifndef MAS_FIFO_SLOTS
-#define MAS_FIFO_SLOTS 8
+#define MAS_FIFO_SLOTS 32
 #endif
-constexpr int kFifoSlots = MAS_FIFO_SLOTS;  // boundary-row FIFO depth, in 64-column iterations
+constexpr int kFifoSlots = MAS_FIFO_SLOTS;  // boundary-row FIFO depth, in 16-column quads
 constexpr int kMaxWarpsPerCta = 8;
 constexpr int kMaxClusterCtas = 16;
 
