@@ -192,14 +192,56 @@ bool encode_out_map(uint8_t* out, int64_t rows, int64_t S, CUtensorMap* m) {
 
 
 struct Geometry {
-  int W = 1, K = 1, N = 2, L = 256, Kseg = 1, T_alloc = 64, M = 1;
+  int R = 4;  // text rows per lane: 4 (mas_fwd4.cu, default) or 2 (mas_fwd.cu)
+  int W = 1, K = 1, N = 2, L = 256, Kseg = 1, T_alloc = 128, M = 1;
 };
 
+int forward_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("MAS_FWD");  // A/B switch between the two K1 kernels
+    return e && e[0] == '2' ? 2 : 4;
+  }();
+  return v;
+}
+
 bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t budget = 220 * 1024;
+  g->R = forward_variant();
+  g->M = (S_cap + 31) / 32;
+  g->L = 256;
+  g->Kseg = (S_cap + g->L - 1) / g->L;
+  if (g->R == 4) {
+    // 128 rows per warp.  Few warps per CTA spreads an item over more SMs
+    // (one warp per SM sub-partition is all the DP needs); use 4 per CTA
+    // only when 2 would not fit the whole batch in one wave of CTAs.
+    const int warps = std::max(1, (t_max + 127) / 128);
+    if (warps <= 2) {
+      g->W = warps;
+      g->K = 1;
+    } else {
+      g->W = 2;
+      g->K = (warps + 1) / 2;
+      if (g->K > mas::kMaxClusterCtas || static_cast<int64_t>(B) * g->K > sms) {
+        g->W = 4;
+        g->K = (warps + 3) / 4;
+      }
+      if (g->K > mas::kMaxClusterCtas) return false;
+    }
+    int N = 4;
+    while (N > 2 && mas::fwd4_smem_bytes(g->W, N) > budget) --N;
+    g->N = N;
+    g->T_alloc = g->K * g->W * 128;
+    return true;
+  }
   const int warps = std::max(1, (t_max + mas::kRowsPerWarp - 1) / mas::kRowsPerWarp);
   // One warp per SM sub-partition (4 per CTA), clusters of up to 16 CTAs;
   // 6 warps x 2 stages for the longest texts.
-  const size_t budget = 220 * 1024;
   if (warps <= 4) {
     g->K = 1;
     g->W = warps;
@@ -212,16 +254,42 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
   } else {
     return false;
   }
-  (void)B;
   int N = 8;
   while (N > 2 && mas::fwd_smem_bytes(g->W, N) > budget) --N;
   g->N = N;
   g->T_alloc = g->K * g->W * mas::kRowsPerWarp;
-  g->M = (S_cap + 31) / 32;
-  // Output segment written by one writer CTA: [T_cap x L] bytes.
-  g->L = 256;
-  g->Kseg = (S_cap + g->L - 1) / g->L;
   return true;
+}
+
+// The input [B*T_pad][pitch] as a 3-D tensor {columns, row groups of four,
+// row residue mod 4}: one {32, 32, 4} box is a 128-row x 32-column stage of
+// mas_fwd4.cu laid out [residue][group][column] (128-byte swizzle).
+bool encode_map4(const float* q, int64_t pitch, int64_t rows_total, int64_t S, CUtensorMap* m) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(rows_total / 4),
+                              4};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(4 * pitch * 4),
+                                 static_cast<cuuint64_t>(pitch * 4)};
+  const cuuint32_t box[3] = {32, 32, 4};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(q), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// The uint8 output as {columns, rows} with 32 x 128 boxes (mas_fwd4.cu's
+// fused zero fill).
+bool encode_out_map4(uint8_t* out, int64_t rows, int64_t S, CUtensorMap* m) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(S)};
+  const cuuint32_t box[2] = {32, 128};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, out, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -371,7 +439,7 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
   if (!choose_geometry(batch, std::max(t_max, 1), speech_cap, &p->geo)) {
     delete p;
     return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
-                     "text length above 6144 rows is not supported by the device path");
+                     "text length above 8192 rows is not supported by the device path");
   }
   const Geometry& g = p->geo;
   auto fail = [&](cudaError_t e, const char* what) {
@@ -379,7 +447,8 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
     return cuda_error(err, e, what);
   };
   cudaError_t e;
-  if ((e = mas::fwd_configure(g.W, g.N, g.K)) != cudaSuccess) return fail(e, "fwd_configure");
+  if ((e = g.R == 4 ? mas::fwd4_configure() : mas::fwd_configure(g.W, g.N, g.K)) != cudaSuccess)
+    return fail(e, "fwd_configure");
   if ((e = mas::bt_configure(g.T_alloc, g.L)) != cudaSuccess) return fail(e, "bt_configure");
   if ((e = pool_setup(p->device)) != cudaSuccess) return fail(e, "memory pool setup");
   // Workspace from the stream-ordered pool on this thread's default stream;
@@ -418,7 +487,7 @@ extern "C" {
 int mas_plan_launches(const mas_plan_t* p) { return p ? p->launches : 0; }
 
 void mas_plan_geometry(const mas_plan_t* p, int32_t geom[5]) {
-  geom[0] = mas::kRowsPerWarp;
+  geom[0] = 32 * p->geo.R;
   geom[1] = p->geo.W;
   geom[2] = p->geo.K;
   geom[3] = p->geo.N;
@@ -433,14 +502,17 @@ namespace {
 // plan's batch.  d_values / d_out / d_paths are the whole batch's buffers.
 int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_values,
                   uint8_t* d_out, int32_t* d_paths, cudaStream_t stream, mas_error_t* err) {
-  if ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (p->pitch & 3) != 0 || (p->T_pad & 1))
+  if ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (p->pitch & 3) != 0 || (p->T_pad & 3))
     return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
-                     "device layout needs 16-byte base, pitch % 4 == 0 and even text_cap");
+                     "device layout needs a 16-byte base, pitch % 4 == 0 and text_cap % 4 == 0");
   const Geometry& g = p->geo;
   int nfwd = 0, nbt = 0;
   if (parts & MAS_PART_FORWARD) {
     CUtensorMap tm0, tm1;
-    if (!encode_maps(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, &tm0, &tm1))
+    const bool r4 = g.R == 4;
+    if (r4 ? !encode_map4(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, &tm0)
+           : !encode_maps(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, &tm0,
+                          &tm1))
       return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled failed");
     MAS_CUDA(cudaMemsetAsync(p->d_flags + b0, 0, sizeof(int) * nb, stream),
              "cudaMemsetAsync(flags)");
@@ -473,14 +545,19 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     }
     CUtensorMap tm_out;
     std::memset(&tm_out, 0, sizeof(tm_out));
-    if (fused_zero && !encode_out_map(d_out, static_cast<int64_t>(p->B) * p->T, p->S, &tm_out))
+    if (fused_zero && !(r4 ? encode_out_map4(d_out, static_cast<int64_t>(p->B) * p->T, p->S, &tm_out)
+                           : encode_out_map(d_out, static_cast<int64_t>(p->B) * p->T, p->S,
+                                            &tm_out)))
       return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled(out) failed");
     fa.zero_fill = fused_zero ? 1 : 0;
     fa.one = 1u;
     fa.zero = 0.0f;
     fa.T_cap = p->T;
     fa.S_cap = p->S;
-    MAS_CUDA(mas::launch_fwd(p->mode, tm0, tm1, tm_out, fa, nb, stream), "launch mas_fwd");
+    if (r4)
+      MAS_CUDA(mas::launch_fwd4(p->mode, tm0, tm_out, fa, nb, stream), "launch mas_fwd4");
+    else
+      MAS_CUDA(mas::launch_fwd(p->mode, tm0, tm1, tm_out, fa, nb, stream), "launch mas_fwd");
     nfwd = 1;
   }
   if ((parts & MAS_PART_BACKTRACK) && (d_out || d_paths)) {
@@ -571,9 +648,9 @@ int mas_align_device(const float* d_values, int64_t row_pitch, int32_t batch, in
   const float* q = d_values;
   float* scratch = nullptr;
   if ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (row_pitch & 3) != 0 ||
-      (text_cap & 1) != 0) {
+      (text_cap & 3) != 0) {
     // Re-pitch into an aligned [B][T_pad][pitch'] copy the TMA path accepts.
-    const int T_pad = (text_cap + 1) & ~1;
+    const int T_pad = (text_cap + 3) & ~3;
     const int64_t pitch2 = (static_cast<int64_t>(speech_cap) + 3) & ~int64_t(3);
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
                                     static_cast<size_t>(batch) * T_pad * pitch2 * 4, stream);
@@ -623,7 +700,7 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
     rc = validate_dims(batch, text_cap, speech_cap, err);
     if (rc) return rc;
   }
-  const int T_pad = (text_cap + 1) & ~1;
+  const int T_pad = (text_cap + 3) & ~3;
   const int64_t pitch = (static_cast<int64_t>(speech_cap) + 3) & ~int64_t(3);
   const size_t q_item = static_cast<size_t>(T_pad) * pitch;  // floats per item on the device
   const size_t o_item = static_cast<size_t>(text_cap) * speech_cap;

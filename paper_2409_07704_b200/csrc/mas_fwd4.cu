@@ -1,0 +1,502 @@
+// mas_fwd4.cu -- K1 with four text rows per lane (128 rows per warp).
+//
+// Same restatement and output as mas_fwd.cu (parallel engine relax_column,
+// src/parallel.cpp:25-31; reference engine forward_reference,
+// src/reference.cpp:9-36; one direction bit per cell,
+// bit(i, c) = Q[i-1][c] > Q[i][c], strict as backtrack.hpp:26), with the
+// work per lane doubled:
+//   * lane k of warp g owns rows 128 g + 4k .. 128 g + 4k + 3.  Per column
+//     only the first of the four needs the row above from another lane (one
+//     SHFL + one FSEL per four cells instead of per two), and the four rows
+//     are four independent FMNMX/FADD chains, so one warp per SM
+//     sub-partition issues at ~2x the rate of the two-row kernel;
+//   * q is staged per warp in 32-column stages by ONE TMA box
+//     {32 columns, 32 lane groups, 4 row residues} of a 3-D view of the
+//     input (rows split by i mod 4), 128-byte swizzle: every LDS.128 of a
+//     residue tile is conflict-free;
+//   * direction words: four rows x one word per 32-column stage, stored as
+//     one 16-byte STG per lane (L2 evict_last);
+//   * boundary row between warps: the same 16-column FIFO hand-offs with
+//     look-ahead mbarrier probes as mas_fwd.cu (st.async / DSMEM across the
+//     CTAs of a cluster);
+//   * NonFinite (types.cpp:107-115) folded as max.NaN over |q| (one
+//     3-input FMNMX per two values); the output's zero fill rides along as
+//     TMA stores of a zero tile.
+#include <cstdio>
+#include <mutex>
+
+#include "mas_kernels.h"
+#include "mas_ptx.cuh"
+
+namespace mas {
+
+namespace {
+
+constexpr int R4 = 4;                       // rows per lane
+constexpr int kRows4 = 32 * R4;             // rows per warp
+constexpr int kCols4 = 32;                  // columns per stage / direction word
+constexpr int kStage4 = kRows4 * kCols4 * 4;  // 16 KiB: [4 residues][32 groups][32 cols]
+constexpr int kQuad = kQuadCols;            // 16 columns per FIFO hand-off
+constexpr int kSlot4 = kQuad * 4;           // 64-byte FIFO slot
+constexpr int kQuadsPerStage = kCols4 / kQuad;
+constexpr int kFifoIt4 = kFifoSlots / kQuadsPerStage;  // FIFO depth in stages
+
+struct Smem4 {
+  uint32_t ring, bars, ebars, full, empty, sink, fifo, zero, total;
+};
+
+__host__ __device__ inline Smem4 smem4_layout(int W, int N) {
+  Smem4 L;
+  L.ring = 0;
+  L.bars = static_cast<uint32_t>(W * N * kStage4);
+  L.ebars = L.bars + static_cast<uint32_t>(W * N * 8);
+  L.full = L.ebars + static_cast<uint32_t>(W * N * 8);
+  L.empty = L.full + static_cast<uint32_t>(W * kFifoSlots * 8);
+  L.sink = L.empty + static_cast<uint32_t>(W * kFifoIt4 * 8);
+  L.fifo = (L.sink + static_cast<uint32_t>(W * 16) + 127u) & ~127u;
+  L.zero = L.fifo + static_cast<uint32_t>(W * kFifoSlots * kSlot4);
+  L.total = L.zero + static_cast<uint32_t>(kRows4 * kCols4);  // uint8 zero tile
+  return L;
+}
+
+struct Lane4 {
+  float o[R4];  // Q of the lane's rows at the previous column
+  float acc;    // max.NaN of |q|: NaN / +inf iff a non-finite q was seen
+  float vlast;  // producer's bottom row at the previous column
+};
+
+struct Fifo4 {
+  uint32_t full, empty;            // my FIFO's "full" barriers, my "empty" barriers
+  uint32_t next_fifo, next_full;   // consumer's slots and "full" barriers
+  uint32_t prev_empty, prev_sink;  // producer's "empty" barriers and release sink
+  const uint8_t* buf;              // my FIFO's slots
+  bool has_in, has_out;
+};
+
+__device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+template <int BIT>
+__device__ __forceinline__ void bit_gt(uint32_t& w, float a, float b, uint32_t one) {
+  set_bit_if_gt<BIT>(w, a, b, one);
+}
+
+// Four columns (one LDS.128 per row residue, one of the FIFO slot) of the
+// DP for one warp.  U0 = index of the first column within the stage.
+template <int MODE, bool GENERIC, int U0>
+__device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uint32_t coff,
+                                          const float4* __restrict__ slot, float (&ex)[kQuad],
+                                          Lane4& L, uint32_t (&w)[R4], bool is31, int srclane,
+                                          int c_base, int nvalid, int row0, float mnv,
+                                          bool row0_is_zero, uint32_t one) {
+  if (GENERIC && U0 >= nvalid) return false;
+  float4 qv[R4];
+#pragma unroll
+  for (int r = 0; r < R4; ++r)
+    qv[r] = *reinterpret_cast<const float4*>(tile + r * 4096 + coff);
+  const float4 vv = slot[(U0 % kQuad) / 4];  // producer's bottom row
+  const float bnds[4] = {L.vlast, vv.x, vv.y, vv.z};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (GENERIC && U0 + e >= nvalid) return false;
+    float q[R4];
+#pragma unroll
+    for (int r = 0; r < R4; ++r) q[r] = e == 0 ? qv[r].x : e == 1 ? qv[r].y : e == 2 ? qv[r].z : qv[r].w;
+    const float send = is31 ? bnds[e] : L.o[R4 - 1];
+    const float up = __shfl_sync(0xffffffffu, send, srclane);
+    constexpr int bitpos = 31 - (U0 + 0);  // adjusted per e below
+    switch (U0 + e) {  // compile-time bit position 31 - column-in-word
+#define MAS_B4(U)                                   \
+  case U:                                           \
+    bit_gt<31 - U>(w[0], up, L.o[0], one);          \
+    bit_gt<31 - U>(w[1], L.o[0], L.o[1], one);      \
+    bit_gt<31 - U>(w[2], L.o[1], L.o[2], one);      \
+    bit_gt<31 - U>(w[3], L.o[2], L.o[3], one);      \
+    break;
+      MAS_B4(0) MAS_B4(1) MAS_B4(2) MAS_B4(3) MAS_B4(4) MAS_B4(5) MAS_B4(6) MAS_B4(7)
+      MAS_B4(8) MAS_B4(9) MAS_B4(10) MAS_B4(11) MAS_B4(12) MAS_B4(13) MAS_B4(14) MAS_B4(15)
+      MAS_B4(16) MAS_B4(17) MAS_B4(18) MAS_B4(19) MAS_B4(20) MAS_B4(21) MAS_B4(22) MAS_B4(23)
+      MAS_B4(24) MAS_B4(25) MAS_B4(26) MAS_B4(27) MAS_B4(28) MAS_B4(29) MAS_B4(30) MAS_B4(31)
+#undef MAS_B4
+    }
+    (void)bitpos;
+    float n[R4];
+    n[0] = q[0] + fmaxf(up, L.o[0]);
+#pragma unroll
+    for (int r = 1; r < R4; ++r) n[r] = q[r] + fmaxf(L.o[r - 1], L.o[r]);
+    if (GENERIC) {
+      const int c = c_base + U0 + e;
+      if (MODE == 1) {
+#pragma unroll
+        for (int r = 0; r < R4; ++r)
+          if (c < row0 + r) n[r] = mnv;
+      }
+      if (c == 0) {  // first column: parallel.cpp:73-75 / reference.cpp:16-24
+        n[0] = row0_is_zero ? q[0] : mnv;
+#pragma unroll
+        for (int r = 1; r < R4; ++r) n[r] = mnv;
+      }
+    }
+    fold_abs_max_nan(L.acc, q[0], q[1]);
+    fold_abs_max_nan(L.acc, q[2], q[3]);
+    ex[(U0 % kQuad) + e] = n[R4 - 1];
+#pragma unroll
+    for (int r = 0; r < R4; ++r) L.o[r] = n[r];
+  }
+  L.vlast = vv.w;
+  return true;
+}
+
+// 16 columns with the FIFO hand-off around them (see mas_fwd.cu fwd_quad).
+template <int MODE, bool GENERIC, int K>
+__device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (&coff)[8],
+                                         const Fifo4& F, float (&ex)[kQuad], Lane4& L,
+                                         uint32_t (&w)[R4], bool& ready, bool more, bool is31,
+                                         int lane, int srclane, int q, int c_base, int nvalid,
+                                         int row0, float mnv, bool row0_is_zero, uint32_t one) {
+  if (GENERIC && K * kQuad >= nvalid) return false;
+  const int fs = q & (kFifoSlots - 1);
+  if (F.has_in && !ready) mbar_wait(F.full + 8u * fs, static_cast<uint32_t>(q / kFifoSlots) & 1u);
+  const bool next = K + 1 < kQuadsPerStage ? (!GENERIC || (K + 1) * kQuad < nvalid) : more;
+  const int q1 = q + 1;
+  const uint32_t bar1 = F.full + 8u * (q1 & (kFifoSlots - 1));
+  if (lane == 0 && next && F.has_in) mbar_arrive_expect_tx(bar1, kSlot4);
+  const bool probe = mbar_test_wait(bar1, static_cast<uint32_t>(q1 / kFifoSlots) & 1u);
+  const float4* slot = reinterpret_cast<const float4*>(F.buf + fs * kSlot4);
+  bool ok = true;
+#define MAS_G4(A)                                                                              \
+  if (ok)                                                                                      \
+    ok = fwd4_group<MODE, GENERIC, K * kQuad + 4 * A>(stage, coff[(K * kQuad / 4 + A) & 7],   \
+                                                      slot, ex, L, w, is31, srclane, c_base, \
+                                                      nvalid, row0, mnv, row0_is_zero, one);
+  MAS_G4(0) MAS_G4(1) MAS_G4(2) MAS_G4(3)
+#undef MAS_G4
+  ready = probe;
+  if (F.has_out && is31) {
+    const uint32_t dst = F.next_fifo + static_cast<uint32_t>(fs * kSlot4);
+    const uint32_t fbar = F.next_full + 8u * fs;
+#pragma unroll
+    for (int q4 = 0; q4 < kQuad / 4; ++q4)
+      st_async_v4(dst + 16u * q4, ex[4 * q4], ex[4 * q4 + 1], ex[4 * q4 + 2], ex[4 * q4 + 3], fbar);
+  }
+  return ok;
+}
+
+template <int MODE, bool GENERIC>
+__device__ __forceinline__ void fwd4_stage(const uint8_t* stage, const uint32_t (&coff)[8],
+                                          const Fifo4& F, float (&ex)[kQuad], Lane4& L,
+                                          uint32_t (&w)[R4], bool& ready, bool more, bool is31,
+                                          int lane, int srclane, int q0, int c_base, int nvalid,
+                                          int row0, float mnv, bool row0_is_zero, uint32_t one) {
+  if (!fwd4_quad<MODE, GENERIC, 0>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane, q0,
+                                   c_base, nvalid, row0, mnv, row0_is_zero, one))
+    return;
+  fwd4_quad<MODE, GENERIC, 1>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane, q0 + 1,
+                              c_base, nvalid, row0, mnv, row0_is_zero, one);
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
+      : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
+    mas_fwd4_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tm_out,
+                    const FwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_addr(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* const sbase = smem_raw + (base - raw);
+  const int W = a.W;  // compute warps; warp W is the CTA's TMA producer
+  const int N = a.N;
+  const Smem4 SL = smem4_layout(W, N);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int crank = static_cast<int>(cluster_ctarank());
+  const int b = a.b0 + static_cast<int>(blockIdx.x) / a.K;
+  const int t_b = static_cast<int>(a.lengths[2 * b]);
+  const int s_b = static_cast<int>(a.lengths[2 * b + 1]);
+  const int nit = (s_b + kCols4 - 1) / kCols4;
+
+  if (warp < W) {
+    const int g = crank * W + warp;
+    const bool has_in = g > 0;
+    const uint32_t bar0 = base + SL.bars + static_cast<uint32_t>(warp * N * 8);
+    const uint32_t ebar0 = base + SL.ebars + static_cast<uint32_t>(warp * N * 8);
+    const uint32_t my_full = base + SL.full + static_cast<uint32_t>(warp * kFifoSlots * 8);
+    const uint32_t my_empty = base + SL.empty + static_cast<uint32_t>(warp * kFifoIt4 * 8);
+    uint8_t* const my_fifo = sbase + SL.fifo + warp * kFifoSlots * kSlot4;
+    if (lane == 0) {
+      for (int s = 0; s < N; ++s) {
+        mbar_init(bar0 + 8u * s, 1u);   // stage loaded (producer's expect_tx + TMA bytes)
+        mbar_init(ebar0 + 8u * s, 1u);  // stage consumed (this warp's lane 0)
+      }
+      for (int s = 0; s < kFifoSlots; ++s) mbar_init(my_full + 8u * s, 1u);
+      for (int s = 0; s < kFifoIt4; ++s) mbar_init(my_empty + 8u * s, 1u);
+    }
+    if (!has_in) {
+      // The first warp of an item has no producer: its FIFO permanently
+      // holds the value above row 0 (max_neg_val, or -inf for
+      // reference.cpp:20-24).
+      for (int k = lane; k < kFifoSlots * kQuad; k += 32)
+        reinterpret_cast<float*>(my_fifo)[k] = a.row0_up;
+    }
+  } else {
+    for (int k = lane; k < kRows4 * kCols4 / 16; k += 32)
+      reinterpret_cast<uint4*>(sbase + SL.zero)[k] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  fence_proxy_async_smem();
+  fence_mbar_init();
+  cluster_sync_all();  // every CTA's FIFO / stage barriers exist before any use
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (warp == W) {
+    // ---- TMA producer warp: loads every compute warp's stages and issues
+    // the output's zero fill, so the compute warps only wait and compute.
+    // Lane w serves compute warp w on its own (independent thread
+    // scheduling lets each lane block on its warp's "stage consumed"
+    // barrier without holding up the others).
+    const int w = lane;
+    const int i0w = (crank * W + w) * kRows4;
+    if (w < W && s_b > 0 && i0w < t_b) {
+      prefetch_tensormap(&tmq);
+      const uint64_t pol_q = policy_evict_first();
+      const bool zero_fill = a.zero_fill != 0;
+      const uint32_t zero_tile = base + SL.zero;
+      const int group = (b * a.T_pad + i0w) / R4;
+      const int orow = b * a.T_cap + i0w;
+      for (int m = 0; m < nit; ++m) {
+        const int st = m % N;
+        const uint32_t bar = base + SL.bars + static_cast<uint32_t>((w * N + st) * 8);
+        if (m >= N) {
+          // stage st of warp w was consumed in iteration m - N
+          const uint32_t eb = base + SL.ebars + static_cast<uint32_t>((w * N + st) * 8);
+          mbar_wait(eb, (static_cast<uint32_t>(m / N) & 1u) ^ 1u);
+        }
+        mbar_arrive_expect_tx(bar, kStage4);
+        tma_load_3d(base + SL.ring + static_cast<uint32_t>((w * N + st) * kStage4), &tmq,
+                    m * kCols4, group, 0, bar, pol_q);
+        if (zero_fill) tma_store_2d(&tm_out, zero_tile, m * kCols4, orow);
+      }
+      if (zero_fill) bulk_store_drain();
+    }
+    __syncwarp();
+    cluster_sync_all();
+    return;
+  }
+
+  const int g = crank * W + warp;
+  const int i0 = g * kRows4;
+  const bool has_in = g > 0;
+  const bool live = i0 < t_b && s_b > 0;
+  if (live) {
+    const uint32_t bar0 = base + SL.bars + static_cast<uint32_t>(warp * N * 8);
+    const uint32_t ebar0 = base + SL.ebars + static_cast<uint32_t>(warp * N * 8);
+    const uint32_t my_full = base + SL.full + static_cast<uint32_t>(warp * kFifoSlots * 8);
+    const uint32_t my_empty = base + SL.empty + static_cast<uint32_t>(warp * kFifoIt4 * 8);
+    uint8_t* const my_fifo = sbase + SL.fifo + warp * kFifoSlots * kSlot4;
+    const bool has_out = i0 + kRows4 < t_b;
+    int nw = warp + 1, nr = crank;
+    if (nw == W) {
+      nw = 0;
+      nr = crank + 1;
+    }
+    int pw = warp - 1, pr = crank;
+    if (pw < 0) {
+      pw = W - 1;
+      pr = crank - 1;
+    }
+    Fifo4 F;
+    F.full = my_full;
+    F.empty = my_empty;
+    F.next_fifo =
+        has_out ? mapa(base + SL.fifo + static_cast<uint32_t>(nw * kFifoSlots * kSlot4), nr) : 0u;
+    F.next_full =
+        has_out ? mapa(base + SL.full + static_cast<uint32_t>(nw * kFifoSlots * 8), nr) : 0u;
+    F.prev_empty =
+        has_in ? mapa(base + SL.empty + static_cast<uint32_t>(pw * kFifoIt4 * 8), pr) : 0u;
+    F.prev_sink = has_in ? mapa(base + SL.sink + static_cast<uint32_t>(pw * 16), pr) : 0u;
+    F.buf = my_fifo;
+    F.has_in = has_in;
+    F.has_out = has_out;
+
+    const uint8_t* ring_ptr = sbase + SL.ring + warp * N * kStage4;
+    uint32_t coff[8];
+#pragma unroll
+    for (int a4 = 0; a4 < 8; ++a4) coff[a4] = lane * 128u + ((a4 ^ (lane & 7)) << 4);
+    const uint64_t pol_dir = policy_evict_last();
+
+    const bool is31 = lane == 31;
+    const int srclane = (lane + 31) & 31;
+    const int row0 = i0 + R4 * lane;
+    const bool row0_is_zero = row0 == 0;
+    const float mnv = a.mnv;
+    const uint32_t one = a.one;
+    Lane4 L;
+#pragma unroll
+    for (int r = 0; r < R4; ++r) L.o[r] = 0.0f;
+    L.acc = 0.0f;
+    L.vlast = a.row0_up;
+    float ex[kQuad];
+#pragma unroll
+    for (int u = 0; u < kQuad; ++u) ex[u] = 0.0f;
+    uint32_t* dirs_ptr = a.dirs + static_cast<size_t>(b) * a.M * a.T_alloc + i0 + R4 * lane;
+
+    bool ready = false;  // FIFO quad look-ahead
+    if (has_in && lane == 0) mbar_arrive_expect_tx(my_full, kSlot4);
+    // Look-ahead probes of the next stage's load and of the next
+    // iteration's FIFO "empty" slot: issued one iteration early so their
+    // latency hides behind the compute; consumed as a bool.
+    bool stage_ready = false;
+    bool empty_ready = !(has_out && is31 && kFifoIt4 <= 0);
+#ifdef MAS_FWD_PROFILE
+    long long pf_t0 = clock64(), pf_stage = 0, pf_empty = 0, pf_comp = 0, pf_rest = 0;
+#endif
+
+    int slot = 0;
+    uint32_t par = 0;
+    for (int m = 0; m < nit; ++m) {
+#ifdef MAS_FWD_PROFILE
+      long long pf_a = clock64();
+#endif
+      if (!stage_ready) mbar_wait(bar0 + 8u * slot, par);
+      {
+        const int ns = slot + 1 == N ? 0 : slot + 1;
+        const uint32_t np = ns == 0 ? par ^ 1u : par;
+        stage_ready = mbar_test_wait(bar0 + 8u * ns, np);  // result used next iteration
+      }
+#ifdef MAS_FWD_PROFILE
+      long long pf_b = clock64();
+      pf_stage += pf_b - pf_a;
+#endif
+      const uint8_t* stage = ring_ptr + slot * kStage4;
+      const int c_base = m * kCols4;
+      const int nvalid = s_b - c_base < kCols4 ? s_b - c_base : kCols4;
+      uint32_t w[R4] = {0u, 0u, 0u, 0u};
+      const bool generic =
+          m == 0 || nvalid < kCols4 || (MODE == 1 && c_base < i0 + kRows4 - 1);
+      if (has_out && is31 && m >= kFifoIt4) {
+        // This iteration's slots in the consumer are free once it released
+        // iteration m - kFifoIt4 (4-byte st.async on empty[m % kFifoIt4]).
+        const uint32_t eb = my_empty + 8u * static_cast<uint32_t>(m % kFifoIt4);
+        const uint32_t ep = (static_cast<uint32_t>(m / kFifoIt4) & 1u) ^ 1u;
+        if (!empty_ready) mbar_wait(eb, ep);
+      }
+      if (has_out && is31 && m + 1 >= kFifoIt4 && m + 1 < nit) {
+        const int m1 = m + 1;
+        const uint32_t eb1 = my_empty + 8u * static_cast<uint32_t>(m1 % kFifoIt4);
+        mbar_arrive_expect_tx(eb1, 4u);
+        empty_ready = mbar_test_wait(eb1, (static_cast<uint32_t>(m1 / kFifoIt4) & 1u) ^ 1u);
+      }
+      const bool more = m + 1 < nit;
+#ifdef MAS_FWD_PROFILE
+      long long pf_c = clock64();
+      pf_empty += pf_c - pf_b;
+#endif
+      if (generic) {
+        fwd4_stage<MODE, true>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
+                               kQuadsPerStage * m, c_base, nvalid, row0, mnv, row0_is_zero, one);
+      } else {
+        fwd4_stage<MODE, false>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
+                                kQuadsPerStage * m, c_base, kCols4, row0, mnv, row0_is_zero, one);
+      }
+#ifdef MAS_FWD_PROFILE
+      long long pf_d = clock64();
+      pf_comp += pf_d - pf_c;
+#endif
+      // Every value of this stage and of this iteration's FIFO slots has been
+      // consumed: hand the stage back to the producer warp and release the
+      // slots to the warp above.
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_local(ebar0 + 8u * slot);
+        if (has_in)
+          st_async_b32(F.prev_sink, static_cast<uint32_t>(m),
+                       F.prev_empty + 8u * static_cast<uint32_t>(m % kFifoIt4));
+      }
+      // Row 0 and column -1 are stored as zero bits (the backtrack never
+      // steps above row 0 or left of column 0).
+      if (m == 0) {
+#pragma unroll
+        for (int r = 0; r < R4; ++r) w[r] &= 0x7fffffffu;
+      }
+      if (row0_is_zero) w[0] = 0u;
+      asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dirs_ptr),
+                   "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "l"(pol_dir)
+                   : "memory");
+      dirs_ptr += a.T_alloc;
+      slot = slot + 1 == N ? 0 : slot + 1;
+      par ^= slot == 0 ? 1u : 0u;
+#ifdef MAS_FWD_PROFILE
+      pf_rest += clock64() - pf_d;
+#endif
+    }
+#ifdef MAS_FWD_PROFILE
+    if (b == 0 && lane == 0)
+      printf("fwd4 warp g=%d: total %lld, stage-wait %lld, empty-wait %lld, compute %lld (%.1f/col), rest %lld, nit %d\n",
+             g, clock64() - pf_t0, pf_stage, pf_empty, pf_comp, (double)pf_comp / s_b, pf_rest, nit);
+#endif
+    __syncwarp();
+    bool bad = false;
+#pragma unroll
+    for (int r = 0; r < R4; ++r) bad |= row0 + r < t_b;
+    bad = bad && !(L.acc < INFINITY);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flags + b, 1);
+  }
+  __syncwarp();
+  cluster_sync_all();  // no CTA leaves while a peer may still write its FIFO
+}
+
+}  // namespace
+
+size_t fwd4_smem_bytes(int W, int N) { return smem4_layout(W, N).total + 1024u; }
+
+cudaError_t fwd4_configure() {
+  constexpr int kMaxDevices = 64;
+  static std::once_flag once[kMaxDevices];
+  static cudaError_t status[kMaxDevices];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::call_once(once[dev], [dev] {
+    int smem_max = 0;
+    cudaError_t r = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    for (int mode = 0; mode < 2 && r == cudaSuccess; ++mode) {
+      const void* fn = mode == 0 ? reinterpret_cast<const void*>(&mas_fwd4_kernel<0>)
+                                 : reinterpret_cast<const void*>(&mas_fwd4_kernel<1>);
+      r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+      if (r == cudaSuccess)
+        r = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
+    status[dev] = r;
+  });
+  return status[dev];
+}
+
+cudaError_t launch_fwd4(int mode, const CUtensorMap& tmq, const CUtensorMap& tm_out,
+                        const FwdArgs& a, int B, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(B * a.K), 1, 1);
+  cfg.blockDim = dim3(static_cast<unsigned>((a.W + 1) * 32), 1, 1);  // + the TMA producer warp
+  cfg.dynamicSmemBytes = fwd4_smem_bytes(a.W, a.N);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(a.K);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (mode == 0) return cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<0>, tmq, tm_out, a);
+  return cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<1>, tmq, tm_out, a);
+}
+
+}  // namespace mas

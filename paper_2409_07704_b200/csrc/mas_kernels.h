@@ -61,6 +61,11 @@ cudaError_t launch_locate_nonfinite(const float* q, int64_t row_pitch, int T_pad
 cudaError_t launch_generate(uint64_t s0, int64_t first_elem, int B, int T, int S, int64_t pitch,
                             float* out, cudaStream_t stream);
 cudaError_t fwd_configure(int W, int N, int K);
+// mas_fwd4.cu: four rows per lane, 128 rows per warp, 32-column stages.
+size_t fwd4_smem_bytes(int W, int N);
+cudaError_t fwd4_configure();
+cudaError_t launch_fwd4(int mode, const CUtensorMap& tmq, const CUtensorMap& tm_out,
+                        const FwdArgs& a, int B, cudaStream_t stream);
 int fwd_max_active_clusters(int W, int N, int K, int mode);
 
 }  // namespace mas
