@@ -158,8 +158,9 @@ MAS_API int mas_plan_finish(mas_plan_t* plan, const float* d_values, void* strea
 /* Number of kernel launches one mas_plan_enqueue issues. */
 MAS_API int mas_plan_launches(const mas_plan_t* plan);
 /* Launch geometry chosen by the plan: {rows_per_warp, warps_per_cta,
- * ctas_per_item (cluster size), stages, segment_columns}. */
-MAS_API void mas_plan_geometry(const mas_plan_t* plan, int32_t geom[5]);
+ * ctas_per_item (cluster size), stages, segment_columns, max co-resident
+ * clusters of the forward kernel}. */
+MAS_API void mas_plan_geometry(const mas_plan_t* plan, int32_t geom[6]);
 MAS_API void mas_plan_destroy(mas_plan_t* plan);
 
 /* validate_config (types.cpp:59-69): MAS_OK or MAS_E_VALIDATION with the

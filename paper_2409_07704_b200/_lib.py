@@ -75,7 +75,7 @@ _SIGS = {
                                              ctypes.POINTER(MasError)]),
     "mas_plan_finish": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(MasError)]),
     "mas_plan_launches": (ctypes.c_int, [_VP]),
-    "mas_plan_geometry": (None, [_VP, ctypes.POINTER(ctypes.c_int32 * 5)]),
+    "mas_plan_geometry": (None, [_VP, ctypes.POINTER(ctypes.c_int32 * 6)]),
     "mas_plan_destroy": (None, [_VP]),
     "mas_generate_device": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32,
                                            ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, _VP,

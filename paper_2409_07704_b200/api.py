@@ -253,10 +253,10 @@ class Plan:
 
     @property
     def geometry(self) -> dict:
-        g = (ctypes.c_int32 * 5)()
+        g = (ctypes.c_int32 * 6)()
         self._lib.mas_plan_geometry(self._h, ctypes.byref(g))
         return {"rows_per_warp": g[0], "warps_per_cta": g[1], "ctas_per_item": g[2],
-                "stages": g[3], "segment_cols": g[4]}
+                "stages": g[3], "segment_cols": g[4], "max_active_clusters": g[5]}
 
     def close(self):
         if getattr(self, "_h", None):

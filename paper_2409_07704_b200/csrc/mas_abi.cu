@@ -217,25 +217,33 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
   g->L = 256;
   g->Kseg = (S_cap + g->L - 1) / g->L;
   if (g->R == 4) {
-    // 128 rows per warp.  Few warps per CTA spreads an item over more SMs
-    // (one warp per SM sub-partition is all the DP needs); use 4 per CTA
-    // only when 2 would not fit the whole batch in one wave of CTAs.
+    // 128 rows per warp; an item's warps form one cluster of K CTAs of W
+    // compute warps.  Candidates in order of preference (few warps per CTA
+    // spread an item over more SMs; more stages give the TMA ring more
+    // lead); the first that runs the whole batch in the fewest waves of
+    // co-resident clusters wins (cudaOccupancyMaxActiveClusters accounts
+    // for shared memory and the GPC placement of clusters).
     const int warps = std::max(1, (t_max + 127) / 128);
-    if (warps <= 2) {
-      g->W = warps;
-      g->K = 1;
-    } else {
-      g->W = 2;
-      g->K = (warps + 1) / 2;
-      if (g->K > mas::kMaxClusterCtas || static_cast<int64_t>(B) * g->K > sms) {
-        g->W = 4;
-        g->K = (warps + 3) / 4;
+    static const int cand[][2] = {{2, 4}, {4, 3}, {2, 3}, {1, 4}, {2, 2}, {4, 2}, {1, 2}};
+    int best = -1;
+    int64_t best_waves = 0;
+    for (int c = 0; c < static_cast<int>(sizeof(cand) / sizeof(cand[0])); ++c) {
+      const int W = std::min(cand[c][0], warps), N = cand[c][1];
+      const int K = (warps + W - 1) / W;
+      if (K > mas::kMaxClusterCtas || mas::fwd4_smem_bytes(W, N) > budget) continue;
+      const int act = mas::fwd4_max_active_clusters(W, N, K);
+      if (act <= 0) continue;
+      const int64_t waves = (static_cast<int64_t>(B) + act - 1) / act;
+      if (best < 0 || waves < best_waves) {
+        best = c;
+        best_waves = waves;
+        g->W = W;
+        g->N = N;
+        g->K = K;
       }
-      if (g->K > mas::kMaxClusterCtas) return false;
+      if (waves == 1) break;
     }
-    int N = 4;
-    while (N > 2 && mas::fwd4_smem_bytes(g->W, N) > budget) --N;
-    g->N = N;
+    if (best < 0) return false;
     g->T_alloc = g->K * g->W * 128;
     return true;
   }
@@ -436,6 +444,10 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
       t_max = std::max<int>(t_max, static_cast<int>(t));
     }
   }
+  if (forward_variant() == 4 && mas::fwd4_configure() != cudaSuccess) {
+    delete p;
+    return set_error(err, MAS_E_CUDA, -1, -1, "forward kernel configuration failed");
+  }
   if (!choose_geometry(batch, std::max(t_max, 1), speech_cap, &p->geo)) {
     delete p;
     return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
@@ -486,7 +498,9 @@ extern "C" {
 
 int mas_plan_launches(const mas_plan_t* p) { return p ? p->launches : 0; }
 
-void mas_plan_geometry(const mas_plan_t* p, int32_t geom[5]) {
+void mas_plan_geometry(const mas_plan_t* p, int32_t geom[6]) {
+  geom[5] = p->geo.R == 4 ? mas::fwd4_max_active_clusters(p->geo.W, p->geo.N, p->geo.K)
+                          : mas::fwd_max_active_clusters(p->geo.W, p->geo.N, p->geo.K, 0);
   geom[0] = 32 * p->geo.R;
   geom[1] = p->geo.W;
   geom[2] = p->geo.K;
@@ -550,6 +564,12 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
                                             &tm_out)))
       return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled(out) failed");
     fa.zero_fill = fused_zero ? 1 : 0;
+    static const int l2_ahead = [] {
+      const char* e = std::getenv("MAS_L2_AHEAD");  // experiment override
+      return e ? std::max(0, std::atoi(e)) : -1;
+    }();
+    // L2 prefetch lead (stages beyond the smem ring) when the ring is short.
+    fa.l2_ahead = l2_ahead >= 0 ? l2_ahead : 0;  // measured: L2 prefetch only hurts
     fa.one = 1u;
     fa.zero = 0.0f;
     fa.T_cap = p->T;

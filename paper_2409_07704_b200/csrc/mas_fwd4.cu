@@ -149,12 +149,23 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
 }
 
 // 16 columns with the FIFO hand-off around them (see mas_fwd.cu fwd_quad).
+// Look-ahead probes of the next stage's load and of the next iteration's
+// FIFO "empty" slot, made inside the first quad's straight-line block so
+// their results are consumed only after it (see fwd4_quad).
+struct Probes {
+  uint32_t stage_bar, stage_par;  // next stage's "loaded" barrier
+  uint32_t empty_bar, empty_par;  // next iteration's consumer-slot barrier
+  bool arm_empty;                 // lane 31: arm empty_bar (expect_tx) first
+  bool stage_ok, empty_ok;        // results
+};
+
 template <int MODE, bool GENERIC, int K>
 __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (&coff)[8],
                                          const Fifo4& F, float (&ex)[kQuad], Lane4& L,
                                          uint32_t (&w)[R4], bool& ready, bool more, bool is31,
                                          int lane, int srclane, int q, int c_base, int nvalid,
-                                         int row0, float mnv, bool row0_is_zero, uint32_t one) {
+                                         int row0, float mnv, bool row0_is_zero, uint32_t one,
+                                         Probes& P) {
   if (GENERIC && K * kQuad >= nvalid) return false;
   const int fs = q & (kFifoSlots - 1);
   if (F.has_in && !ready) mbar_wait(F.full + 8u * fs, static_cast<uint32_t>(q / kFifoSlots) & 1u);
@@ -163,6 +174,12 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
   const uint32_t bar1 = F.full + 8u * (q1 & (kFifoSlots - 1));
   if (lane == 0 && next && F.has_in) mbar_arrive_expect_tx(bar1, kSlot4);
   const bool probe = mbar_test_wait(bar1, static_cast<uint32_t>(q1 / kFifoSlots) & 1u);
+  bool p_stage = false, p_empty = false;
+  if (K == 0) {
+    if (P.arm_empty) mbar_arrive_expect_tx(P.empty_bar, 4u);
+    p_stage = mbar_test_wait(P.stage_bar, P.stage_par);
+    p_empty = mbar_test_wait(P.empty_bar, P.empty_par);
+  }
   const float4* slot = reinterpret_cast<const float4*>(F.buf + fs * kSlot4);
   bool ok = true;
 #define MAS_G4(A)                                                                              \
@@ -173,6 +190,10 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
   MAS_G4(0) MAS_G4(1) MAS_G4(2) MAS_G4(3)
 #undef MAS_G4
   ready = probe;
+  if (K == 0) {
+    P.stage_ok = p_stage;
+    P.empty_ok = p_empty;
+  }
   if (F.has_out && is31) {
     const uint32_t dst = F.next_fifo + static_cast<uint32_t>(fs * kSlot4);
     const uint32_t fbar = F.next_full + 8u * fs;
@@ -188,12 +209,13 @@ __device__ __forceinline__ void fwd4_stage(const uint8_t* stage, const uint32_t 
                                           const Fifo4& F, float (&ex)[kQuad], Lane4& L,
                                           uint32_t (&w)[R4], bool& ready, bool more, bool is31,
                                           int lane, int srclane, int q0, int c_base, int nvalid,
-                                          int row0, float mnv, bool row0_is_zero, uint32_t one) {
+                                          int row0, float mnv, bool row0_is_zero, uint32_t one,
+                                          Probes& P) {
   if (!fwd4_quad<MODE, GENERIC, 0>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane, q0,
-                                   c_base, nvalid, row0, mnv, row0_is_zero, one))
+                                   c_base, nvalid, row0, mnv, row0_is_zero, one, P))
     return;
   fwd4_quad<MODE, GENERIC, 1>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane, q0 + 1,
-                              c_base, nvalid, row0, mnv, row0_is_zero, one);
+                              c_base, nvalid, row0, mnv, row0_is_zero, one, P);
 }
 
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
@@ -203,6 +225,13 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
       : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
 }
 
 template <int MODE>
@@ -224,6 +253,12 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   const int t_b = static_cast<int>(a.lengths[2 * b]);
   const int s_b = static_cast<int>(a.lengths[2 * b + 1]);
   const int nit = (s_b + kCols4 - 1) / kCols4;
+#ifdef MAS_FWD_TIMELINE
+  unsigned long long tl_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_start));
+  unsigned tl_smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(tl_smid));
+#endif
 
   if (warp < W) {
     const int g = crank * W + warp;
@@ -262,7 +297,10 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     // the output's zero fill, so the compute warps only wait and compute.
     // Lane w serves compute warp w on its own (independent thread
     // scheduling lets each lane block on its warp's "stage consumed"
-    // barrier without holding up the others).
+    // barrier without holding up the others).  Stages further ahead than
+    // the shared-memory ring are prefetched into L2 (kL2Ahead4 stages), so
+    // a ring refill finds its data in L2 when DRAM latency exceeds the
+    // ring's lead.
     const int w = lane;
     const int i0w = (crank * W + w) * kRows4;
     if (w < W && s_b > 0 && i0w < t_b) {
@@ -272,6 +310,8 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       const uint32_t zero_tile = base + SL.zero;
       const int group = (b * a.T_pad + i0w) / R4;
       const int orow = b * a.T_cap + i0w;
+      const int l2a = a.l2_ahead;
+      for (int m = 0; m < l2a && m < nit; ++m) tma_prefetch_3d(&tmq, m * kCols4, group, 0);
       for (int m = 0; m < nit; ++m) {
         const int st = m % N;
         const uint32_t bar = base + SL.bars + static_cast<uint32_t>((w * N + st) * 8);
@@ -280,6 +320,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
           const uint32_t eb = base + SL.ebars + static_cast<uint32_t>((w * N + st) * 8);
           mbar_wait(eb, (static_cast<uint32_t>(m / N) & 1u) ^ 1u);
         }
+        if (l2a > 0 && m + l2a < nit) tma_prefetch_3d(&tmq, (m + l2a) * kCols4, group, 0);
         mbar_arrive_expect_tx(bar, kStage4);
         tma_load_3d(base + SL.ring + static_cast<uint32_t>((w * N + st) * kStage4), &tmq,
                     m * kCols4, group, 0, bar, pol_q);
@@ -351,11 +392,9 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
 
     bool ready = false;  // FIFO quad look-ahead
     if (has_in && lane == 0) mbar_arrive_expect_tx(my_full, kSlot4);
-    // Look-ahead probes of the next stage's load and of the next
-    // iteration's FIFO "empty" slot: issued one iteration early so their
-    // latency hides behind the compute; consumed as a bool.
+    // Look-ahead results of the previous iteration's probes (see Probes).
     bool stage_ready = false;
-    bool empty_ready = !(has_out && is31 && kFifoIt4 <= 0);
+    bool empty_ready = true;
 #ifdef MAS_FWD_PROFILE
     long long pf_t0 = clock64(), pf_stage = 0, pf_empty = 0, pf_comp = 0, pf_rest = 0;
 #endif
@@ -367,11 +406,6 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       long long pf_a = clock64();
 #endif
       if (!stage_ready) mbar_wait(bar0 + 8u * slot, par);
-      {
-        const int ns = slot + 1 == N ? 0 : slot + 1;
-        const uint32_t np = ns == 0 ? par ^ 1u : par;
-        stage_ready = mbar_test_wait(bar0 + 8u * ns, np);  // result used next iteration
-      }
 #ifdef MAS_FWD_PROFILE
       long long pf_b = clock64();
       pf_stage += pf_b - pf_a;
@@ -382,31 +416,40 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       uint32_t w[R4] = {0u, 0u, 0u, 0u};
       const bool generic =
           m == 0 || nvalid < kCols4 || (MODE == 1 && c_base < i0 + kRows4 - 1);
-      if (has_out && is31 && m >= kFifoIt4) {
+      if (has_out && is31 && m >= kFifoIt4 && !empty_ready) {
         // This iteration's slots in the consumer are free once it released
         // iteration m - kFifoIt4 (4-byte st.async on empty[m % kFifoIt4]).
-        const uint32_t eb = my_empty + 8u * static_cast<uint32_t>(m % kFifoIt4);
-        const uint32_t ep = (static_cast<uint32_t>(m / kFifoIt4) & 1u) ^ 1u;
-        if (!empty_ready) mbar_wait(eb, ep);
-      }
-      if (has_out && is31 && m + 1 >= kFifoIt4 && m + 1 < nit) {
-        const int m1 = m + 1;
-        const uint32_t eb1 = my_empty + 8u * static_cast<uint32_t>(m1 % kFifoIt4);
-        mbar_arrive_expect_tx(eb1, 4u);
-        empty_ready = mbar_test_wait(eb1, (static_cast<uint32_t>(m1 / kFifoIt4) & 1u) ^ 1u);
+        mbar_wait(my_empty + 8u * static_cast<uint32_t>(m % kFifoIt4),
+                  (static_cast<uint32_t>(m / kFifoIt4) & 1u) ^ 1u);
       }
       const bool more = m + 1 < nit;
+      Probes P;
+      {
+        const int ns = slot + 1 == N ? 0 : slot + 1;
+        P.stage_bar = bar0 + 8u * ns;
+        P.stage_par = ns == 0 ? par ^ 1u : par;
+        const int m1 = m + 1;
+        P.empty_bar = my_empty + 8u * static_cast<uint32_t>(m1 % kFifoIt4);
+        P.empty_par = (static_cast<uint32_t>(m1 / kFifoIt4) & 1u) ^ 1u;
+        P.arm_empty = has_out && is31 && m1 >= kFifoIt4 && more;
+        P.stage_ok = false;
+        P.empty_ok = false;
+      }
 #ifdef MAS_FWD_PROFILE
       long long pf_c = clock64();
       pf_empty += pf_c - pf_b;
 #endif
       if (generic) {
         fwd4_stage<MODE, true>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
-                               kQuadsPerStage * m, c_base, nvalid, row0, mnv, row0_is_zero, one);
+                               kQuadsPerStage * m, c_base, nvalid, row0, mnv, row0_is_zero, one,
+                               P);
       } else {
         fwd4_stage<MODE, false>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
-                                kQuadsPerStage * m, c_base, kCols4, row0, mnv, row0_is_zero, one);
+                                kQuadsPerStage * m, c_base, kCols4, row0, mnv, row0_is_zero, one,
+                                P);
       }
+      stage_ready = P.stage_ok;
+      empty_ready = P.empty_ok || !P.arm_empty;
 #ifdef MAS_FWD_PROFILE
       long long pf_d = clock64();
       pf_comp += pf_d - pf_c;
@@ -452,6 +495,14 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   }
   __syncwarp();
   cluster_sync_all();  // no CTA leaves while a peer may still write its FIFO
+#ifdef MAS_FWD_TIMELINE
+  if (threadIdx.x == 0) {
+    unsigned long long tl_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_end));
+    printf("TL cta %d item %d rank %d sm %u start %llu end %llu\n", blockIdx.x, b, crank, tl_smid,
+           tl_start, tl_end);
+  }
+#endif
 }
 
 }  // namespace
@@ -479,6 +530,27 @@ cudaError_t fwd4_configure() {
     status[dev] = r;
   });
   return status[dev];
+}
+
+int fwd4_max_active_clusters(int W, int N, int K) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(K), 1, 1);
+  cfg.blockDim = dim3(static_cast<unsigned>((W + 1) * 32), 1, 1);
+  cfg.dynamicSmemBytes = fwd4_smem_bytes(W, N);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(K);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(&mas_fwd4_kernel<0>), &cfg) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return n;
 }
 
 cudaError_t launch_fwd4(int mode, const CUtensorMap& tmq, const CUtensorMap& tm_out,

@@ -38,6 +38,7 @@ struct FwdArgs {
   float row0_up;            // value above row 0: mnv (parallel) / -inf (reference)
   int zero_fill;            // 1: TMA-store zero tiles of the output (tm_out) as we go
   int T_cap, S_cap;         // output shape
+  int l2_ahead;             // mas_fwd4: stages prefetched into L2 beyond the smem ring
   uint32_t one;             // 1 and 0.0f passed at run time so ptxas keeps the
   float zero;               //   bit IMADs / NonFinite FFMAs on the FMA pipe
 };
@@ -64,6 +65,7 @@ cudaError_t fwd_configure(int W, int N, int K);
 // mas_fwd4.cu: four rows per lane, 128 rows per warp, 32-column stages.
 size_t fwd4_smem_bytes(int W, int N);
 cudaError_t fwd4_configure();
+int fwd4_max_active_clusters(int W, int N, int K);
 cudaError_t launch_fwd4(int mode, const CUtensorMap& tmq, const CUtensorMap& tm_out,
                         const FwdArgs& a, int B, cudaStream_t stream);
 int fwd_max_active_clusters(int W, int N, int K, int mode);
