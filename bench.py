@@ -314,7 +314,7 @@ def run_ours(args):
                    "parallelism": f"batch-shard dp{world}, no collective",
                    "l2": "inputs larger than L2 (1.07 GB q per GPU vs 126 MB L2), no flush",
                    "geometry": geom},
-        "roofline": {"bound": "hbm", "kernel": "mas_fwd_kernel", "achieved": round(achieved, 1),
+        "roofline": {"bound": "hbm", "kernel": "mas_fwd4_kernel", "achieved": round(achieved, 1),
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "bytes_per_cell": BYTES_PER_CELL,
