@@ -64,6 +64,12 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
   return v;
 }
+// Refill a queue register in place: the register is an input too, so the
+// load stays after the register's last use (no hoisting into a fresh
+// register followed by a copy that would wait for the load).
+__device__ __forceinline__ void lds32_into(uint32_t& r, uint32_t addr) {
+  asm volatile("ld.shared.u32 %0, [%1];" : "+r"(r) : "r"(addr) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -96,8 +102,9 @@ __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
 // A window miss (the walk descending more than ~R - 35 rows within four
 // stages) re-centres the window with a synchronous reload.
 __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
-  // Guard words in front: a block may read up to 8 rows below row 0.
-  constexpr int kGuard = 32;
+  // Guard words in front: a block may read up to 8 rows below row 0, and the
+  // speculative next-word load one word (R rows) before the first word.
+  constexpr int kGuard = kBtMaxRows + 32;
   __shared__ alignas(128) uint32_t win_raw[kGuard + kBtStages * kBtWords * kBtMaxRows];
   __shared__ alignas(8) uint64_t bars[3 * kBtStages];  // full | done | free
   __shared__ int rec_y[kBtStages][kBtWords];
@@ -197,62 +204,76 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
           mbar_wait(full_s + 8u * slot, (ph_full >> slot) & 1u);
           ph_full ^= 1u << slot;
         };
-        // The window must hold rows y-40 .. y: a word has at most 32 exits
-        // and a block reads eight rows ahead.
-        if (y - 40 < ylo && ylo > 0) recenter();
-        rec_y[slot][ml] = y;
+        // Words are walked in pairs (ml, ml-1) as one bit-reversed 64-bit
+        // value, lo = word ml, hi = word ml-1 (position p of the pair is bit
+        // 63 - p), so a word change happens every 64 columns; a stage's last
+        // word walks alone when the pairing leaves it over (hi = 0).  The
+        // window must hold rows y-72 .. y: a pair has at most 64 exits and
+        // a block reads eight rows ahead.
+        auto ld64 = [&](uint32_t a, bool pair) -> uint64_t {
+          const uint64_t lo = lds32(a);
+          return pair ? lo | (static_cast<uint64_t>(lds32(a - wstride)) << 32) : lo;
+        };
+        if (y - 72 < ylo && ylo > 0) recenter();
         // pw: shared address of (word ml, row y)
         uint32_t pw = slot_base + static_cast<uint32_t>((ml * R + (y - ylo)) * 4);
-        // x: the current row's word, restricted to positions the walk may
-        // still take
-        uint32_t x = lds32(pw) & lim;
+        bool pair = ml > 0;
+        uint64_t x = ld64(pw, pair) & (static_cast<uint64_t>(0xffffffffu) << 32 | lim);
         lim = 0xffffffffu;
-        while (true) {  // one direction word per pass; pw = (word ml, row y)
-          // q1..q4: rows y-1 .. y-4 of the word
-          uint32_t q1 = lds32(pw - 4), q2 = lds32(pw - 8), q3 = lds32(pw - 12),
-                   q4 = lds32(pw - 16);
-          uint32_t pb = pw, ps = pw;
-          uint32_t exw = 0u;
+        uint64_t q1 = ld64(pw - 4, pair), q2 = ld64(pw - 8, pair), q3 = ld64(pw - 12, pair),
+                 q4 = ld64(pw - 16, pair);
+        while (true) {  // one word pair per pass; pw = (word ml, row y)
+          rec_y[slot][ml] = y;
+          uint32_t pb = pw;
+          uint64_t exw = 0u;
           // A step: the lowest set bit of x (bit-reversed: the last column
           // on this row) is an exit; with d = x - 1, x & ~d is that bit and
           // ~(x ^ d) the positions left of it, so the next row's x is one
-          // LOP3 after the IADD.  The step is self-terminating: once x has
-          // no bit it stays 0, and an exit at position 0 (bit 31) is
-          // recorded and leaves x = 0.  So four steps run without a branch,
-          // and the row reached is y - popc(exits).
-// ps steps down one row per exit (x != 0), so the next word's address is
-// known when the block ends, without waiting for a popc.
+          // LOP3 pair after the IADD pair.  The step is self-terminating:
+          // once x has no bit it stays 0, and an exit at the pair's position
+          // 0 (bit 63) is recorded and leaves x = 0.  So four steps run
+          // without a branch, and the row reached is y - popc(exits).
 #define MAS_BT_STEP(Q, OFF)                    \
   {                                            \
-    const uint32_t d = x - 1u;                 \
+    const uint64_t d = x - 1u;                 \
     exw |= x & ~d;                             \
-    ps -= x != 0u ? 4u : 0u;                   \
     x = (Q) & ~(x ^ d);                        \
-    (Q) = lds32(pb - (OFF));                   \
+    (Q) = ld64(pb - (OFF), pair);              \
   }
           while (true) {
             MAS_BT_STEP(q1, 20u) MAS_BT_STEP(q2, 24u) MAS_BT_STEP(q3, 28u) MAS_BT_STEP(q4, 32u)
             pb -= 16u;
-            if ((x & 0x7fffffffu) == 0u) break;
+            if ((x & 0x7fffffffffffffffull) == 0u) break;
           }
 #undef MAS_BT_STEP
-          exw |= x;  // a pending exit at position 0
-          ps -= x != 0u ? 4u : 0u;
-          rec_ex[slot][ml] = exw;
+          exw |= x;  // a pending exit at the pair's position 0
+          const int ex_lo = __popc(static_cast<uint32_t>(exw));
+          const int ex = ex_lo + __popc(static_cast<uint32_t>(exw >> 32));
+          // next pair: two words (or one) to the left, ex rows up
+          const uint32_t pn = pw - static_cast<uint32_t>(ex * 4) - (pair ? 2u : 1u) * wstride;
+          rec_ex[slot][ml] = static_cast<uint32_t>(exw);
+          if (pair) {
+            rec_ex[slot][ml - 1] = static_cast<uint32_t>(exw >> 32);
+            rec_y[slot][ml - 1] = y - ex_lo;
+          }
 #ifdef MAS_BT_PROFILE
-          if (pr_words < 300) { pr_ts[pr_words] = static_cast<unsigned>(clock64() - pr_t0); pr_ex[pr_words] = static_cast<unsigned char>(__popc(exw | x)); }
+          if (pr_words < 300) { pr_ts[pr_words] = static_cast<unsigned>(clock64() - pr_t0); pr_ex[pr_words] = static_cast<unsigned char>(ex); }
           ++pr_words;
 #endif
-          y -= static_cast<int>((pw - ps) >> 2);
-          --ml;
+          y -= ex;
+          ml -= pair ? 2 : 1;
           if (y == 0 || ml < 0) break;
-          pw = ps - wstride;
-          if (y - 40 < ylo && ylo > 0) {
+          pair = ml > 0;
+          pw = pn;
+          if (y - 72 < ylo && ylo > 0) {
             recenter();
             pw = slot_base + static_cast<uint32_t>((ml * R + (y - ylo)) * 4);
           }
-          rec_y[slot][ml] = y;
-          x = lds32(pw);
+          x = ld64(pw, pair);
+          q1 = ld64(pw - 4, pair);
+          q2 = ld64(pw - 8, pair);
+          q3 = ld64(pw - 12, pair);
+          q4 = ld64(pw - 16, pair);
         }
       }
       for (; ml >= 0; --ml) {  // the walk reached row 0: the rest stays there
