@@ -77,9 +77,25 @@ __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// The four direction bits of one column, w[r] += (1 << BIT) if the row
+// above beats row r.  One asm block with four predicates: ptxas otherwise
+// funnels the four compares through a single predicate register
+// (FSETP -> @P IMAD -> FSETP ...), a serial chain behind the shuffle.  The
+// three bits that do not need `up` are compared first.
 template <int BIT>
-__device__ __forceinline__ void bit_gt(uint32_t& w, float a, float b, uint32_t one) {
-  set_bit_if_gt<BIT>(w, a, b, one);
+__device__ __forceinline__ void bits4(uint32_t (&w)[R4], float up, const float (&o)[R4],
+                                      uint32_t one) {
+  asm("{\n\t.reg .pred p0, p1, p2, p3;\n\t"
+      "setp.gt.f32 p1, %5, %6;\n\t"
+      "setp.gt.f32 p2, %6, %7;\n\t"
+      "setp.gt.f32 p3, %7, %8;\n\t"
+      "setp.gt.f32 p0, %4, %5;\n\t"
+      "@p1 mad.lo.u32 %1, %9, %10, %1;\n\t"
+      "@p2 mad.lo.u32 %2, %9, %10, %2;\n\t"
+      "@p3 mad.lo.u32 %3, %9, %10, %3;\n\t"
+      "@p0 mad.lo.u32 %0, %9, %10, %0;\n\t}"
+      : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3])
+      : "f"(up), "f"(o[0]), "f"(o[1]), "f"(o[2]), "f"(o[3]), "r"(one), "n"(1u << BIT));
 }
 
 // Four columns (one LDS.128 per row residue, one of the FIFO slot) of the
@@ -92,9 +108,14 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
                                           bool row0_is_zero, uint32_t one) {
   if (GENERIC && U0 >= nvalid) return false;
   float4 qv[R4];
+#ifndef MAS_ABL_NOQLDS
 #pragma unroll
   for (int r = 0; r < R4; ++r)
     qv[r] = *reinterpret_cast<const float4*>(tile + r * 4096 + coff);
+#else
+#pragma unroll
+  for (int r = 0; r < R4; ++r) qv[r] = make_float4(mnv * 1e-36f, 1.f, 2.f, 3.f);
+#endif
   const float4 vv = slot[(U0 % kQuad) / 4];  // producer's bottom row
   const float bnds[4] = {L.vlast, vv.x, vv.y, vv.z};
 #pragma unroll
@@ -104,15 +125,17 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
 #pragma unroll
     for (int r = 0; r < R4; ++r) q[r] = e == 0 ? qv[r].x : e == 1 ? qv[r].y : e == 2 ? qv[r].z : qv[r].w;
     const float send = is31 ? bnds[e] : L.o[R4 - 1];
+#ifndef MAS_ABL_NOSHFL
     const float up = __shfl_sync(0xffffffffu, send, srclane);
+#else
+    const float up = send;
+#endif
     constexpr int bitpos = 31 - (U0 + 0);  // adjusted per e below
+#ifndef MAS_ABL_NOBITS
     switch (U0 + e) {  // compile-time bit position 31 - column-in-word
-#define MAS_B4(U)                                   \
-  case U:                                           \
-    bit_gt<31 - U>(w[0], up, L.o[0], one);          \
-    bit_gt<31 - U>(w[1], L.o[0], L.o[1], one);      \
-    bit_gt<31 - U>(w[2], L.o[1], L.o[2], one);      \
-    bit_gt<31 - U>(w[3], L.o[2], L.o[3], one);      \
+#define MAS_B4(U)                       \
+  case U:                               \
+    bits4<31 - U>(w, up, L.o, one);     \
     break;
       MAS_B4(0) MAS_B4(1) MAS_B4(2) MAS_B4(3) MAS_B4(4) MAS_B4(5) MAS_B4(6) MAS_B4(7)
       MAS_B4(8) MAS_B4(9) MAS_B4(10) MAS_B4(11) MAS_B4(12) MAS_B4(13) MAS_B4(14) MAS_B4(15)
@@ -120,6 +143,7 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
       MAS_B4(24) MAS_B4(25) MAS_B4(26) MAS_B4(27) MAS_B4(28) MAS_B4(29) MAS_B4(30) MAS_B4(31)
 #undef MAS_B4
     }
+#endif
     (void)bitpos;
     float n[R4];
     n[0] = q[0] + fmaxf(up, L.o[0]);
@@ -138,8 +162,10 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
         for (int r = 1; r < R4; ++r) n[r] = mnv;
       }
     }
+#ifndef MAS_ABL_NOFOLD
     fold_abs_max_nan(L.acc, q[0], q[1]);
     fold_abs_max_nan(L.acc, q[2], q[3]);
+#endif
     ex[(U0 % kQuad) + e] = n[R4 - 1];
 #pragma unroll
     for (int r = 0; r < R4; ++r) L.o[r] = n[r];
@@ -168,12 +194,19 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
                                          Probes& P) {
   if (GENERIC && K * kQuad >= nvalid) return false;
   const int fs = q & (kFifoSlots - 1);
+#ifndef MAS_ABL_NOFIFO
   if (F.has_in && !ready) mbar_wait(F.full + 8u * fs, static_cast<uint32_t>(q / kFifoSlots) & 1u);
+#endif
   const bool next = K + 1 < kQuadsPerStage ? (!GENERIC || (K + 1) * kQuad < nvalid) : more;
   const int q1 = q + 1;
   const uint32_t bar1 = F.full + 8u * (q1 & (kFifoSlots - 1));
+#ifndef MAS_ABL_NOFIFO
   if (lane == 0 && next && F.has_in) mbar_arrive_expect_tx(bar1, kSlot4);
   const bool probe = mbar_test_wait(bar1, static_cast<uint32_t>(q1 / kFifoSlots) & 1u);
+#else
+  const bool probe = true;
+  (void)bar1;
+#endif
   bool p_stage = false, p_empty = false;
   if (K == 0) {
     if (P.arm_empty) mbar_arrive_expect_tx(P.empty_bar, 4u);
@@ -194,7 +227,11 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
     P.stage_ok = p_stage;
     P.empty_ok = p_empty;
   }
+#ifndef MAS_ABL_NOFIFO
   if (F.has_out && is31) {
+#else
+  if (false) {
+#endif
     const uint32_t dst = F.next_fifo + static_cast<uint32_t>(fs * kSlot4);
     const uint32_t fbar = F.next_full + 8u * fs;
 #pragma unroll
