@@ -194,6 +194,8 @@ bool encode_out_map(uint8_t* out, int64_t rows, int64_t S, CUtensorMap* m) {
 struct Geometry {
   int R = 4;  // text rows per lane: 4 (mas_fwd4.cu, default) or 2 (mas_fwd.cu)
   int W = 1, K = 1, N = 2, L = 256, Kseg = 1, T_alloc = 128, M = 1;
+  int bands = 1;       // mas_fwd4: launches of K*W*128 rows each (text longer than a cluster)
+  int band_rows = 128;
 };
 
 int forward_variant() {
@@ -223,7 +225,14 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
     // lead); the first that runs the whole batch in the fewest waves of
     // co-resident clusters wins (cudaOccupancyMaxActiveClusters accounts
     // for shared memory and the GPC placement of clusters).
-    const int warps = std::max(1, (t_max + 127) / 128);
+    // Texts longer than one cluster of 16 CTAs x 4 warps x 128 rows run in
+    // bands of that height, one launch each (see mas_fwd4.cu, banded mode).
+    static const int band_warps_cap = [] {
+      const char* e = std::getenv("MAS_BAND_WARPS");  // test hook: force short bands
+      return e ? std::max(1, std::min(4 * mas::kMaxClusterCtas, std::atoi(e)))
+               : 4 * mas::kMaxClusterCtas;
+    }();
+    const int warps = std::min(std::max(1, (t_max + 127) / 128), band_warps_cap);
     static const int cand[][2] = {{2, 4}, {4, 3}, {2, 3}, {1, 4}, {2, 2}, {4, 2}, {1, 2}};
     int best = -1;
     int64_t best_waves = 0;
@@ -244,7 +253,9 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
       if (waves == 1) break;
     }
     if (best < 0) return false;
-    g->T_alloc = g->K * g->W * 128;
+    g->band_rows = g->K * g->W * 128;
+    g->bands = (std::max(t_max, 1) + g->band_rows - 1) / g->band_rows;
+    g->T_alloc = g->bands * g->band_rows;
     return true;
   }
   const int warps = std::max(1, (t_max + mas::kRowsPerWarp - 1) / mas::kRowsPerWarp);
@@ -338,6 +349,8 @@ struct mas_plan {
   int launches = 0;
   int device = 0;
   int bt_rows = 64;       // backtrack window rows
+  float* d_bnd = nullptr; // banded forward: 2 x [B][bnd_pitch] boundary rows
+  int bnd_pitch = 0;
   bool internal = false;  // created by mas_align_host / _device, which order the frees
   int item_base = 0;      // added to item indices in messages (validate_item of one item)
 };
@@ -373,6 +386,7 @@ void mas_plan_destroy(mas_plan_t* p) {
   cudaFreeAsync(p->d_dirs, st);
   cudaFreeAsync(p->d_flags, st);
   cudaFreeAsync(p->d_locate, st);
+  if (p->d_bnd) cudaFreeAsync(p->d_bnd, st);
   cudaSetDevice(prev);
   delete p;
 }
@@ -481,6 +495,12 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
     return e ? std::max(16, std::min(256, std::atoi(e))) & ~15 : 256;
   }();
   p->bt_rows = std::min(bt_rows_cap, g.T_alloc);
+  if (g.bands > 1) {
+    p->bnd_pitch = (speech_cap + 31) & ~31;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_bnd),
+                             2 * nB * p->bnd_pitch * sizeof(float), st)) != cudaSuccess)
+      return fail(e, "cudaMallocAsync(boundary rows)");
+  }
   if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_flags), nB * sizeof(int), st)) !=
       cudaSuccess)
     return fail(e, "cudaMallocAsync(flags)");
@@ -574,11 +594,26 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     fa.zero = 0.0f;
     fa.T_cap = p->T;
     fa.S_cap = p->S;
-    if (r4)
-      MAS_CUDA(mas::launch_fwd4(p->mode, tm0, tm_out, fa, nb, stream), "launch mas_fwd4");
-    else
+    fa.row_base = 0;
+    fa.bnd_in = nullptr;
+    fa.bnd_out = nullptr;
+    fa.bnd_pitch = p->bnd_pitch;
+    if (r4) {
+      // One launch per band of K*W*128 rows; band k's bottom row reaches
+      // band k+1 through a [B][bnd_pitch] boundary buffer (double-buffered).
+      for (int band = 0; band < g.bands; ++band) {
+        const size_t half = static_cast<size_t>(p->B) * p->bnd_pitch;
+        fa.row_base = band * g.band_rows;
+        fa.bnd_in = band > 0 ? p->d_bnd + ((band - 1) & 1) * half : nullptr;
+        fa.bnd_out = band + 1 < g.bands ? p->d_bnd + (band & 1) * half : nullptr;
+        MAS_CUDA(mas::launch_fwd4(p->mode, tm0, tm_out, fa, nb, stream), "launch mas_fwd4");
+      }
+      nfwd = g.bands;
+    } else
+    {
       MAS_CUDA(mas::launch_fwd(p->mode, tm0, tm1, tm_out, fa, nb, stream), "launch mas_fwd");
-    nfwd = 1;
+      nfwd = 1;
+    }
   }
   if ((parts & MAS_PART_BACKTRACK) && (d_out || d_paths)) {
     mas::BtArgs ba;

@@ -52,8 +52,10 @@ __host__ __device__ inline Smem4 smem4_layout(int W, int N) {
   L.ebars = L.bars + static_cast<uint32_t>(W * N * 8);
   L.full = L.ebars + static_cast<uint32_t>(W * N * 8);
   L.empty = L.full + static_cast<uint32_t>(W * kFifoSlots * 8);
-  L.sink = L.empty + static_cast<uint32_t>(W * kFifoIt4 * 8);
-  L.fifo = (L.sink + static_cast<uint32_t>(W * 16) + 127u) & ~127u;
+  // one extra "empty" set and sink (index W): the band feeder's, when the
+  // first warp of a band gets its row above from global memory
+  L.sink = L.empty + static_cast<uint32_t>((W + 1) * kFifoIt4 * 8);
+  L.fifo = (L.sink + static_cast<uint32_t>((W + 1) * 16) + 127u) & ~127u;
   L.zero = L.fifo + static_cast<uint32_t>(W * kFifoSlots * kSlot4);
   L.total = L.zero + static_cast<uint32_t>(kRows4 * kCols4);  // uint8 zero tile
   return L;
@@ -71,6 +73,7 @@ struct Fifo4 {
   uint32_t prev_empty, prev_sink;  // producer's "empty" barriers and release sink
   const uint8_t* buf;              // my FIFO's slots
   bool has_in, has_out;
+  float* bnd_out;                  // banded mode: the band's bottom row, this item (or null)
 };
 
 __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
@@ -238,6 +241,13 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
     for (int q4 = 0; q4 < kQuad / 4; ++q4)
       st_async_v4(dst + 16u * q4, ex[4 * q4], ex[4 * q4 + 1], ex[4 * q4 + 2], ex[4 * q4 + 3], fbar);
   }
+  if (F.bnd_out != nullptr && is31) {
+    // last warp of a band: its bottom row feeds the next band's first warp
+    float4* dst = reinterpret_cast<float4*>(F.bnd_out + q * kQuad);
+#pragma unroll
+    for (int q4 = 0; q4 < kQuad / 4; ++q4)
+      dst[q4] = make_float4(ex[4 * q4], ex[4 * q4 + 1], ex[4 * q4 + 2], ex[4 * q4 + 3]);
+  }
   return ok;
 }
 
@@ -297,9 +307,11 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   asm volatile("mov.u32 %0, %%smid;" : "=r"(tl_smid));
 #endif
 
+  const int band = a.row_base;  // first text row of this launch (banded mode)
+  const bool fed = band > 0 && a.bnd_in != nullptr;  // band's first warp fed from global
   if (warp < W) {
     const int g = crank * W + warp;
-    const bool has_in = g > 0;
+    const bool has_in = g > 0 || fed;
     const uint32_t bar0 = base + SL.bars + static_cast<uint32_t>(warp * N * 8);
     const uint32_t ebar0 = base + SL.ebars + static_cast<uint32_t>(warp * N * 8);
     const uint32_t my_full = base + SL.full + static_cast<uint32_t>(warp * kFifoSlots * 8);
@@ -323,6 +335,9 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   } else {
     for (int k = lane; k < kRows4 * kCols4 / 16; k += 32)
       reinterpret_cast<uint4*>(sbase + SL.zero)[k] = make_uint4(0u, 0u, 0u, 0u);
+    if (lane == 0)
+      for (int s = 0; s < kFifoIt4; ++s)
+        mbar_init(base + SL.empty + static_cast<uint32_t>((W * kFifoIt4 + s) * 8), 1u);
   }
   fence_proxy_async_smem();
   fence_mbar_init();
@@ -339,7 +354,33 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     // a ring refill finds its data in L2 when DRAM latency exceeds the
     // ring's lead.
     const int w = lane;
-    const int i0w = (crank * W + w) * kRows4;
+    const int i0w = band + (crank * W + w) * kRows4;
+    if (w == W && fed && crank == 0 && s_b > 0 && band < t_b) {
+      // Band feeder: the band's first warp (warp 0 of rank 0) gets the row
+      // above the band, written by the previous band's last warp, through
+      // its ordinary FIFO: 64-byte bulk copies completing its "full"
+      // barriers; slots are released to this lane's "empty" set (index W).
+      const float* src = a.bnd_in + static_cast<size_t>(b) * a.bnd_pitch;
+      const uint32_t fempty = base + SL.empty + static_cast<uint32_t>(W * kFifoIt4 * 8);
+      for (int m = 0; m < nit; ++m) {
+        if (m >= kFifoIt4) {
+          const uint32_t eb = fempty + 8u * static_cast<uint32_t>(m % kFifoIt4);
+          mbar_arrive_expect_tx(eb, 4u);
+          mbar_wait(eb, (static_cast<uint32_t>(m / kFifoIt4) & 1u) ^ 1u);
+        }
+        const int nvalid = s_b - m * kCols4 < kCols4 ? s_b - m * kCols4 : kCols4;
+        for (int k = 0; k < kQuadsPerStage && k * kQuad < nvalid; ++k) {
+          const int qq = kQuadsPerStage * m + k;
+          const int fs = qq & (kFifoSlots - 1);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  base + SL.fifo + static_cast<uint32_t>(fs * kSlot4)),
+              "l"(src + qq * kQuad), "r"(kSlot4),
+              "r"(base + SL.full + static_cast<uint32_t>(fs * 8))
+              : "memory");
+        }
+      }
+    }
     if (w < W && s_b > 0 && i0w < t_b) {
       prefetch_tensormap(&tmq);
       const uint64_t pol_q = policy_evict_first();
@@ -371,8 +412,9 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   }
 
   const int g = crank * W + warp;
-  const int i0 = g * kRows4;
-  const bool has_in = g > 0;
+  const int i0 = band + g * kRows4;
+  const bool has_in = g > 0 || fed;
+  const bool last_in_band = g == a.K * W - 1;
   const bool live = i0 < t_b && s_b > 0;
   if (live) {
     const uint32_t bar0 = base + SL.bars + static_cast<uint32_t>(warp * N * 8);
@@ -380,14 +422,17 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     const uint32_t my_full = base + SL.full + static_cast<uint32_t>(warp * kFifoSlots * 8);
     const uint32_t my_empty = base + SL.empty + static_cast<uint32_t>(warp * kFifoIt4 * 8);
     uint8_t* const my_fifo = sbase + SL.fifo + warp * kFifoSlots * kSlot4;
-    const bool has_out = i0 + kRows4 < t_b;
+    const bool has_out = i0 + kRows4 < t_b && !last_in_band;
     int nw = warp + 1, nr = crank;
     if (nw == W) {
       nw = 0;
       nr = crank + 1;
     }
     int pw = warp - 1, pr = crank;
-    if (pw < 0) {
+    if (g == 0) {  // fed by the band feeder (producer warp lane W)
+      pw = W;
+      pr = crank;
+    } else if (pw < 0) {
       pw = W - 1;
       pr = crank - 1;
     }
@@ -404,6 +449,9 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     F.buf = my_fifo;
     F.has_in = has_in;
     F.has_out = has_out;
+    F.bnd_out = last_in_band && a.bnd_out != nullptr && i0 + kRows4 < t_b
+                    ? a.bnd_out + static_cast<size_t>(b) * a.bnd_pitch
+                    : nullptr;
 
     const uint8_t* ring_ptr = sbase + SL.ring + warp * N * kStage4;
     uint32_t coff[8];

@@ -39,6 +39,14 @@ struct FwdArgs {
   int zero_fill;            // 1: TMA-store zero tiles of the output (tm_out) as we go
   int T_cap, S_cap;         // output shape
   int l2_ahead;             // mas_fwd4: stages prefetched into L2 beyond the smem ring
+  // mas_fwd4 banded mode (text longer than one cluster's rows): this launch
+  // computes rows [row_base, row_base + K*W*128); the row above row_base
+  // comes from bnd_in, this band's bottom row goes to bnd_out (both
+  // [B][bnd_pitch] floats, one value per column, or null).
+  int row_base;
+  const float* bnd_in;
+  float* bnd_out;
+  int bnd_pitch;
   uint32_t one;             // 1 and 0.0f passed at run time so ptxas keeps the
   float zero;               //   bit IMADs / NonFinite FFMAs on the FMA pipe
 };

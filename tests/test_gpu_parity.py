@@ -352,3 +352,52 @@ def test_config_c2_ragged_glowtts(mas, oracle, cuda):
         out = mas.align(arr, lengths=lengths)
         assert sha(out) == exp_sha
     _invariants(out, lengths)
+
+
+@pytest.mark.parametrize("shape", [(2, 900, 1500), (3, 1300, 2100), (1, 2048, 2048)])
+def test_banded_forward_small_bands(mas, oracle, cuda, shape):
+    """Texts taller than one cluster run in bands (mas_fwd4.cu banded mode);
+    MAS_BAND_WARPS=2 forces 256-row bands so band hand-offs are exercised
+    at oracle-friendly sizes.  Runs in a subprocess (the cap is read once)."""
+    import os
+    import subprocess
+    import sys
+
+    B, T, S = shape
+    code = f"""
+import sys, numpy as np
+sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))})
+import paper_2409_07704_b200 as m
+from oracle.oracle import Oracle
+o = Oracle()
+rng = np.random.default_rng({B * T})
+q = rng.uniform(-5, 5, ({B}, {T}, {S})).astype(np.float32)
+lt = np.array([{T}] + [int(x) for x in rng.integers(1, {T} + 1, {B} - 1)])
+ls = np.array([max(int(a), int(rng.integers(a, {S} + 1))) for a in lt])
+lens = np.stack([lt, ls], 1)
+assert m.Plan({B}, {T}, {S} + 3 - ({S} + 3) % 4, lengths=lens).geometry['rows_per_warp'] == 128
+for eng in ('parallel', 'reference'):
+    got = m.align(q, lengths=lens, engine=eng)
+    exp = o.align(q, lens, engine=eng)[3]
+    assert np.array_equal(got, exp), (eng, int((got != exp).sum()))
+    gp = m.align_paths(q, lengths=lens, engine=eng)
+    ep = o.align(q, lens, engine=eng)[4]
+    for b in range({B}):
+        assert np.array_equal(gp[b], ep[b, :ls[b]]), (eng, b)
+print('OK')
+"""
+    env = dict(os.environ, MAS_BAND_WARPS="2")
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         timeout=600)
+    assert res.returncode == 0 and "OK" in res.stdout, res.stdout[-2000:] + res.stderr[-3000:]
+
+
+@pytest.mark.slow
+def test_text_longer_than_a_cluster(mas, oracle, cuda):
+    """T > 8192 (more than 16 CTAs x 4 warps x 128 rows): two bands."""
+    rng = np.random.default_rng(9001)
+    T, S = 9000, 9300
+    q = rng.uniform(-5, 5, (1, T, S)).astype(np.float32)
+    got = mas.align_paths(q)
+    exp = oracle.align(q)[4]
+    np.testing.assert_array_equal(got[0], exp[0])
