@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define MAS_ABI_VERSION 1
+#define MAS_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define MAS_API __attribute__((visibility("default")))
@@ -120,6 +120,13 @@ MAS_API void mas_config_default(mas_config_t* cfg);
 MAS_API int mas_align_host(const float* values, int32_t batch, int32_t text_cap, int32_t speech_cap,
                    const uint32_t* lengths, const mas_config_t* cfg, uint8_t* out,
                    int32_t* paths, mas_error_t* err);
+/* The same plus per-token durations (ABI 2):
+ *   durations [batch][text_cap] int32, the row sums of the alignment
+ *   (columns spent on each text row; 0 past the item's text length), or NULL.
+ * With out == NULL the dense [B][T][S] output is neither zeroed nor written. */
+MAS_API int mas_align_host_ex(const float* values, int32_t batch, int32_t text_cap,
+                      int32_t speech_cap, const uint32_t* lengths, const mas_config_t* cfg,
+                      uint8_t* out, int32_t* paths, int32_t* durations, mas_error_t* err);
 
 /*
  * Device buffers (caller-owned, current device).  `row_pitch` = elements
@@ -130,6 +137,11 @@ MAS_API int mas_align_host(const float* values, int32_t batch, int32_t text_cap,
 MAS_API int mas_align_device(const float* d_values, int64_t row_pitch, int32_t batch, int32_t text_cap,
                      int32_t speech_cap, const uint32_t* lengths, const mas_config_t* cfg,
                      uint8_t* d_out, int32_t* d_paths, void* stream, mas_error_t* err);
+/* ... plus device durations [batch][text_cap] int32 (see mas_align_host_ex). */
+MAS_API int mas_align_device_ex(const float* d_values, int64_t row_pitch, int32_t batch,
+                        int32_t text_cap, int32_t speech_cap, const uint32_t* lengths,
+                        const mas_config_t* cfg, uint8_t* d_out, int32_t* d_paths,
+                        int32_t* d_durations, void* stream, mas_error_t* err);
 
 /* ---- plan API: validation + workspace once, enqueue-only execution ------ */
 typedef struct mas_plan mas_plan_t;
@@ -152,6 +164,10 @@ MAS_API int mas_plan_enqueue(mas_plan_t* plan, const float* d_values, uint8_t* d
 #define MAS_PART_ALL 0x3u
 MAS_API int mas_plan_enqueue_part(mas_plan_t* plan, uint32_t parts, const float* d_values,
                           uint8_t* d_out, int32_t* d_paths, void* stream, mas_error_t* err);
+/* mas_plan_enqueue_part plus device durations [batch][text_cap] int32. */
+MAS_API int mas_plan_enqueue_ex(mas_plan_t* plan, uint32_t parts, const float* d_values,
+                        uint8_t* d_out, int32_t* d_paths, int32_t* d_durations, void* stream,
+                        mas_error_t* err);
 /* Synchronises `stream` and turns device-side NonFinite flags and recorded
  * host-side item errors into the reference's error (or MAS_OK). */
 MAS_API int mas_plan_finish(mas_plan_t* plan, const float* d_values, void* stream, mas_error_t* err);

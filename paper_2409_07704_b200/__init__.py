@@ -12,6 +12,7 @@ from .api import (
     __version__,
     _align_unchecked,
     align,
+    align_durations,
     align_paths,
     generate_device,
     generate_random_batch,
@@ -21,6 +22,7 @@ __all__ = [
     "__version__",
     "align",
     "align_paths",
+    "align_durations",
     "generate_random_batch",
     "generate_device",
     "Plan",

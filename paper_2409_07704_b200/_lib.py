@@ -64,15 +64,23 @@ _SIGS = {
     "mas_align_host": (ctypes.c_int, [_VP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _VP,
                                       ctypes.POINTER(MasConfig), _VP, _VP,
                                       ctypes.POINTER(MasError)]),
+    "mas_align_host_ex": (ctypes.c_int, [_VP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                         _VP, ctypes.POINTER(MasConfig), _VP, _VP, _VP,
+                                         ctypes.POINTER(MasError)]),
     "mas_align_device": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                         ctypes.c_int32, _VP, ctypes.POINTER(MasConfig), _VP, _VP,
                                         _VP, ctypes.POINTER(MasError)]),
+    "mas_align_device_ex": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.c_int32, _VP, ctypes.POINTER(MasConfig), _VP,
+                                           _VP, _VP, _VP, ctypes.POINTER(MasError)]),
     "mas_plan_create": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                        ctypes.c_int64, _VP, ctypes.POINTER(MasConfig),
                                        ctypes.POINTER(_VP), ctypes.POINTER(MasError)]),
     "mas_plan_enqueue": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, ctypes.POINTER(MasError)]),
     "mas_plan_enqueue_part": (ctypes.c_int, [_VP, ctypes.c_uint32, _VP, _VP, _VP, _VP,
                                              ctypes.POINTER(MasError)]),
+    "mas_plan_enqueue_ex": (ctypes.c_int, [_VP, ctypes.c_uint32, _VP, _VP, _VP, _VP, _VP,
+                                           ctypes.POINTER(MasError)]),
     "mas_plan_finish": (ctypes.c_int, [_VP, _VP, _VP, ctypes.POINTER(MasError)]),
     "mas_plan_launches": (ctypes.c_int, [_VP]),
     "mas_plan_geometry": (None, [_VP, ctypes.POINTER(ctypes.c_int32 * 6)]),

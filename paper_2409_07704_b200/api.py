@@ -85,20 +85,26 @@ def _prepare(values, lengths, engine, max_neg_val, threads, unchecked):
     return values, lens, cfg, was_2d, b, t, s
 
 
-def _run_host(values, lens, cfg, b, t, s, want_out, want_paths):
+def _ptr(a, attr):
+    return None if a is None else getattr(a, attr)
+
+
+def _run_host(values, lens, cfg, b, t, s, want_out, want_paths, want_dur=False):
     lib = _lib.load()
     out = np.empty((b, t, s), np.uint8) if want_out else None
     paths = np.empty((b, s), np.int32) if want_paths else None
+    dur = np.empty((b, t), np.int32) if want_dur else None
     err = _lib.MasError()
-    rc = lib.mas_align_host(
+    rc = lib.mas_align_host_ex(
         values.ctypes.data, b, t, s, None if lens is None else lens.ctypes.data,
         ctypes.byref(cfg), None if out is None else out.ctypes.data,
-        None if paths is None else paths.ctypes.data, ctypes.byref(err))
+        None if paths is None else paths.ctypes.data, None if dur is None else dur.ctypes.data,
+        ctypes.byref(err))
     _lib.raise_for(rc, err)
-    return out, paths
+    return out, paths, dur
 
 
-def _run_device(values, lens, cfg, b, t, s, want_out, want_paths):
+def _run_device(values, lens, cfg, b, t, s, want_out, want_paths, want_dur=False):
     import torch
 
     lib = _lib.load()
@@ -111,28 +117,30 @@ def _run_device(values, lens, cfg, b, t, s, want_out, want_paths):
     pitch = values.stride(1)
     out = torch.empty((b, t, s), dtype=torch.uint8, device=dev) if want_out else None
     paths = torch.empty((b, s), dtype=torch.int32, device=dev) if want_paths else None
+    dur = torch.empty((b, t), dtype=torch.int32, device=dev) if want_dur else None
     err = _lib.MasError()
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev)
-        rc = lib.mas_align_device(
+        rc = lib.mas_align_device_ex(
             values.data_ptr(), pitch, b, t, s, None if lens is None else lens.ctypes.data,
             ctypes.byref(cfg), None if out is None else out.data_ptr(),
-            None if paths is None else paths.data_ptr(), ctypes.c_void_p(stream.cuda_stream),
-            ctypes.byref(err))
+            None if paths is None else paths.data_ptr(), None if dur is None else dur.data_ptr(),
+            ctypes.c_void_p(stream.cuda_stream), ctypes.byref(err))
     _lib.raise_for(rc, err)
-    return out, paths
+    return out, paths, dur
 
 
-def _align_impl(values, lengths, engine, max_neg_val, threads, unchecked, want_out, want_paths):
+def _align_impl(values, lengths, engine, max_neg_val, threads, unchecked, want_out, want_paths,
+                want_dur=False):
     values, lens, cfg, was_2d, b, t, s = _prepare(values, lengths, engine, max_neg_val, threads,
                                                   unchecked)
     if _is_torch(values) and values.is_cuda:
-        out, paths = _run_device(values, lens, cfg, b, t, s, want_out, want_paths)
+        out, paths, dur = _run_device(values, lens, cfg, b, t, s, want_out, want_paths, want_dur)
     else:
         if _is_torch(values):
             values = np.ascontiguousarray(values.detach().numpy(), dtype=np.float32)
-        out, paths = _run_host(values, lens, cfg, b, t, s, want_out, want_paths)
-    return out, paths, was_2d, lens, b, s
+        out, paths, dur = _run_host(values, lens, cfg, b, t, s, want_out, want_paths, want_dur)
+    return out, paths, dur, was_2d, lens, b, s
 
 
 def align(values, lengths=None, engine="parallel", max_neg_val=_DEFAULT_MAX_NEG_VAL, threads=0):
@@ -140,9 +148,22 @@ def align(values, lengths=None, engine="parallel", max_neg_val=_DEFAULT_MAX_NEG_
     alignment array of the same shape. Optional lengths ([B, 2] of (t, s))
     mark each item's valid region.  (module.cpp:222-228; torch CUDA tensors
     in -> torch CUDA tensor out.)"""
-    out, _, was_2d, _, _, _ = _align_impl(values, lengths, engine, max_neg_val, threads, False,
-                                          True, False)
+    out, _, _, was_2d, _, _, _ = _align_impl(values, lengths, engine, max_neg_val, threads, False,
+                                             True, False)
     return out[0] if was_2d else out
+
+
+def align_durations(values, lengths=None, engine="parallel", max_neg_val=_DEFAULT_MAX_NEG_VAL,
+                    threads=0):
+    """Per-token durations: the row sums of ``align``'s alignment, int32
+    [B, T] ([T] for 2-D input) -- the number of speech frames spent on each
+    text token, 0 past an item's text length.  Not in the reference's
+    surface: the dense uint8 [B, T, S] output is
+    never written, so the call moves 4.125 instead of 5.125 bytes per cell.
+    Same arguments, checks and errors as ``align``."""
+    _, _, dur, was_2d, _, _, _ = _align_impl(values, lengths, engine, max_neg_val, threads, False,
+                                             False, False, True)
+    return dur[0] if was_2d else dur
 
 
 def align_paths(values, lengths=None, engine="parallel", max_neg_val=_DEFAULT_MAX_NEG_VAL,
@@ -150,8 +171,8 @@ def align_paths(values, lengths=None, engine="parallel", max_neg_val=_DEFAULT_MA
     """Like align, but returns per-frame text indices: one int32 array per
     item (a single array for 2-D input).  Each item's array has length s_b
     (path_from_matrix walks the item's valid lengths, types.cpp:161-179)."""
-    _, paths, was_2d, lens, b, s = _align_impl(values, lengths, engine, max_neg_val, threads,
-                                               False, False, True)
+    _, paths, _, was_2d, lens, b, s = _align_impl(values, lengths, engine, max_neg_val, threads,
+                                                  False, False, True)
     result = []
     for i in range(b):
         sb = s if lens is None else int(lens[i, 1])
@@ -165,8 +186,8 @@ def _align_unchecked(values, lengths=None, engine="parallel", max_neg_val=_DEFAU
     (parallel.hpp:29-31, reference.hpp:42-44): no validate_config, so -inf and
     -1e9 sentinels run.  Not part of the reference's Python surface; needed
     for the sentinel boundary checks."""
-    out, _, was_2d, _, _, _ = _align_impl(values, lengths, engine, max_neg_val, threads, True,
-                                          True, False)
+    out, _, _, was_2d, _, _, _ = _align_impl(values, lengths, engine, max_neg_val, threads, True,
+                                             True, False)
     return out[0] if was_2d else out
 
 
@@ -226,15 +247,19 @@ class Plan:
         _lib.raise_for(rc, err)
         self._h = handle
 
-    def enqueue(self, values, out=None, paths=None, stream=None, parts=_lib.MAS_PART_ALL):
-        """Enqueues the kernels (`parts`: MAS_PART_FORWARD / _BACKTRACK bits)."""
+    def enqueue(self, values, out=None, paths=None, stream=None, parts=_lib.MAS_PART_ALL,
+                durations=None):
+        """Enqueues the kernels (`parts`: MAS_PART_FORWARD / _BACKTRACK bits)
+        writing any of out [B,T,S] uint8, paths [B,S] int32, durations [B,T]
+        int32 (device tensors)."""
         import torch
 
         err = _lib.MasError()
         st = torch.cuda.current_stream() if stream is None else stream
-        rc = self._lib.mas_plan_enqueue_part(
+        rc = self._lib.mas_plan_enqueue_ex(
             self._h, parts, values.data_ptr(), None if out is None else out.data_ptr(),
-            None if paths is None else paths.data_ptr(), ctypes.c_void_p(st.cuda_stream),
+            None if paths is None else paths.data_ptr(),
+            None if durations is None else durations.data_ptr(), ctypes.c_void_p(st.cuda_stream),
             ctypes.byref(err))
         _lib.raise_for(rc, err)
 

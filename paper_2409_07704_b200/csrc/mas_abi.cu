@@ -192,15 +192,19 @@ bool encode_out_map(uint8_t* out, int64_t rows, int64_t S, CUtensorMap* m) {
 
 
 struct Geometry {
-  int R = 4;  // text rows per lane: 4 (mas_fwd4.cu, default) or 2 (mas_fwd.cu)
+  int R = 4;            // text rows per lane of mas_fwd4.cu: 4 (default) or 2
+  bool legacy = false;  // mas_fwd.cu (two rows per lane, MAS_FWD=old)
   int W = 1, K = 1, N = 2, L = 256, Kseg = 1, T_alloc = 128, M = 1;
   int bands = 1;       // mas_fwd4: launches of K*W*128 rows each (text longer than a cluster)
   int band_rows = 128;
 };
 
+// K1 selection (A/B switch): MAS_FWD=4 / 2 picks the rows per lane of
+// mas_fwd4.cu, MAS_FWD=old the legacy mas_fwd.cu; default 4.
 int forward_variant() {
   static const int v = [] {
-    const char* e = std::getenv("MAS_FWD");  // A/B switch between the two K1 kernels
+    const char* e = std::getenv("MAS_FWD");
+    if (e && std::strcmp(e, "old") == 0) return 0;
     return e && e[0] == '2' ? 2 : 4;
   }();
   return v;
@@ -214,33 +218,39 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const size_t budget = 220 * 1024;
-  g->R = forward_variant();
+  const int variant = forward_variant();
+  g->legacy = variant == 0;
+  g->R = g->legacy ? 2 : variant;
   g->M = (S_cap + 31) / 32;
   g->L = 256;
   g->Kseg = (S_cap + g->L - 1) / g->L;
-  if (g->R == 4) {
-    // 128 rows per warp; an item's warps form one cluster of K CTAs of W
+  if (!g->legacy) {
+    // 32 R rows per warp; an item's warps form one cluster of K CTAs of W
     // compute warps.  Candidates in order of preference (few warps per CTA
     // spread an item over more SMs; more stages give the TMA ring more
     // lead); the first that runs the whole batch in the fewest waves of
     // co-resident clusters wins (cudaOccupancyMaxActiveClusters accounts
     // for shared memory and the GPC placement of clusters).
-    // Texts longer than one cluster of 16 CTAs x 4 warps x 128 rows run in
+    // Texts longer than one cluster of 16 CTAs x 4 warps x 32 R rows run in
     // bands of that height, one launch each (see mas_fwd4.cu, banded mode).
     static const int band_warps_cap = [] {
       const char* e = std::getenv("MAS_BAND_WARPS");  // test hook: force short bands
       return e ? std::max(1, std::min(4 * mas::kMaxClusterCtas, std::atoi(e)))
                : 4 * mas::kMaxClusterCtas;
     }();
-    const int warps = std::min(std::max(1, (t_max + 127) / 128), band_warps_cap);
-    static const int cand[][2] = {{2, 4}, {4, 3}, {2, 3}, {1, 4}, {2, 2}, {4, 2}, {1, 2}};
+    const int rows = 32 * g->R;
+    const int warps = std::min(std::max(1, (t_max + rows - 1) / rows), band_warps_cap);
+    static const int cand4[][2] = {{2, 4}, {4, 3}, {2, 3}, {1, 4}, {2, 2}, {4, 2}, {1, 2}};
+    static const int cand2[][2] = {{4, 4}, {4, 3}, {2, 4}, {2, 3}, {4, 2}, {1, 4}, {1, 2}};
+    const int(*cand)[2] = g->R == 4 ? cand4 : cand2;
+    const int ncand = 7;
     int best = -1;
     int64_t best_waves = 0;
-    for (int c = 0; c < static_cast<int>(sizeof(cand) / sizeof(cand[0])); ++c) {
+    for (int c = 0; c < ncand; ++c) {
       const int W = std::min(cand[c][0], warps), N = cand[c][1];
       const int K = (warps + W - 1) / W;
-      if (K > mas::kMaxClusterCtas || mas::fwd4_smem_bytes(W, N) > budget) continue;
-      const int act = mas::fwd4_max_active_clusters(W, N, K);
+      if (K > mas::kMaxClusterCtas || mas::fwd4_smem_bytes(g->R, W, N) > budget) continue;
+      const int act = mas::fwd4_max_active_clusters(g->R, W, N, K);
       if (act <= 0) continue;
       const int64_t waves = (static_cast<int64_t>(B) + act - 1) / act;
       if (best < 0 || waves < best_waves) {
@@ -253,7 +263,7 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
       if (waves == 1) break;
     }
     if (best < 0) return false;
-    g->band_rows = g->K * g->W * 128;
+    g->band_rows = g->K * g->W * rows;
     g->bands = (std::max(t_max, 1) + g->band_rows - 1) / g->band_rows;
     g->T_alloc = g->bands * g->band_rows;
     return true;
@@ -280,31 +290,32 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
   return true;
 }
 
-// The input [B*T_pad][pitch] as a 3-D tensor {columns, row groups of four,
-// row residue mod 4}: one {32, 32, 4} box is a 128-row x 32-column stage of
+// The input [B*T_pad][pitch] as a 3-D tensor {columns, row groups of R,
+// row residue mod R}: one {32, 32, R} box is a 32R-row x 32-column stage of
 // mas_fwd4.cu laid out [residue][group][column] (128-byte swizzle).
-bool encode_map4(const float* q, int64_t pitch, int64_t rows_total, int64_t S, CUtensorMap* m) {
+bool encode_map4(const float* q, int64_t pitch, int64_t rows_total, int64_t S, int R,
+                 CUtensorMap* m) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
-  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(rows_total / 4),
-                              4};
-  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(4 * pitch * 4),
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(rows_total / R),
+                              static_cast<cuuint64_t>(R)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(R * pitch * 4),
                                  static_cast<cuuint64_t>(pitch * 4)};
-  const cuuint32_t box[3] = {32, 32, 4};
+  const cuuint32_t box[3] = {32, 32, static_cast<cuuint32_t>(R)};
   const cuuint32_t estr[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(q), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// The uint8 output as {columns, rows} with 32 x 128 boxes (mas_fwd4.cu's
+// The uint8 output as {columns, rows} with 32 x 32R boxes (mas_fwd4.cu's
 // fused zero fill).
-bool encode_out_map4(uint8_t* out, int64_t rows, int64_t S, CUtensorMap* m) {
+bool encode_out_map4(uint8_t* out, int64_t rows, int64_t S, int R, CUtensorMap* m) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(S)};
-  const cuuint32_t box[2] = {32, 128};
+  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(32 * R)};
   const cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, out, dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -458,7 +469,7 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
       t_max = std::max<int>(t_max, static_cast<int>(t));
     }
   }
-  if (forward_variant() == 4 && mas::fwd4_configure() != cudaSuccess) {
+  if (forward_variant() != 0 && mas::fwd4_configure() != cudaSuccess) {
     delete p;
     return set_error(err, MAS_E_CUDA, -1, -1, "forward kernel configuration failed");
   }
@@ -473,7 +484,7 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
     return cuda_error(err, e, what);
   };
   cudaError_t e;
-  if ((e = g.R == 4 ? mas::fwd4_configure() : mas::fwd_configure(g.W, g.N, g.K)) != cudaSuccess)
+  if ((e = !g.legacy ? mas::fwd4_configure() : mas::fwd_configure(g.W, g.N, g.K)) != cudaSuccess)
     return fail(e, "fwd_configure");
   if ((e = mas::bt_configure(g.T_alloc, g.L)) != cudaSuccess) return fail(e, "bt_configure");
   if ((e = pool_setup(p->device)) != cudaSuccess) return fail(e, "memory pool setup");
@@ -519,8 +530,9 @@ extern "C" {
 int mas_plan_launches(const mas_plan_t* p) { return p ? p->launches : 0; }
 
 void mas_plan_geometry(const mas_plan_t* p, int32_t geom[6]) {
-  geom[5] = p->geo.R == 4 ? mas::fwd4_max_active_clusters(p->geo.W, p->geo.N, p->geo.K)
-                          : mas::fwd_max_active_clusters(p->geo.W, p->geo.N, p->geo.K, 0);
+  geom[5] = !p->geo.legacy
+                ? mas::fwd4_max_active_clusters(p->geo.R, p->geo.W, p->geo.N, p->geo.K)
+                : mas::fwd_max_active_clusters(p->geo.W, p->geo.N, p->geo.K, 0);
   geom[0] = 32 * p->geo.R;
   geom[1] = p->geo.W;
   geom[2] = p->geo.K;
@@ -535,7 +547,8 @@ namespace {
 // Enqueues the kernels (MAS_PART_* bits) for items [b0, b0 + nb) of the
 // plan's batch.  d_values / d_out / d_paths are the whole batch's buffers.
 int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_values,
-                  uint8_t* d_out, int32_t* d_paths, cudaStream_t stream, mas_error_t* err) {
+                  uint8_t* d_out, int32_t* d_paths, int32_t* d_dur, cudaStream_t stream,
+                  mas_error_t* err) {
   if ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (p->pitch & 3) != 0 || (p->T_pad & 3))
     return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
                      "device layout needs a 16-byte base, pitch % 4 == 0 and text_cap % 4 == 0");
@@ -543,8 +556,9 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
   int nfwd = 0, nbt = 0;
   if (parts & MAS_PART_FORWARD) {
     CUtensorMap tm0, tm1;
-    const bool r4 = g.R == 4;
-    if (r4 ? !encode_map4(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, &tm0)
+    const bool r4 = !g.legacy;
+    if (r4 ? !encode_map4(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, g.R,
+                          &tm0)
            : !encode_maps(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, &tm0,
                           &tm1))
       return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled failed");
@@ -579,7 +593,8 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     }
     CUtensorMap tm_out;
     std::memset(&tm_out, 0, sizeof(tm_out));
-    if (fused_zero && !(r4 ? encode_out_map4(d_out, static_cast<int64_t>(p->B) * p->T, p->S, &tm_out)
+    if (fused_zero && !(r4 ? encode_out_map4(d_out, static_cast<int64_t>(p->B) * p->T, p->S, g.R,
+                                             &tm_out)
                            : encode_out_map(d_out, static_cast<int64_t>(p->B) * p->T, p->S,
                                             &tm_out)))
       return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled(out) failed");
@@ -590,6 +605,11 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     }();
     // L2 prefetch lead (stages beyond the smem ring) when the ring is short.
     fa.l2_ahead = l2_ahead >= 0 ? l2_ahead : 0;  // measured: L2 prefetch only hurts
+    static const int self_tma = [] {
+      const char* e = std::getenv("MAS_SELF_TMA");  // experiment override
+      return e ? std::atoi(e) : -1;
+    }();
+    fa.self_tma = self_tma >= 0 ? self_tma : 0;
     fa.one = 1u;
     fa.zero = 0.0f;
     fa.T_cap = p->T;
@@ -606,7 +626,7 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
         fa.row_base = band * g.band_rows;
         fa.bnd_in = band > 0 ? p->d_bnd + ((band - 1) & 1) * half : nullptr;
         fa.bnd_out = band + 1 < g.bands ? p->d_bnd + (band & 1) * half : nullptr;
-        MAS_CUDA(mas::launch_fwd4(p->mode, tm0, tm_out, fa, nb, stream), "launch mas_fwd4");
+        MAS_CUDA(mas::launch_fwd4(g.R, p->mode, tm0, tm_out, fa, nb, stream), "launch mas_fwd4");
       }
       nfwd = g.bands;
     } else
@@ -615,13 +635,14 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
       nfwd = 1;
     }
   }
-  if ((parts & MAS_PART_BACKTRACK) && (d_out || d_paths)) {
+  if ((parts & MAS_PART_BACKTRACK) && (d_out || d_paths || d_dur)) {
     mas::BtArgs ba;
     ba.b0 = b0;
     ba.lengths = p->d_lengths;
     ba.dirs = p->d_dirs;
     ba.path = d_paths;
     ba.out = d_out;
+    ba.dur = d_dur;
     ba.B = nb;
     ba.T_cap = p->T;
     ba.S_cap = p->S;
@@ -640,13 +661,19 @@ extern "C" {
 
 int mas_plan_enqueue(mas_plan_t* p, const float* d_values, uint8_t* d_out, int32_t* d_paths,
                      void* stream_v, mas_error_t* err) {
-  return mas_plan_enqueue_part(p, MAS_PART_ALL, d_values, d_out, d_paths, stream_v, err);
+  return mas_plan_enqueue_ex(p, MAS_PART_ALL, d_values, d_out, d_paths, nullptr, stream_v, err);
 }
 
 int mas_plan_enqueue_part(mas_plan_t* p, uint32_t parts, const float* d_values, uint8_t* d_out,
                           int32_t* d_paths, void* stream_v, mas_error_t* err) {
+  return mas_plan_enqueue_ex(p, parts, d_values, d_out, d_paths, nullptr, stream_v, err);
+}
+
+int mas_plan_enqueue_ex(mas_plan_t* p, uint32_t parts, const float* d_values, uint8_t* d_out,
+                        int32_t* d_paths, int32_t* d_durations, void* stream_v,
+                        mas_error_t* err) {
   clear_error(err);
-  return enqueue_items(p, parts, 0, p->B, d_values, d_out, d_paths,
+  return enqueue_items(p, parts, 0, p->B, d_values, d_out, d_paths, d_durations,
                        static_cast<cudaStream_t>(stream_v), err);
 }
 
@@ -694,6 +721,14 @@ int mas_plan_finish(mas_plan_t* p, const float* d_values, void* stream_v, mas_er
 int mas_align_device(const float* d_values, int64_t row_pitch, int32_t batch, int32_t text_cap,
                      int32_t speech_cap, const uint32_t* lengths, const mas_config_t* cfg,
                      uint8_t* d_out, int32_t* d_paths, void* stream_v, mas_error_t* err) {
+  return mas_align_device_ex(d_values, row_pitch, batch, text_cap, speech_cap, lengths, cfg, d_out,
+                             d_paths, nullptr, stream_v, err);
+}
+
+int mas_align_device_ex(const float* d_values, int64_t row_pitch, int32_t batch,
+                        int32_t text_cap, int32_t speech_cap, const uint32_t* lengths,
+                        const mas_config_t* cfg, uint8_t* d_out, int32_t* d_paths,
+                        int32_t* d_durations, void* stream_v, mas_error_t* err) {
   clear_error(err);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   mas_plan_t* plan = nullptr;
@@ -728,7 +763,7 @@ int mas_align_device(const float* d_values, int64_t row_pitch, int32_t batch, in
     plan->T_pad = T_pad;
     q = scratch;
   }
-  rc = mas_plan_enqueue(plan, q, d_out, d_paths, stream, err);
+  rc = mas_plan_enqueue_ex(plan, MAS_PART_ALL, q, d_out, d_paths, d_durations, stream, err);
   if (rc == MAS_OK) rc = mas_plan_finish(plan, q, stream, err);
   if (scratch) cudaFreeAsync(scratch, stream);
   cudaStreamSynchronize(stream);
@@ -742,7 +777,7 @@ namespace {
 
 int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_t speech_cap,
                     const uint32_t* lengths, const mas_config_t* cfg, uint8_t* out,
-                    int32_t* paths, int item_base, mas_error_t* err) {
+                    int32_t* paths, int32_t* durations, int item_base, mas_error_t* err) {
   clear_error(err);
   {
     mas_config_t c;
@@ -775,6 +810,7 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
   float* d_q = nullptr;
   uint8_t* d_out = nullptr;
   int32_t* d_paths = nullptr;
+  int32_t* d_dur = nullptr;
   cudaError_t e = cudaSuccess;
   for (int k = 0; k < 2 && e == cudaSuccess; ++k)
     e = cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
@@ -785,6 +821,9 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
   if (e == cudaSuccess && paths)
     e = cudaMallocAsync(reinterpret_cast<void**>(&d_paths),
                         static_cast<size_t>(batch) * speech_cap * sizeof(int32_t), st[0]);
+  if (e == cudaSuccess && durations)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&d_dur),
+                        static_cast<size_t>(batch) * text_cap * sizeof(int32_t), st[0]);
   cudaEvent_t ready = nullptr;
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventRecord(ready, st[0]);
@@ -804,7 +843,7 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
       rc = cuda_error(err, e, "host->device staging");
       break;
     }
-    rc = enqueue_items(plan, MAS_PART_ALL, b0, nb, d_q, d_out, d_paths, s, err);
+    rc = enqueue_items(plan, MAS_PART_ALL, b0, nb, d_q, d_out, d_paths, d_dur, s, err);
     if (rc != MAS_OK) break;
     if (out &&
         (e = cudaMemcpyAsync(out + b0 * o_item, d_out + b0 * o_item, nb * o_item,
@@ -816,6 +855,12 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
                              static_cast<size_t>(nb) * speech_cap * sizeof(int32_t),
                              cudaMemcpyDeviceToHost, s)) != cudaSuccess)
       rc = cuda_error(err, e, "device->host paths");
+    if (rc == MAS_OK && durations &&
+        (e = cudaMemcpyAsync(durations + static_cast<size_t>(b0) * text_cap,
+                             d_dur + static_cast<size_t>(b0) * text_cap,
+                             static_cast<size_t>(nb) * text_cap * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      rc = cuda_error(err, e, "device->host durations");
   }
   // Join the second stream into the first; the NonFinite check and the
   // frees follow on st[0].
@@ -827,6 +872,7 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
   if (d_q) cudaFreeAsync(d_q, st[0]);
   if (d_out) cudaFreeAsync(d_out, st[0]);
   if (d_paths) cudaFreeAsync(d_paths, st[0]);
+  if (d_dur) cudaFreeAsync(d_dur, st[0]);
   if (st[0]) cudaStreamSynchronize(st[0]);
   if (ready) cudaEventDestroy(ready);
   for (int k = 0; k < 2; ++k)
@@ -842,7 +888,15 @@ extern "C" {
 int mas_align_host(const float* values, int32_t batch, int32_t text_cap, int32_t speech_cap,
                    const uint32_t* lengths, const mas_config_t* cfg, uint8_t* out, int32_t* paths,
                    mas_error_t* err) {
-  return align_host_impl(values, batch, text_cap, speech_cap, lengths, cfg, out, paths, 0, err);
+  return align_host_impl(values, batch, text_cap, speech_cap, lengths, cfg, out, paths, nullptr, 0,
+                         err);
+}
+
+int mas_align_host_ex(const float* values, int32_t batch, int32_t text_cap, int32_t speech_cap,
+                      const uint32_t* lengths, const mas_config_t* cfg, uint8_t* out,
+                      int32_t* paths, int32_t* durations, mas_error_t* err) {
+  return align_host_impl(values, batch, text_cap, speech_cap, lengths, cfg, out, paths, durations,
+                         0, err);
 }
 
 int mas_validate_config(const mas_config_t* cfg, mas_error_t* err) {
@@ -862,7 +916,7 @@ int mas_validate_host(const float* values, int32_t batch, int32_t text_cap, int3
   mas_config_default(&c);
   c.flags = MAS_FLAG_UNCHECKED;
   return align_host_impl(values, batch, text_cap, speech_cap, lengths, &c, nullptr, nullptr,
-                         item_base, err);
+                         nullptr, item_base, err);
 }
 
 int mas_generate_device(uint64_t seed, int32_t batch, int32_t text_cap, int32_t speech_cap,

@@ -134,6 +134,14 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
 #ifndef MAS_BT_NO_PDL
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
+  // Durations (row sums of the alignment): zeroed here, accumulated by the
+  // expander below one run of equal rows per word at a time.
+  int32_t* dur = a.dur ? a.dur + static_cast<size_t>(b) * a.T_cap : nullptr;
+  if (dur) {
+    for (int i = threadIdx.x; i < a.T_cap; i += 64) dur[i] = 0;
+    __threadfence_block();
+  }
+  __syncthreads();
   if (t <= 0 || s <= 0) {
     int32_t* path = a.path ? a.path + static_cast<size_t>(b) * a.S_cap : nullptr;
     if (path)
@@ -308,6 +316,7 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
   if (lane == 0) {  // backtrack.hpp:23-24
     if (path) path[s - 1] = t - 1;
     if (out) out[static_cast<size_t>(t - 1) * a.S_cap + s - 1] = 1;
+    if (dur) atomicAdd(dur + (t - 1), 1);
   }
   if (s == 1) return;
   uint32_t ph_done = 0;
@@ -339,11 +348,24 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
 #pragma unroll
     for (int i = 0; i < kBtWords; ++i) {
       const int j = 256 * n + 32 * i + lane - 1;
-      if (j >= 0 && j <= s - 2) {
-        // exits at positions >= lane are bits <= 31 - lane
-        const int row = ry[i] - __popc(rx[i] << lane);
+      const bool valid = j >= 0 && j <= s - 2;
+      // exits at positions >= lane are bits <= 31 - lane
+      const int row = valid ? ry[i] - __popc(rx[i] << lane) : -1;
+      if (valid) {
         if (path) path[j] = row;
         if (out) out[static_cast<size_t>(row) * a.S_cap + j] = 1;
+      }
+      if (dur) {
+        // one atomic per run of equal rows among these 32 columns
+        const int prev = __shfl_up_sync(0xffffffffu, row, 1);
+        const int next = __shfl_down_sync(0xffffffffu, row, 1);
+        const bool start = valid && (lane == 0 || prev != row);
+        const bool end = valid && (lane == 31 || next != row);
+        const uint32_t starts = __ballot_sync(0xffffffffu, start);
+        if (end) {
+          const int first = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
+          atomicAdd(dur + row, lane - first + 1);
+        }
       }
     }
   }
@@ -357,6 +379,9 @@ __global__ void bt_serial_kernel(const BtArgs a) {
   const int b = a.b0 + bi;
   const int t = static_cast<int>(a.lengths[2 * b]);
   const int s = static_cast<int>(a.lengths[2 * b + 1]);
+  int32_t* dur = a.dur ? a.dur + static_cast<size_t>(b) * a.T_cap : nullptr;
+  if (dur)
+    for (int i = 0; i < a.T_cap; ++i) dur[i] = 0;
   if (t <= 0 || s <= 0) return;
   const uint32_t* src = a.dirs + static_cast<size_t>(b) * a.M * a.T_alloc;
   uint8_t* out = a.out ? a.out + static_cast<size_t>(b) * a.T_cap * a.S_cap : nullptr;
@@ -364,6 +389,7 @@ __global__ void bt_serial_kernel(const BtArgs a) {
   int cur = t - 1;
   if (out) out[static_cast<size_t>(cur) * a.S_cap + s - 1] = 1;
   if (prow) prow[s - 1] = cur;
+  if (dur) ++dur[cur];
   for (int j = s - 2; j >= 0; --j) {
     if (cur > 0) {
       const int p = j + 1;
@@ -372,6 +398,7 @@ __global__ void bt_serial_kernel(const BtArgs a) {
     }
     if (out) out[static_cast<size_t>(cur) * a.S_cap + j] = 1;
     if (prow) prow[j] = cur;
+    if (dur) ++dur[cur];
   }
 }
 

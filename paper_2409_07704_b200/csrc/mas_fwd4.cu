@@ -14,8 +14,12 @@
 //     {32 columns, 32 lane groups, 4 row residues} of a 3-D view of the
 //     input (rows split by i mod 4), 128-byte swizzle: every LDS.128 of a
 //     residue tile is conflict-free;
-//   * direction words: four rows x one word per 32-column stage, stored as
-//     one 16-byte STG per lane (L2 evict_last);
+//   * direction bits: FSET (0.0 / 1.0) + FFMA into a float accumulator per
+//     row and 16-column quad (no predicates, see bits4); four rows x one
+//     word per 32-column stage, stored as one 16-byte STG per lane (L2
+//     evict_last);
+//   * the compute warps wait and probe with warp-uniform votes, so a warp
+//     never enters a quad's shuffles partly diverged;
 //   * boundary row between warps: the same 16-column FIFO hand-offs with
 //     look-ahead mbarrier probes as mas_fwd.cu (st.async / DSMEM across the
 //     CTAs of a cluster);
@@ -32,10 +36,11 @@ namespace mas {
 
 namespace {
 
-constexpr int R4 = 4;                       // rows per lane
-constexpr int kRows4 = 32 * R4;             // rows per warp
-constexpr int kCols4 = 32;                  // columns per stage / direction word
-constexpr int kStage4 = kRows4 * kCols4 * 4;  // 16 KiB: [4 residues][32 groups][32 cols]
+// R = text rows per lane (4 or 2): a warp owns 32 R rows; a stage is one
+// [R residues][32 groups][32 cols] fp32 box (R * 4 KiB).
+constexpr int kCols4 = 32;  // columns per stage / direction word
+__host__ __device__ constexpr int rows_of(int R) { return 32 * R; }
+__host__ __device__ constexpr int stage_bytes(int R) { return rows_of(R) * kCols4 * 4; }
 constexpr int kQuad = kQuadCols;            // 16 columns per FIFO hand-off
 constexpr int kSlot4 = kQuad * 4;           // 64-byte FIFO slot
 constexpr int kQuadsPerStage = kCols4 / kQuad;
@@ -45,10 +50,10 @@ struct Smem4 {
   uint32_t ring, bars, ebars, full, empty, sink, fifo, zero, total;
 };
 
-__host__ __device__ inline Smem4 smem4_layout(int W, int N) {
+__host__ __device__ inline Smem4 smem4_layout(int R, int W, int N) {
   Smem4 L;
   L.ring = 0;
-  L.bars = static_cast<uint32_t>(W * N * kStage4);
+  L.bars = static_cast<uint32_t>(W * N * stage_bytes(R));
   L.ebars = L.bars + static_cast<uint32_t>(W * N * 8);
   L.full = L.ebars + static_cast<uint32_t>(W * N * 8);
   L.empty = L.full + static_cast<uint32_t>(W * kFifoSlots * 8);
@@ -57,12 +62,13 @@ __host__ __device__ inline Smem4 smem4_layout(int W, int N) {
   L.sink = L.empty + static_cast<uint32_t>((W + 1) * kFifoIt4 * 8);
   L.fifo = (L.sink + static_cast<uint32_t>((W + 1) * 16) + 127u) & ~127u;
   L.zero = L.fifo + static_cast<uint32_t>(W * kFifoSlots * kSlot4);
-  L.total = L.zero + static_cast<uint32_t>(kRows4 * kCols4);  // uint8 zero tile
+  L.total = L.zero + static_cast<uint32_t>(rows_of(R) * kCols4);  // uint8 zero tile
   return L;
 }
 
+template <int R>
 struct Lane4 {
-  float o[R4];  // Q of the lane's rows at the previous column
+  float o[R];   // Q of the lane's rows at the previous column
   float acc;    // max.NaN of |q|: NaN / +inf iff a non-finite q was seen
   float vlast;  // producer's bottom row at the previous column
 };
@@ -80,98 +86,97 @@ __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-// The four direction bits of one column, w[r] += (1 << BIT) if the row
-// above beats row r.  One asm block with four predicates: ptxas otherwise
-// funnels the four compares through a single predicate register
-// (FSETP -> @P IMAD -> FSETP ...), a serial chain behind the shuffle.  The
-// three bits that do not need `up` are compared first.
+// The four direction bits of one column.  Each bit is a 0.0 / 1.0 compare
+// (FSET, ALU pipe) folded into a float accumulator with one FFMA (FMA
+// pipe): wf[r] += (row above beats row r) * 2^BIT.  The accumulators start
+// at 2^23, so the 16 bits of a quad sit in the low mantissa bits
+// (__float_as_uint(wf) & 0xffff).  No predicate registers are involved: a
+// predicated form (FSETP -> @P IMAD) lets ptxas funnel the four compares
+// through a single predicate whenever other predicates are live, which
+// serialises the column behind FSETP->IMAD latencies.
 template <int BIT>
-__device__ __forceinline__ void bits4(uint32_t (&w)[R4], float up, const float (&o)[R4],
-                                      uint32_t one) {
-  asm("{\n\t.reg .pred p0, p1, p2, p3;\n\t"
-      "setp.gt.f32 p1, %5, %6;\n\t"
-      "setp.gt.f32 p2, %6, %7;\n\t"
-      "setp.gt.f32 p3, %7, %8;\n\t"
-      "setp.gt.f32 p0, %4, %5;\n\t"
-      "@p1 mad.lo.u32 %1, %9, %10, %1;\n\t"
-      "@p2 mad.lo.u32 %2, %9, %10, %2;\n\t"
-      "@p3 mad.lo.u32 %3, %9, %10, %3;\n\t"
-      "@p0 mad.lo.u32 %0, %9, %10, %0;\n\t}"
-      : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3])
-      : "f"(up), "f"(o[0]), "f"(o[1]), "f"(o[2]), "f"(o[3]), "r"(one), "n"(1u << BIT));
+__device__ __forceinline__ void bit1(float& wf, float a, float b) {
+  constexpr float kBit = static_cast<float>(1u << BIT);
+  asm("{\n\t.reg .f32 t;\n\tset.gt.f32.f32 t, %1, %2;\n\tfma.rn.f32 %0, t, %3, %0;\n\t}"
+      : "+f"(wf)
+      : "f"(a), "f"(b), "f"(kBit));
 }
+template <int R, int BIT>
+__device__ __forceinline__ void bits4(float (&wf)[R], float up, const float (&o)[R]) {
+  // the bits that do not need `up` (the shuffled row above) first
+#pragma unroll
+  for (int r = 1; r < R; ++r) bit1<BIT>(wf[r], o[r - 1], o[r]);
+  bit1<BIT>(wf[0], up, o[0]);
+}
+constexpr float kBitsBase = 8388608.0f;  // 2^23
 
 // Four columns (one LDS.128 per row residue, one of the FIFO slot) of the
 // DP for one warp.  U0 = index of the first column within the stage.
-template <int MODE, bool GENERIC, int U0>
+template <int R, int MODE, bool GENERIC, int U0>
 __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uint32_t coff,
                                           const float4* __restrict__ slot, float (&ex)[kQuad],
-                                          Lane4& L, uint32_t (&w)[R4], bool is31, int srclane,
+                                          Lane4<R>& L, float (&wf)[R], bool is31, int srclane,
                                           int c_base, int nvalid, int row0, float mnv,
-                                          bool row0_is_zero, uint32_t one) {
+                                          bool row0_is_zero) {
   if (GENERIC && U0 >= nvalid) return false;
-  float4 qv[R4];
+  float4 qv[R];
 #ifndef MAS_ABL_NOQLDS
 #pragma unroll
-  for (int r = 0; r < R4; ++r)
+  for (int r = 0; r < R; ++r)
     qv[r] = *reinterpret_cast<const float4*>(tile + r * 4096 + coff);
 #else
 #pragma unroll
-  for (int r = 0; r < R4; ++r) qv[r] = make_float4(mnv * 1e-36f, 1.f, 2.f, 3.f);
+  for (int r = 0; r < R; ++r) qv[r] = make_float4(mnv * 1e-36f, 1.f, 2.f, 3.f);
 #endif
   const float4 vv = slot[(U0 % kQuad) / 4];  // producer's bottom row
   const float bnds[4] = {L.vlast, vv.x, vv.y, vv.z};
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     if (GENERIC && U0 + e >= nvalid) return false;
-    float q[R4];
+    float q[R];
 #pragma unroll
-    for (int r = 0; r < R4; ++r) q[r] = e == 0 ? qv[r].x : e == 1 ? qv[r].y : e == 2 ? qv[r].z : qv[r].w;
-    const float send = is31 ? bnds[e] : L.o[R4 - 1];
+    for (int r = 0; r < R; ++r) q[r] = e == 0 ? qv[r].x : e == 1 ? qv[r].y : e == 2 ? qv[r].z : qv[r].w;
+    const float send = is31 ? bnds[e] : L.o[R - 1];
 #ifndef MAS_ABL_NOSHFL
     const float up = __shfl_sync(0xffffffffu, send, srclane);
 #else
     const float up = send;
 #endif
-    constexpr int bitpos = 31 - (U0 + 0);  // adjusted per e below
 #ifndef MAS_ABL_NOBITS
-    switch (U0 + e) {  // compile-time bit position 31 - column-in-word
-#define MAS_B4(U)                       \
-  case U:                               \
-    bits4<31 - U>(w, up, L.o, one);     \
+    switch ((U0 + e) % kQuad) {  // compile-time bit 15 - column-in-quad
+#define MAS_B4(U)                   \
+  case U:                           \
+    bits4<R, 15 - U>(wf, up, L.o);  \
     break;
       MAS_B4(0) MAS_B4(1) MAS_B4(2) MAS_B4(3) MAS_B4(4) MAS_B4(5) MAS_B4(6) MAS_B4(7)
       MAS_B4(8) MAS_B4(9) MAS_B4(10) MAS_B4(11) MAS_B4(12) MAS_B4(13) MAS_B4(14) MAS_B4(15)
-      MAS_B4(16) MAS_B4(17) MAS_B4(18) MAS_B4(19) MAS_B4(20) MAS_B4(21) MAS_B4(22) MAS_B4(23)
-      MAS_B4(24) MAS_B4(25) MAS_B4(26) MAS_B4(27) MAS_B4(28) MAS_B4(29) MAS_B4(30) MAS_B4(31)
 #undef MAS_B4
     }
 #endif
-    (void)bitpos;
-    float n[R4];
+    float n[R];
     n[0] = q[0] + fmaxf(up, L.o[0]);
 #pragma unroll
-    for (int r = 1; r < R4; ++r) n[r] = q[r] + fmaxf(L.o[r - 1], L.o[r]);
+    for (int r = 1; r < R; ++r) n[r] = q[r] + fmaxf(L.o[r - 1], L.o[r]);
     if (GENERIC) {
       const int c = c_base + U0 + e;
       if (MODE == 1) {
 #pragma unroll
-        for (int r = 0; r < R4; ++r)
+        for (int r = 0; r < R; ++r)
           if (c < row0 + r) n[r] = mnv;
       }
       if (c == 0) {  // first column: parallel.cpp:73-75 / reference.cpp:16-24
         n[0] = row0_is_zero ? q[0] : mnv;
 #pragma unroll
-        for (int r = 1; r < R4; ++r) n[r] = mnv;
+        for (int r = 1; r < R; ++r) n[r] = mnv;
       }
     }
 #ifndef MAS_ABL_NOFOLD
-    fold_abs_max_nan(L.acc, q[0], q[1]);
-    fold_abs_max_nan(L.acc, q[2], q[3]);
-#endif
-    ex[(U0 % kQuad) + e] = n[R4 - 1];
 #pragma unroll
-    for (int r = 0; r < R4; ++r) L.o[r] = n[r];
+    for (int r = 0; r + 1 < R; r += 2) fold_abs_max_nan(L.acc, q[r], q[r + 1]);
+#endif
+    ex[(U0 % kQuad) + e] = n[R - 1];
+#pragma unroll
+    for (int r = 0; r < R; ++r) L.o[r] = n[r];
   }
   L.vlast = vv.w;
   return true;
@@ -184,47 +189,56 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
 struct Probes {
   uint32_t stage_bar, stage_par;  // next stage's "loaded" barrier
   uint32_t empty_bar, empty_par;  // next iteration's consumer-slot barrier
-  bool arm_empty;                 // lane 31: arm empty_bar (expect_tx) first
+  bool arm_empty;                 // arm empty_bar (expect_tx, lane 31) first
   bool stage_ok, empty_ok;        // results
 };
 
-template <int MODE, bool GENERIC, int K>
+template <int R, int MODE, bool GENERIC, int K>
 __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (&coff)[8],
-                                         const Fifo4& F, float (&ex)[kQuad], Lane4& L,
-                                         uint32_t (&w)[R4], bool& ready, bool more, bool is31,
+                                         const Fifo4& F, float (&ex)[kQuad], Lane4<R>& L,
+                                         uint32_t (&w)[R], bool& ready, bool more, bool is31,
                                          int lane, int srclane, int q, int c_base, int nvalid,
-                                         int row0, float mnv, bool row0_is_zero, uint32_t one,
+                                         int row0, float mnv, bool row0_is_zero,
                                          Probes& P) {
   if (GENERIC && K * kQuad >= nvalid) return false;
   const int fs = q & (kFifoSlots - 1);
 #ifndef MAS_ABL_NOFIFO
-  if (F.has_in && !ready) mbar_wait(F.full + 8u * fs, static_cast<uint32_t>(q / kFifoSlots) & 1u);
+  if (F.has_in && !ready) mbar_wait_all(F.full + 8u * fs, static_cast<uint32_t>(q / kFifoSlots) & 1u);
 #endif
   const bool next = K + 1 < kQuadsPerStage ? (!GENERIC || (K + 1) * kQuad < nvalid) : more;
   const int q1 = q + 1;
   const uint32_t bar1 = F.full + 8u * (q1 & (kFifoSlots - 1));
 #ifndef MAS_ABL_NOFIFO
   if (lane == 0 && next && F.has_in) mbar_arrive_expect_tx(bar1, kSlot4);
-  const bool probe = mbar_test_wait(bar1, static_cast<uint32_t>(q1 / kFifoSlots) & 1u);
+  const bool probe = mbar_test_wait_all(bar1, static_cast<uint32_t>(q1 / kFifoSlots) & 1u);
 #else
   const bool probe = true;
   (void)bar1;
 #endif
   bool p_stage = false, p_empty = false;
   if (K == 0) {
-    if (P.arm_empty) mbar_arrive_expect_tx(P.empty_bar, 4u);
-    p_stage = mbar_test_wait(P.stage_bar, P.stage_par);
-    p_empty = mbar_test_wait(P.empty_bar, P.empty_par);
+    if (P.arm_empty && is31) mbar_arrive_expect_tx(P.empty_bar, 4u);
+    p_stage = mbar_test_wait_all(P.stage_bar, P.stage_par);
+    p_empty = mbar_test_wait_all(P.empty_bar, P.empty_par);
   }
   const float4* slot = reinterpret_cast<const float4*>(F.buf + fs * kSlot4);
   bool ok = true;
+  float wf[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) wf[r] = kBitsBase;
 #define MAS_G4(A)                                                                              \
   if (ok)                                                                                      \
-    ok = fwd4_group<MODE, GENERIC, K * kQuad + 4 * A>(stage, coff[(K * kQuad / 4 + A) & 7],   \
-                                                      slot, ex, L, w, is31, srclane, c_base, \
-                                                      nvalid, row0, mnv, row0_is_zero, one);
+    ok = fwd4_group<R, MODE, GENERIC, K * kQuad + 4 * A>(stage, coff[(K * kQuad / 4 + A) & 7], \
+                                                      slot, ex, L, wf, is31, srclane, c_base, \
+                                                      nvalid, row0, mnv, row0_is_zero);
   MAS_G4(0) MAS_G4(1) MAS_G4(2) MAS_G4(3)
 #undef MAS_G4
+  // quad 0 holds word bits 31..16 (columns 0..15), quad 1 bits 15..0
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t v = __float_as_uint(wf[r]) & 0xffffu;
+    w[r] |= K == 0 ? v << 16 : v;
+  }
   ready = probe;
   if (K == 0) {
     P.stage_ok = p_stage;
@@ -241,7 +255,11 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
     for (int q4 = 0; q4 < kQuad / 4; ++q4)
       st_async_v4(dst + 16u * q4, ex[4 * q4], ex[4 * q4 + 1], ex[4 * q4 + 2], ex[4 * q4 + 3], fbar);
   }
+#ifndef MAS_ABL_NOBND
   if (F.bnd_out != nullptr && is31) {
+#else
+  if (false) {
+#endif
     // last warp of a band: its bottom row feeds the next band's first warp
     float4* dst = reinterpret_cast<float4*>(F.bnd_out + q * kQuad);
 #pragma unroll
@@ -251,18 +269,18 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
   return ok;
 }
 
-template <int MODE, bool GENERIC>
+template <int R, int MODE, bool GENERIC>
 __device__ __forceinline__ void fwd4_stage(const uint8_t* stage, const uint32_t (&coff)[8],
-                                          const Fifo4& F, float (&ex)[kQuad], Lane4& L,
-                                          uint32_t (&w)[R4], bool& ready, bool more, bool is31,
+                                          const Fifo4& F, float (&ex)[kQuad], Lane4<R>& L,
+                                          uint32_t (&w)[R], bool& ready, bool more, bool is31,
                                           int lane, int srclane, int q0, int c_base, int nvalid,
-                                          int row0, float mnv, bool row0_is_zero, uint32_t one,
+                                          int row0, float mnv, bool row0_is_zero,
                                           Probes& P) {
-  if (!fwd4_quad<MODE, GENERIC, 0>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane, q0,
-                                   c_base, nvalid, row0, mnv, row0_is_zero, one, P))
+  if (!fwd4_quad<R, MODE, GENERIC, 0>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane, q0,
+                                   c_base, nvalid, row0, mnv, row0_is_zero, P))
     return;
-  fwd4_quad<MODE, GENERIC, 1>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane, q0 + 1,
-                              c_base, nvalid, row0, mnv, row0_is_zero, one, P);
+  fwd4_quad<R, MODE, GENERIC, 1>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane, q0 + 1,
+                              c_base, nvalid, row0, mnv, row0_is_zero, P);
 }
 
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
@@ -281,7 +299,7 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
                : "memory");
 }
 
-template <int MODE>
+template <int R, int MODE>
 __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     mas_fwd4_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tm_out,
                     const FwdArgs a) {
@@ -291,7 +309,9 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   uint8_t* const sbase = smem_raw + (base - raw);
   const int W = a.W;  // compute warps; warp W is the CTA's TMA producer
   const int N = a.N;
-  const Smem4 SL = smem4_layout(W, N);
+  constexpr int kRows4 = rows_of(R);
+  constexpr int kStage4 = stage_bytes(R);
+  const Smem4 SL = smem4_layout(R, W, N);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -355,7 +375,11 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     // ring's lead.
     const int w = lane;
     const int i0w = band + (crank * W + w) * kRows4;
+#ifndef MAS_ABL_NOFEED
     if (w == W && fed && crank == 0 && s_b > 0 && band < t_b) {
+#else
+    if (false) {
+#endif
       // Band feeder: the band's first warp (warp 0 of rank 0) gets the row
       // above the band, written by the previous band's last warp, through
       // its ordinary FIFO: 64-byte bulk copies completing its "full"
@@ -381,12 +405,12 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
         }
       }
     }
-    if (w < W && s_b > 0 && i0w < t_b) {
+    if (w < W && s_b > 0 && i0w < t_b && !a.self_tma) {
       prefetch_tensormap(&tmq);
       const uint64_t pol_q = policy_evict_first();
       const bool zero_fill = a.zero_fill != 0;
       const uint32_t zero_tile = base + SL.zero;
-      const int group = (b * a.T_pad + i0w) / R4;
+      const int group = (b * a.T_pad + i0w) / R;
       const int orow = b * a.T_cap + i0w;
       const int l2a = a.l2_ahead;
       for (int m = 0; m < l2a && m < nit; ++m) tma_prefetch_3d(&tmq, m * kCols4, group, 0);
@@ -454,6 +478,26 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
                     : nullptr;
 
     const uint8_t* ring_ptr = sbase + SL.ring + warp * N * kStage4;
+    // Self-issued stage loads (a.self_tma): lane 0 refills a stage as soon as
+    // the warp has consumed it, so no producer warp spins on this SM
+    // sub-partition.  The output's zero tiles ride along as before.
+    const bool self_tma = a.self_tma != 0;
+    const bool zero_fill = a.zero_fill != 0;
+    const int tma_group = (b * a.T_pad + i0) / R;
+    const int tma_orow = b * a.T_cap + i0;
+    const uint64_t pol_q = policy_evict_first();
+    auto issue_stage = [&](int mm) {
+      const int st = mm % N;
+      const uint32_t bar = bar0 + 8u * static_cast<uint32_t>(st);
+      mbar_arrive_expect_tx(bar, kStage4);
+      tma_load_3d(base + SL.ring + static_cast<uint32_t>((warp * N + st) * kStage4), &tmq,
+                  mm * kCols4, tma_group, 0, bar, pol_q);
+      if (zero_fill) tma_store_2d(&tm_out, base + SL.zero, mm * kCols4, tma_orow);
+    };
+    if (self_tma && lane == 0) {
+      prefetch_tensormap(&tmq);
+      for (int mm = 0; mm < N && mm < nit; ++mm) issue_stage(mm);
+    }
     uint32_t coff[8];
 #pragma unroll
     for (int a4 = 0; a4 < 8; ++a4) coff[a4] = lane * 128u + ((a4 ^ (lane & 7)) << 4);
@@ -461,19 +505,18 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
 
     const bool is31 = lane == 31;
     const int srclane = (lane + 31) & 31;
-    const int row0 = i0 + R4 * lane;
+    const int row0 = i0 + R * lane;
     const bool row0_is_zero = row0 == 0;
     const float mnv = a.mnv;
-    const uint32_t one = a.one;
-    Lane4 L;
+    Lane4<R> L;
 #pragma unroll
-    for (int r = 0; r < R4; ++r) L.o[r] = 0.0f;
+    for (int r = 0; r < R; ++r) L.o[r] = 0.0f;
     L.acc = 0.0f;
     L.vlast = a.row0_up;
     float ex[kQuad];
 #pragma unroll
     for (int u = 0; u < kQuad; ++u) ex[u] = 0.0f;
-    uint32_t* dirs_ptr = a.dirs + static_cast<size_t>(b) * a.M * a.T_alloc + i0 + R4 * lane;
+    uint32_t* dirs_ptr = a.dirs + static_cast<size_t>(b) * a.M * a.T_alloc + i0 + R * lane;
 
     bool ready = false;  // FIFO quad look-ahead
     if (has_in && lane == 0) mbar_arrive_expect_tx(my_full, kSlot4);
@@ -490,7 +533,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
 #ifdef MAS_FWD_PROFILE
       long long pf_a = clock64();
 #endif
-      if (!stage_ready) mbar_wait(bar0 + 8u * slot, par);
+      if (!stage_ready) mbar_wait_all(bar0 + 8u * slot, par);
 #ifdef MAS_FWD_PROFILE
       long long pf_b = clock64();
       pf_stage += pf_b - pf_a;
@@ -498,13 +541,15 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       const uint8_t* stage = ring_ptr + slot * kStage4;
       const int c_base = m * kCols4;
       const int nvalid = s_b - c_base < kCols4 ? s_b - c_base : kCols4;
-      uint32_t w[R4] = {0u, 0u, 0u, 0u};
+      uint32_t w[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) w[r] = 0u;
       const bool generic =
           m == 0 || nvalid < kCols4 || (MODE == 1 && c_base < i0 + kRows4 - 1);
-      if (has_out && is31 && m >= kFifoIt4 && !empty_ready) {
+      if (has_out && m >= kFifoIt4 && !empty_ready) {
         // This iteration's slots in the consumer are free once it released
         // iteration m - kFifoIt4 (4-byte st.async on empty[m % kFifoIt4]).
-        mbar_wait(my_empty + 8u * static_cast<uint32_t>(m % kFifoIt4),
+        mbar_wait_all(my_empty + 8u * static_cast<uint32_t>(m % kFifoIt4),
                   (static_cast<uint32_t>(m / kFifoIt4) & 1u) ^ 1u);
       }
       const bool more = m + 1 < nit;
@@ -516,7 +561,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
         const int m1 = m + 1;
         P.empty_bar = my_empty + 8u * static_cast<uint32_t>(m1 % kFifoIt4);
         P.empty_par = (static_cast<uint32_t>(m1 / kFifoIt4) & 1u) ^ 1u;
-        P.arm_empty = has_out && is31 && m1 >= kFifoIt4 && more;
+        P.arm_empty = has_out && m1 >= kFifoIt4 && more;  // lane 31 arms
         P.stage_ok = false;
         P.empty_ok = false;
       }
@@ -525,12 +570,12 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       pf_empty += pf_c - pf_b;
 #endif
       if (generic) {
-        fwd4_stage<MODE, true>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
-                               kQuadsPerStage * m, c_base, nvalid, row0, mnv, row0_is_zero, one,
+        fwd4_stage<R, MODE, true>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
+                               kQuadsPerStage * m, c_base, nvalid, row0, mnv, row0_is_zero,
                                P);
       } else {
-        fwd4_stage<MODE, false>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
-                                kQuadsPerStage * m, c_base, kCols4, row0, mnv, row0_is_zero, one,
+        fwd4_stage<R, MODE, false>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
+                                kQuadsPerStage * m, c_base, kCols4, row0, mnv, row0_is_zero,
                                 P);
       }
       stage_ready = P.stage_ok;
@@ -544,7 +589,12 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       // slots to the warp above.
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive_local(ebar0 + 8u * slot);
+        if (!self_tma) {
+          mbar_arrive_local(ebar0 + 8u * slot);
+        } else if (m + N < nit) {
+          fence_proxy_async_smem();  // this warp's reads of the slot before the TMA rewrite
+          issue_stage(m + N);
+        }
         if (has_in)
           st_async_b32(F.prev_sink, static_cast<uint32_t>(m),
                        F.prev_empty + 8u * static_cast<uint32_t>(m % kFifoIt4));
@@ -553,12 +603,15 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       // steps above row 0 or left of column 0).
       if (m == 0) {
 #pragma unroll
-        for (int r = 0; r < R4; ++r) w[r] &= 0x7fffffffu;
+        for (int r = 0; r < R; ++r) w[r] &= 0x7fffffffu;
       }
       if (row0_is_zero) w[0] = 0u;
-      asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dirs_ptr),
-                   "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "l"(pol_dir)
-                   : "memory");
+      if constexpr (R == 4)
+        asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dirs_ptr),
+                     "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "l"(pol_dir)
+                     : "memory");
+      else
+        st_global_v2_evict_last(dirs_ptr, w[0], w[1], pol_dir);
       dirs_ptr += a.T_alloc;
       slot = slot + 1 == N ? 0 : slot + 1;
       par ^= slot == 0 ? 1u : 0u;
@@ -571,10 +624,11 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       printf("fwd4 warp g=%d: total %lld, stage-wait %lld, empty-wait %lld, compute %lld (%.1f/col), rest %lld, nit %d\n",
              g, clock64() - pf_t0, pf_stage, pf_empty, pf_comp, (double)pf_comp / s_b, pf_rest, nit);
 #endif
+    if (self_tma && zero_fill && lane == 0) bulk_store_drain();
     __syncwarp();
     bool bad = false;
 #pragma unroll
-    for (int r = 0; r < R4; ++r) bad |= row0 + r < t_b;
+    for (int r = 0; r < R; ++r) bad |= row0 + r < t_b;
     bad = bad && !(L.acc < INFINITY);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flags + b, 1);
   }
@@ -592,7 +646,18 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
 
 }  // namespace
 
-size_t fwd4_smem_bytes(int W, int N) { return smem4_layout(W, N).total + 1024u; }
+size_t fwd4_smem_bytes(int R, int W, int N) { return smem4_layout(R, W, N).total + 1024u; }
+
+namespace {
+template <int R, int MODE>
+const void* fwd4_fn() {
+  return reinterpret_cast<const void*>(&mas_fwd4_kernel<R, MODE>);
+}
+const void* fwd4_fn(int R, int mode) {
+  if (R == 2) return mode == 0 ? fwd4_fn<2, 0>() : fwd4_fn<2, 1>();
+  return mode == 0 ? fwd4_fn<4, 0>() : fwd4_fn<4, 1>();
+}
+}  // namespace
 
 cudaError_t fwd4_configure() {
   constexpr int kMaxDevices = 64;
@@ -605,9 +670,8 @@ cudaError_t fwd4_configure() {
   std::call_once(once[dev], [dev] {
     int smem_max = 0;
     cudaError_t r = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    for (int mode = 0; mode < 2 && r == cudaSuccess; ++mode) {
-      const void* fn = mode == 0 ? reinterpret_cast<const void*>(&mas_fwd4_kernel<0>)
-                                 : reinterpret_cast<const void*>(&mas_fwd4_kernel<1>);
+    for (int v = 0; v < 4 && r == cudaSuccess; ++v) {
+      const void* fn = fwd4_fn(v < 2 ? 4 : 2, v & 1);
       r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
       if (r == cudaSuccess)
         r = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -617,11 +681,11 @@ cudaError_t fwd4_configure() {
   return status[dev];
 }
 
-int fwd4_max_active_clusters(int W, int N, int K) {
+int fwd4_max_active_clusters(int R, int W, int N, int K) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(K), 1, 1);
   cfg.blockDim = dim3(static_cast<unsigned>((W + 1) * 32), 1, 1);
-  cfg.dynamicSmemBytes = fwd4_smem_bytes(W, N);
+  cfg.dynamicSmemBytes = fwd4_smem_bytes(R, W, N);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(K);
@@ -630,20 +694,19 @@ int fwd4_max_active_clusters(int W, int N, int K) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(&mas_fwd4_kernel<0>), &cfg) !=
-      cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, fwd4_fn(R, 0), &cfg) != cudaSuccess) {
     cudaGetLastError();
     return -1;
   }
   return n;
 }
 
-cudaError_t launch_fwd4(int mode, const CUtensorMap& tmq, const CUtensorMap& tm_out,
+cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorMap& tm_out,
                         const FwdArgs& a, int B, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(B * a.K), 1, 1);
   cfg.blockDim = dim3(static_cast<unsigned>((a.W + 1) * 32), 1, 1);  // + the TMA producer warp
-  cfg.dynamicSmemBytes = fwd4_smem_bytes(a.W, a.N);
+  cfg.dynamicSmemBytes = fwd4_smem_bytes(R, a.W, a.N);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -652,8 +715,11 @@ cudaError_t launch_fwd4(int mode, const CUtensorMap& tmq, const CUtensorMap& tm_
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (mode == 0) return cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<0>, tmq, tm_out, a);
-  return cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<1>, tmq, tm_out, a);
+  if (R == 2)
+    return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<2, 0>, tmq, tm_out, a)
+                     : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<2, 1>, tmq, tm_out, a);
+  return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0>, tmq, tm_out, a)
+                   : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 1>, tmq, tm_out, a);
 }
 
 }  // namespace mas

@@ -39,6 +39,8 @@ struct FwdArgs {
   int zero_fill;            // 1: TMA-store zero tiles of the output (tm_out) as we go
   int T_cap, S_cap;         // output shape
   int l2_ahead;             // mas_fwd4: stages prefetched into L2 beyond the smem ring
+  int self_tma;             // mas_fwd4: each compute warp issues its own stage loads
+                            //   (no TMA producer warp competing for its SM sub-partition)
   // mas_fwd4 banded mode (text longer than one cluster's rows): this launch
   // computes rows [row_base, row_base + K*W*128); the row above row_base
   // comes from bnd_in, this band's bottom row goes to bnd_out (both
@@ -57,6 +59,7 @@ struct BtArgs {
   const uint32_t* dirs;     // [B][M][T_alloc]
   int32_t* path;            // [B][S_cap] int32 path rows, -1 past s_b, or null
   uint8_t* out;             // [B][T_cap][S_cap] (already zero-filled) or null
+  int32_t* dur;             // [B][T_cap] int32 durations (row sums of the alignment) or null
   int B, T_cap, S_cap, M, T_alloc;
   int R;                    // rows per backtrack window (<= 256, <= T_alloc)
 };
@@ -70,11 +73,11 @@ cudaError_t launch_locate_nonfinite(const float* q, int64_t row_pitch, int T_pad
 cudaError_t launch_generate(uint64_t s0, int64_t first_elem, int B, int T, int S, int64_t pitch,
                             float* out, cudaStream_t stream);
 cudaError_t fwd_configure(int W, int N, int K);
-// mas_fwd4.cu: four rows per lane, 128 rows per warp, 32-column stages.
-size_t fwd4_smem_bytes(int W, int N);
+// mas_fwd4.cu: R (4 or 2) rows per lane, 32 R rows per warp, 32-column stages.
+size_t fwd4_smem_bytes(int R, int W, int N);
 cudaError_t fwd4_configure();
-int fwd4_max_active_clusters(int W, int N, int K);
-cudaError_t launch_fwd4(int mode, const CUtensorMap& tmq, const CUtensorMap& tm_out,
+int fwd4_max_active_clusters(int R, int W, int N, int K);
+cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorMap& tm_out,
                         const FwdArgs& a, int B, cudaStream_t stream);
 int fwd_max_active_clusters(int W, int N, int K, int mode);
 

@@ -50,6 +50,27 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Warp-uniform variants for warps that shuffle right after: every lane
+// leaves with the same answer, so the warp stays converged (a lane that
+// left a spin loop alone would push every later SHFL onto the divergent
+// WARPSYNC path).
+#ifndef MAS_NO_VOTE
+__device__ __forceinline__ bool mbar_test_wait_all(uint32_t bar, uint32_t parity) {
+  return __all_sync(0xffffffffu, mbar_test_wait(bar, parity));
+}
+__device__ __forceinline__ void mbar_wait_all(uint32_t bar, uint32_t parity) {
+  while (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
+  }
+}
+#else
+__device__ __forceinline__ bool mbar_test_wait_all(uint32_t bar, uint32_t parity) {
+  return mbar_test_wait(bar, parity);
+}
+__device__ __forceinline__ void mbar_wait_all(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+#endif
 
 // ---- TMA ------------------------------------------------------------------
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -401,3 +401,80 @@ def test_text_longer_than_a_cluster(mas, oracle, cuda):
     got = mas.align_paths(q)
     exp = oracle.align(q)[4]
     np.testing.assert_array_equal(got[0], exp[0])
+
+
+# ---- durations: row sums of the alignment ---------
+def _durations_of(out, lens=None):
+    d = out.sum(axis=-1, dtype=np.int64).astype(np.int32)
+    return d
+
+
+def test_durations_match_alignment_row_sums(mas, oracle, cuda):
+    rng = np.random.default_rng(77)
+    for it in range(30):
+        B = int(rng.integers(1, 6))
+        T = int(rng.integers(1, 300))
+        S = int(rng.integers(T, 1400))
+        q = rng.uniform(-5, 5, (B, T, S)).astype(np.float32)
+        lt = rng.integers(1, T + 1, B)
+        ls = np.array([int(rng.integers(a, S + 1)) for a in lt])
+        lens = np.stack([lt, ls], 1) if it % 3 else None
+        for eng in ("parallel", "reference"):
+            exp = oracle.align(q, lens, engine=eng)[3]
+            got = mas.align_durations(q, lengths=lens, engine=eng)
+            assert got.dtype == np.int32 and got.shape == (B, T)
+            np.testing.assert_array_equal(got, _durations_of(exp), err_msg=f"{it} {eng}")
+            if lens is not None:
+                assert np.all(got.sum(axis=1) == ls)
+                for b in range(B):
+                    assert np.all(got[b, lt[b]:] == 0)
+
+
+def test_durations_golden_and_2d(mas, oracle, cuda):
+    for tag in ("c1", "c2"):
+        q, lengths = inputs(tag, _gen(oracle))
+        exp_paths, _ = expected(tag, "parallel", "m1e32")
+        T, S = q.shape[-2:]
+        exp_out = paths_to_out(exp_paths, T, S)
+        got = mas.align_durations(q, lengths=lengths)
+        got = got[None] if got.ndim == 1 else got
+        np.testing.assert_array_equal(got, _durations_of(exp_out))
+    q = np.random.default_rng(4).uniform(-5, 5, (70, 333)).astype(np.float32)
+    d = mas.align_durations(q)
+    assert d.shape == (70,) and int(d.sum()) == 333
+    np.testing.assert_array_equal(d, _durations_of(oracle.align(q[None])[3])[0])
+
+
+def test_durations_device_plan_and_errors(mas, oracle, cuda):
+    import torch
+
+    B, T, S = 3, 257, 1031
+    q = mas.generate_device(B, T, S, 5)
+    exp = _durations_of(oracle.align(oracle.generate(B, T, S, 5))[3])
+    d = mas.align_durations(q)
+    assert d.is_cuda and d.dtype == torch.int32
+    np.testing.assert_array_equal(d.cpu().numpy(), exp)
+    # plan (aligned layout: T % 4 == 0, pitch % 4 == 0): durations only (no
+    # dense output), then with the dense output
+    T = 256
+    q = mas.generate_device(B, T, S, 5, row_pitch=1032)
+    exp = _durations_of(oracle.align(oracle.generate(B, T, S, 5))[3])
+    plan = mas.Plan(B, T, S, row_pitch=1032)
+    dur = torch.full((B, T), -5, dtype=torch.int32, device=cuda)
+    plan.enqueue(q, durations=dur)
+    plan.finish(q)
+    np.testing.assert_array_equal(dur.cpu().numpy(), exp)
+    out = torch.empty((B, T, S), dtype=torch.uint8, device=cuda)
+    dur.fill_(-1)
+    plan.enqueue(q, out=out, durations=dur)
+    plan.finish(q)
+    np.testing.assert_array_equal(dur.cpu().numpy(), exp)
+    np.testing.assert_array_equal(out.sum(dim=2, dtype=torch.int32).cpu().numpy(), exp)
+    plan.close()
+    # the same errors as align
+    bad = oracle.generate(2, 20, 50, 1)
+    bad[1, 3, 7] = np.inf
+    with pytest.raises(ValueError, match=r"item 1: non-finite likelihood at \(3, 7\)"):
+        mas.align_durations(bad)
+    with pytest.raises(ValueError):
+        mas.align_durations(bad[:, :, :10], lengths=[[20, 10], [20, 10]])
