@@ -284,6 +284,45 @@ def run_ours(args):
     h2d = B * T * S * 4
     d2h = B * T * S + 4 * B  # alignment bytes + NonFinite flags
 
+    # ---- secondary: durations only, no dense output
+    dur = torch.empty((B, T), dtype=torch.int32, device=dev)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            plan.enqueue(q, stream=stream, durations=dur)
+    torch.cuda.synchronize(dev)
+    d0 = torch.cuda.Event(enable_timing=True)
+    d1 = torch.cuda.Event(enable_timing=True)
+    d0.record(stream)
+    for _ in range(K):
+        plan.enqueue(q, stream=stream, durations=dur)
+    d1.record(stream)
+    torch.cuda.synchronize(dev)
+    dur_ms = d0.elapsed_time(d1) / K
+    assert torch.equal(dur, out.sum(dim=2, dtype=torch.int32)), "durations != alignment row sums"
+    hdur = torch.empty((B, T), dtype=torch.int32, pin_memory=True)
+
+    def host_dur_call():
+        rc = lib.mas_align_host_ex(hq.data_ptr(), B, T, S, None, ctypes.byref(cfg), None, None,
+                                   hdur.data_ptr(), ctypes.byref(err))
+        _lib.raise_for(rc, err)
+
+    host_dur_call()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        host_dur_call()
+    e2e_dur_s = time.perf_counter() - t0
+    durations_line = {
+        "value": round(world * cells / (dur_ms / 1e3) / 1e9, 2), "unit": "Gcells/s",
+        "ms_per_step": round(dur_ms, 4), "bytes_per_cell": 4.125,
+        "frac": None,  # filled below once the peak is known
+        "e2e": {"value": round(world * cells * e2e_steps / e2e_dur_s / 1e9, 3),
+                "unit": "Gcells/s", "h2d_bytes_per_step": B * T * S * 4,
+                "d2h_bytes_per_step": B * T * 4 + 4 * B,
+                "path": "mas_align_host_ex (C-ABI), pinned host in, durations out"},
+        "path": "plan.enqueue(durations=...): K1 without the zero fill + K2 writing [B,T] int32",
+    }
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -304,6 +343,8 @@ def run_ours(args):
     achieved = BYTES_PER_CELL * cells / (fwd_avg / 1e3) / 1e9
     traffic = _ncu_traffic()
     step_ms = elapsed_ms / K
+    durations_line["frac"] = round(4.125 * cells / (durations_line["ms_per_step"] / 1e3) / 1e9
+                                   / peak, 4)
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "Gcells/s", "n_gpus": world,
         "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": round(step_ms, 4),
@@ -324,6 +365,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "path": "mas_align_host (C-ABI), pinned host in/out, H2D+kernels+D2H+checks"},
         "gpu_launches": K * launches_per_step,
+        "variants": {"durations_only": durations_line},
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
     }

@@ -41,8 +41,11 @@ namespace {
 constexpr int kCols4 = 32;  // columns per stage / direction word
 __host__ __device__ constexpr int rows_of(int R) { return 32 * R; }
 __host__ __device__ constexpr int stage_bytes(int R) { return rows_of(R) * kCols4 * 4; }
-constexpr int kQuad = kQuadCols;            // 16 columns per FIFO hand-off
-constexpr int kSlot4 = kQuad * 4;           // 64-byte FIFO slot
+#ifndef MAS_QUAD4
+#define MAS_QUAD4 32
+#endif
+constexpr int kQuad = MAS_QUAD4;            // columns per FIFO hand-off (16 or 32)
+constexpr int kSlot4 = kQuad * 4;           // FIFO slot bytes
 constexpr int kQuadsPerStage = kCols4 / kQuad;
 constexpr int kFifoIt4 = kFifoSlots / kQuadsPerStage;  // FIFO depth in stages
 
@@ -143,7 +146,7 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
     const float up = send;
 #endif
 #ifndef MAS_ABL_NOBITS
-    switch ((U0 + e) % kQuad) {  // compile-time bit 15 - column-in-quad
+    switch ((U0 + e) % 16) {  // compile-time bit 15 - column-in-half-word
 #define MAS_B4(U)                   \
   case U:                           \
     bits4<R, 15 - U>(wf, up, L.o);  \
@@ -210,7 +213,11 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
   const uint32_t bar1 = F.full + 8u * (q1 & (kFifoSlots - 1));
 #ifndef MAS_ABL_NOFIFO
   if (lane == 0 && next && F.has_in) mbar_arrive_expect_tx(bar1, kSlot4);
+#ifndef MAS_ABL_NOPROBE
   const bool probe = mbar_test_wait_all(bar1, static_cast<uint32_t>(q1 / kFifoSlots) & 1u);
+#else
+  const bool probe = false;
+#endif
 #else
   const bool probe = true;
   (void)bar1;
@@ -218,27 +225,34 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
   bool p_stage = false, p_empty = false;
   if (K == 0) {
     if (P.arm_empty && is31) mbar_arrive_expect_tx(P.empty_bar, 4u);
+#ifndef MAS_ABL_NOPROBE
     p_stage = mbar_test_wait_all(P.stage_bar, P.stage_par);
     p_empty = mbar_test_wait_all(P.empty_bar, P.empty_par);
+#endif
   }
   const float4* slot = reinterpret_cast<const float4*>(F.buf + fs * kSlot4);
   bool ok = true;
   float wf[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) wf[r] = kBitsBase;
-#define MAS_G4(A)                                                                              \
-  if (ok)                                                                                      \
-    ok = fwd4_group<R, MODE, GENERIC, K * kQuad + 4 * A>(stage, coff[(K * kQuad / 4 + A) & 7], \
-                                                      slot, ex, L, wf, is31, srclane, c_base, \
-                                                      nvalid, row0, mnv, row0_is_zero);
-  MAS_G4(0) MAS_G4(1) MAS_G4(2) MAS_G4(3)
-#undef MAS_G4
-  // quad 0 holds word bits 31..16 (columns 0..15), quad 1 bits 15..0
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const uint32_t v = __float_as_uint(wf[r]) & 0xffffu;
-    w[r] |= K == 0 ? v << 16 : v;
+  // Groups of four columns; the bits of each 16-column half-word collect in
+  // wf (columns 0..15 of the stage -> word bits 31..16, 16..31 -> 15..0).
+#define MAS_G4(A)                                                                               \
+  if constexpr (4 * (A) < kQuad) {                                                              \
+    constexpr int U0 = K * kQuad + 4 * (A);                                                     \
+    if constexpr (U0 % 16 == 0) {                                                               \
+      _Pragma("unroll") for (int r = 0; r < R; ++r) wf[r] = kBitsBase;                          \
+    }                                                                                           \
+    if (ok)                                                                                     \
+      ok = fwd4_group<R, MODE, GENERIC, U0>(stage, coff[(U0 / 4) & 7], slot, ex, L, wf, is31,   \
+                                            srclane, c_base, nvalid, row0, mnv, row0_is_zero);  \
+    if constexpr (U0 % 16 == 12) {                                                              \
+      _Pragma("unroll") for (int r = 0; r < R; ++r) {                                           \
+        const uint32_t v = __float_as_uint(wf[r]) & 0xffffu;                                    \
+        w[r] |= U0 < 16 ? v << 16 : v;                                                          \
+      }                                                                                         \
+    }                                                                                           \
   }
+  MAS_G4(0) MAS_G4(1) MAS_G4(2) MAS_G4(3) MAS_G4(4) MAS_G4(5) MAS_G4(6) MAS_G4(7)
+#undef MAS_G4
   ready = probe;
   if (K == 0) {
     P.stage_ok = p_stage;
@@ -279,8 +293,9 @@ __device__ __forceinline__ void fwd4_stage(const uint8_t* stage, const uint32_t 
   if (!fwd4_quad<R, MODE, GENERIC, 0>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane, q0,
                                    c_base, nvalid, row0, mnv, row0_is_zero, P))
     return;
-  fwd4_quad<R, MODE, GENERIC, 1>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane, q0 + 1,
-                              c_base, nvalid, row0, mnv, row0_is_zero, P);
+  if constexpr (kQuadsPerStage > 1)
+    fwd4_quad<R, MODE, GENERIC, 1>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
+                                   q0 + 1, c_base, nvalid, row0, mnv, row0_is_zero, P);
 }
 
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
