@@ -225,42 +225,52 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
   g->L = 256;
   g->Kseg = (S_cap + g->L - 1) / g->L;
   if (!g->legacy) {
-    // 32 R rows per warp; an item's warps form one cluster of K CTAs of W
-    // compute warps.  Candidates in order of preference (few warps per CTA
-    // spread an item over more SMs; more stages give the TMA ring more
-    // lead); the first that runs the whole batch in the fewest waves of
-    // co-resident clusters wins (cudaOccupancyMaxActiveClusters accounts
-    // for shared memory and the GPC placement of clusters).
-    // Texts longer than one cluster of 16 CTAs x 4 warps x 32 R rows run in
-    // bands of that height, one launch each (see mas_fwd4.cu, banded mode).
+    // 32 R rows per warp; an item's warps form `bands` clusters of K CTAs of
+    // W compute warps, all in one launch (mas_fwd4.cu, bands).  Candidates
+    // (W, stages) in order of preference (few warps per CTA spread an item
+    // over more SMs; more stages give the TMA ring more lead); for each, the
+    // fewest bands whose clusters all run in one wave of co-resident
+    // clusters (cudaOccupancyMaxActiveClusters accounts for shared memory
+    // and the GPC placement of clusters).  The first candidate reaching one
+    // wave wins, otherwise the fewest waves, then the fewest bands.
     static const int band_warps_cap = [] {
       const char* e = std::getenv("MAS_BAND_WARPS");  // test hook: force short bands
       return e ? std::max(1, std::min(4 * mas::kMaxClusterCtas, std::atoi(e)))
                : 4 * mas::kMaxClusterCtas;
     }();
     const int rows = 32 * g->R;
-    const int warps = std::min(std::max(1, (t_max + rows - 1) / rows), band_warps_cap);
+    const int warps_total = std::max(1, (t_max + rows - 1) / rows);
     static const int cand4[][2] = {{2, 4}, {4, 3}, {2, 3}, {1, 4}, {2, 2}, {4, 2}, {1, 2}};
     static const int cand2[][2] = {{4, 4}, {4, 3}, {2, 4}, {2, 3}, {4, 2}, {1, 4}, {1, 2}};
     const int(*cand)[2] = g->R == 4 ? cand4 : cand2;
     const int ncand = 7;
     int best = -1;
     int64_t best_waves = 0;
-    for (int c = 0; c < ncand; ++c) {
-      const int W = std::min(cand[c][0], warps), N = cand[c][1];
-      const int K = (warps + W - 1) / W;
-      if (K > mas::kMaxClusterCtas || mas::fwd4_smem_bytes(g->R, W, N) > budget) continue;
-      const int act = mas::fwd4_max_active_clusters(g->R, W, N, K);
-      if (act <= 0) continue;
-      const int64_t waves = (static_cast<int64_t>(B) + act - 1) / act;
-      if (best < 0 || waves < best_waves) {
-        best = c;
-        best_waves = waves;
-        g->W = W;
-        g->N = N;
-        g->K = K;
+    int best_bands = 0;
+    for (int c = 0; c < ncand && !(best >= 0 && best_waves == 1); ++c) {
+      const int W = std::min(cand[c][0], warps_total), N = cand[c][1];
+      if (mas::fwd4_smem_bytes(g->R, W, N) > budget) continue;
+      int last_K = -1;
+      for (int nb = 1; nb <= warps_total; ++nb) {
+        const int per_band = (warps_total + nb - 1) / nb;
+        if (per_band > band_warps_cap) continue;
+        const int K = (per_band + W - 1) / W;
+        if (K > mas::kMaxClusterCtas || K == last_K) continue;
+        last_K = K;
+        const int bands = (warps_total + K * W - 1) / (K * W);
+        const int act = mas::fwd4_max_active_clusters(g->R, W, N, K);
+        if (act <= 0) continue;
+        const int64_t waves = (static_cast<int64_t>(B) * bands + act - 1) / act;
+        if (best < 0 || waves < best_waves || (waves == best_waves && bands < best_bands)) {
+          best = c;
+          best_waves = waves;
+          best_bands = bands;
+          g->W = W;
+          g->N = N;
+          g->K = K;
+        }
+        if (waves == 1) break;
       }
-      if (waves == 1) break;
     }
     if (best < 0) return false;
     g->band_rows = g->K * g->W * rows;
@@ -308,14 +318,15 @@ bool encode_map4(const float* q, int64_t pitch, int64_t rows_total, int64_t S, i
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// The uint8 output as {columns, rows} with 32 x 32R boxes (mas_fwd4.cu's
-// fused zero fill).
+// The uint8 output as {columns, rows} with kZeroCols x 32R boxes
+// (mas_fwd4.cu's fused zero fill).
 bool encode_out_map4(uint8_t* out, int64_t rows, int64_t S, int R, CUtensorMap* m) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(S)};
-  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(32 * R)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(mas::kZeroCols),
+                             static_cast<cuuint32_t>(32 * R)};
   const cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, out, dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -360,7 +371,9 @@ struct mas_plan {
   int launches = 0;
   int device = 0;
   int bt_rows = 64;       // backtrack window rows
-  float* d_bnd = nullptr; // banded forward: 2 x [B][bnd_pitch] boundary rows
+  float* d_bnd = nullptr; // bands: [B][bands-1][bnd_pitch] boundary rows
+  int* d_sync = nullptr;  // bands: tickets [B] (one per launch, at its first item) +
+                          //        progress [B][bands-1]
   int bnd_pitch = 0;
   bool internal = false;  // created by mas_align_host / _device, which order the frees
   int item_base = 0;      // added to item indices in messages (validate_item of one item)
@@ -398,6 +411,7 @@ void mas_plan_destroy(mas_plan_t* p) {
   cudaFreeAsync(p->d_flags, st);
   cudaFreeAsync(p->d_locate, st);
   if (p->d_bnd) cudaFreeAsync(p->d_bnd, st);
+  if (p->d_sync) cudaFreeAsync(p->d_sync, st);
   cudaSetDevice(prev);
   delete p;
 }
@@ -509,8 +523,12 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
   if (g.bands > 1) {
     p->bnd_pitch = (speech_cap + 31) & ~31;
     if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_bnd),
-                             2 * nB * p->bnd_pitch * sizeof(float), st)) != cudaSuccess)
+                             nB * (g.bands - 1) * p->bnd_pitch * sizeof(float), st)) !=
+        cudaSuccess)
       return fail(e, "cudaMallocAsync(boundary rows)");
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_sync),
+                             nB * g.bands * sizeof(int), st)) != cudaSuccess)
+      return fail(e, "cudaMallocAsync(band progress)");
   }
   if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_flags), nB * sizeof(int), st)) !=
       cudaSuccess)
@@ -578,13 +596,30 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     fa.mnv = p->mnv;
     fa.row0_up = p->mode == 1 ? -std::numeric_limits<float>::infinity() : p->mnv;
     // The output's zero fill rides along with the forward pass when every
-    // item is full length (its warps then cover every row and column);
-    // ragged batches get a stream-ordered memset instead.
-    static const bool no_fuse = [] {
-      const char* e = std::getenv("MAS_NO_FUSED_ZERO");
-      return e && e[0] == '1';
+    // item is full length (its warps then cover every row and column) and
+    // K1 is bound by its column chains: the stores are then nearly free.
+    // When K1 is HBM-bound, interleaving 1 B/cell of writes with the
+    // 4 B/cell read stream costs more than a separate memset (measured at
+    // B256 T512 S4096: 527 us fused vs 380 + ~80 us).  Estimate: the chains
+    // take S x ~50 cycles per warp (x warps per SM sub-partition beyond
+    // one), the stream cells x 4.125 B at ~5.9 TB/s.  Ragged batches always
+    // take the memset.  MAS_FUSED_ZERO=0/1 forces either.
+    static const int fuse_env = [] {
+      const char* e = std::getenv("MAS_FUSED_ZERO");
+      return e ? std::atoi(e) : -1;
     }();
-    const bool fused_zero = d_out && !no_fuse && p->all_full && (p->S % 16) == 0 &&
+    static const int sms = [] {
+      int dev = 0, n = 148;
+      if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+      return n;
+    }();
+    const double warps = static_cast<double>(nb) * g.bands * g.K * g.W;
+    const double chain_s = p->S * 50.0 / 1.9e9 * std::max(1.0, warps / (4.0 * sms));
+    const double stream_s = static_cast<double>(nb) * p->T * p->S * 4.125 / 5.9e12;
+    const bool chain_bound = stream_s <= 1.1 * chain_s;
+    const bool fused_zero = d_out && (fuse_env >= 0 ? fuse_env == 1 : chain_bound) &&
+                            p->all_full && (p->S % 16) == 0 &&
                             (reinterpret_cast<uintptr_t>(d_out) & 15u) == 0;
     const size_t item_bytes = static_cast<size_t>(p->T) * p->S;
     if (d_out && !fused_zero) {
@@ -614,21 +649,24 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     fa.zero = 0.0f;
     fa.T_cap = p->T;
     fa.S_cap = p->S;
-    fa.row_base = 0;
-    fa.bnd_in = nullptr;
-    fa.bnd_out = nullptr;
+    fa.bands = g.bands;
+    fa.band_rows = g.band_rows;
+    fa.nb = nb;
+    fa.bnd = p->d_bnd;
     fa.bnd_pitch = p->bnd_pitch;
+    fa.ticket = p->d_sync ? p->d_sync + b0 : nullptr;
+    fa.progress = p->d_sync ? p->d_sync + p->B : nullptr;
     if (r4) {
-      // One launch per band of K*W*128 rows; band k's bottom row reaches
-      // band k+1 through a [B][bnd_pitch] boundary buffer (double-buffered).
-      for (int band = 0; band < g.bands; ++band) {
-        const size_t half = static_cast<size_t>(p->B) * p->bnd_pitch;
-        fa.row_base = band * g.band_rows;
-        fa.bnd_in = band > 0 ? p->d_bnd + ((band - 1) & 1) * half : nullptr;
-        fa.bnd_out = band + 1 < g.bands ? p->d_bnd + (band & 1) * half : nullptr;
-        MAS_CUDA(mas::launch_fwd4(g.R, p->mode, tm0, tm_out, fa, nb, stream), "launch mas_fwd4");
+      // All bands of all items in one launch (clusters ordered by ticket).
+      if (g.bands > 1) {
+        MAS_CUDA(cudaMemsetAsync(fa.ticket, 0, sizeof(int), stream), "cudaMemsetAsync(ticket)");
+        MAS_CUDA(cudaMemsetAsync(fa.progress + static_cast<size_t>(b0) * (g.bands - 1), 0,
+                                 sizeof(int) * nb * (g.bands - 1), stream),
+                 "cudaMemsetAsync(progress)");
       }
-      nfwd = g.bands;
+      MAS_CUDA(mas::launch_fwd4(g.R, p->mode, tm0, tm_out, fa, nb * g.bands, stream),
+               "launch mas_fwd4");
+      nfwd = 1;
     } else
     {
       MAS_CUDA(mas::launch_fwd(p->mode, tm0, tm1, tm_out, fa, nb, stream), "launch mas_fwd");

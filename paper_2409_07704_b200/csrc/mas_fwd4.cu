@@ -39,6 +39,11 @@ namespace {
 // R = text rows per lane (4 or 2): a warp owns 32 R rows; a stage is one
 // [R residues][32 groups][32 cols] fp32 box (R * 4 KiB).
 constexpr int kCols4 = 32;  // columns per stage / direction word
+// The output's fused zero fill: one TMA store of a {kZCols, 32 R} uint8
+// zero box every kZCols / 32 stages (128-byte row segments: whole L2 lines,
+// a quarter of the scattered 32-byte writes a per-stage box would make).
+constexpr int kZCols = kZeroCols;
+constexpr int kZStages = kZCols / kCols4;
 __host__ __device__ constexpr int rows_of(int R) { return 32 * R; }
 __host__ __device__ constexpr int stage_bytes(int R) { return rows_of(R) * kCols4 * 4; }
 #ifndef MAS_QUAD4
@@ -50,7 +55,7 @@ constexpr int kQuadsPerStage = kCols4 / kQuad;
 constexpr int kFifoIt4 = kFifoSlots / kQuadsPerStage;  // FIFO depth in stages
 
 struct Smem4 {
-  uint32_t ring, bars, ebars, full, empty, sink, fifo, zero, total;
+  uint32_t ring, bars, ebars, full, empty, sink, fifo, zero, ticket, total;
 };
 
 __host__ __device__ inline Smem4 smem4_layout(int R, int W, int N) {
@@ -59,13 +64,16 @@ __host__ __device__ inline Smem4 smem4_layout(int R, int W, int N) {
   L.bars = static_cast<uint32_t>(W * N * stage_bytes(R));
   L.ebars = L.bars + static_cast<uint32_t>(W * N * 8);
   L.full = L.ebars + static_cast<uint32_t>(W * N * 8);
-  L.empty = L.full + static_cast<uint32_t>(W * kFifoSlots * 8);
+  // W + 1 FIFOs: index W is the band drain's staging FIFO (the band's last
+  // warp hands its bottom row to the producer warp, which publishes it)
+  L.empty = L.full + static_cast<uint32_t>((W + 1) * kFifoSlots * 8);
   // one extra "empty" set and sink (index W): the band feeder's, when the
   // first warp of a band gets its row above from global memory
   L.sink = L.empty + static_cast<uint32_t>((W + 1) * kFifoIt4 * 8);
   L.fifo = (L.sink + static_cast<uint32_t>((W + 1) * 16) + 127u) & ~127u;
-  L.zero = L.fifo + static_cast<uint32_t>(W * kFifoSlots * kSlot4);
-  L.total = L.zero + static_cast<uint32_t>(rows_of(R) * kCols4);  // uint8 zero tile
+  L.zero = L.fifo + static_cast<uint32_t>((W + 1) * kFifoSlots * kSlot4);
+  L.ticket = L.zero + static_cast<uint32_t>(rows_of(R) * kZCols);  // after the uint8 zero tile
+  L.total = L.ticket + 16u;
   return L;
 }
 
@@ -82,8 +90,16 @@ struct Fifo4 {
   uint32_t prev_empty, prev_sink;  // producer's "empty" barriers and release sink
   const uint8_t* buf;              // my FIFO's slots
   bool has_in, has_out;
-  float* bnd_out;                  // banded mode: the band's bottom row, this item (or null)
 };
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -269,17 +285,6 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
     for (int q4 = 0; q4 < kQuad / 4; ++q4)
       st_async_v4(dst + 16u * q4, ex[4 * q4], ex[4 * q4 + 1], ex[4 * q4 + 2], ex[4 * q4 + 3], fbar);
   }
-#ifndef MAS_ABL_NOBND
-  if (F.bnd_out != nullptr && is31) {
-#else
-  if (false) {
-#endif
-    // last warp of a band: its bottom row feeds the next band's first warp
-    float4* dst = reinterpret_cast<float4*>(F.bnd_out + q * kQuad);
-#pragma unroll
-    for (int q4 = 0; q4 < kQuad / 4; ++q4)
-      dst[q4] = make_float4(ex[4 * q4], ex[4 * q4 + 1], ex[4 * q4 + 2], ex[4 * q4 + 3]);
-  }
   return ok;
 }
 
@@ -331,7 +336,21 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int crank = static_cast<int>(cluster_ctarank());
-  const int b = a.b0 + static_cast<int>(blockIdx.x) / a.K;
+  // (item, band) of this cluster: the cluster index, or with bands a ticket
+  // drawn by rank 0 in launch order (band-major) and shared over DSMEM.
+  int cl = static_cast<int>(blockIdx.x) / a.K;
+  if (a.bands > 1) {
+    if (crank == 0 && threadIdx.x == 0) {
+      const int t = atomicAdd(a.ticket, 1);
+      for (int r = 0; r < a.K; ++r)
+        asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(mapa(base + SL.ticket, r)), "r"(t)
+                     : "memory");
+    }
+    cluster_sync_all();
+    cl = *reinterpret_cast<volatile int*>(sbase + SL.ticket);
+  }
+  const int band_idx = cl / a.nb;
+  const int b = a.b0 + cl % a.nb;
   const int t_b = static_cast<int>(a.lengths[2 * b]);
   const int s_b = static_cast<int>(a.lengths[2 * b + 1]);
   const int nit = (s_b + kCols4 - 1) / kCols4;
@@ -342,8 +361,10 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   asm volatile("mov.u32 %0, %%smid;" : "=r"(tl_smid));
 #endif
 
-  const int band = a.row_base;  // first text row of this launch (banded mode)
-  const bool fed = band > 0 && a.bnd_in != nullptr;  // band's first warp fed from global
+  const int band = band_idx * a.band_rows;  // first text row of this cluster
+  const bool fed = band_idx > 0;              // band's first warp fed from the band above
+  // this band's bottom row continues in the band below (drained to global)
+  const bool drains = band_idx + 1 < a.bands && band + a.band_rows < t_b && s_b > 0;
   if (warp < W) {
     const int g = crank * W + warp;
     const bool has_in = g > 0 || fed;
@@ -368,11 +389,14 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
         reinterpret_cast<float*>(my_fifo)[k] = a.row0_up;
     }
   } else {
-    for (int k = lane; k < kRows4 * kCols4 / 16; k += 32)
+    for (int k = lane; k < kRows4 * kZCols / 16; k += 32)
       reinterpret_cast<uint4*>(sbase + SL.zero)[k] = make_uint4(0u, 0u, 0u, 0u);
-    if (lane == 0)
+    if (lane == 0) {
       for (int s = 0; s < kFifoIt4; ++s)
         mbar_init(base + SL.empty + static_cast<uint32_t>((W * kFifoIt4 + s) * 8), 1u);
+      for (int s = 0; s < kFifoSlots; ++s)
+        mbar_init(base + SL.full + static_cast<uint32_t>((W * kFifoSlots + s) * 8), 1u);
+    }
   }
   fence_proxy_async_smem();
   fence_mbar_init();
@@ -399,7 +423,10 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       // above the band, written by the previous band's last warp, through
       // its ordinary FIFO: 64-byte bulk copies completing its "full"
       // barriers; slots are released to this lane's "empty" set (index W).
-      const float* src = a.bnd_in + static_cast<size_t>(b) * a.bnd_pitch;
+      const size_t link = static_cast<size_t>(b) * (a.bands - 1) + (band_idx - 1);
+      const float* src = a.bnd + link * a.bnd_pitch;
+      const int* prog = a.progress + link;
+      int avail = 0;  // quads the band above has published
       const uint32_t fempty = base + SL.empty + static_cast<uint32_t>(W * kFifoIt4 * 8);
       for (int m = 0; m < nit; ++m) {
         if (m >= kFifoIt4) {
@@ -411,12 +438,50 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
         for (int k = 0; k < kQuadsPerStage && k * kQuad < nvalid; ++k) {
           const int qq = kQuadsPerStage * m + k;
           const int fs = qq & (kFifoSlots - 1);
+          while (avail <= qq) {
+            avail = ld_acquire_gpu(prog);
+            if (avail <= qq) __nanosleep(256);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                   base + SL.fifo + static_cast<uint32_t>(fs * kSlot4)),
               "l"(src + qq * kQuad), "r"(kSlot4),
               "r"(base + SL.full + static_cast<uint32_t>(fs * 8))
               : "memory");
+        }
+      }
+    }
+    if (w == W + 1 && drains && crank == a.K - 1) {
+      // Band drain: the band's last warp (warp W-1 of the last rank) sends
+      // its bottom row into staging FIFO W like into a consumer's FIFO; this
+      // lane publishes each quad to global memory (release) for the band
+      // below and releases the slots as that warp's consumer would.
+      const size_t link = static_cast<size_t>(b) * (a.bands - 1) + band_idx;
+      float* dst = a.bnd + link * a.bnd_pitch;
+      int* prog = a.progress + link;
+      const uint32_t dfull = base + SL.full + static_cast<uint32_t>(W * kFifoSlots * 8);
+      const uint8_t* dfifo = sbase + SL.fifo + W * kFifoSlots * kSlot4;
+      const uint32_t lempty =
+          mapa(base + SL.empty + static_cast<uint32_t>((W - 1) * kFifoIt4 * 8), crank);
+      const uint32_t lsink = mapa(base + SL.sink + static_cast<uint32_t>((W - 1) * 16), crank);
+      const int nq = (s_b + kQuad - 1) / kQuad;
+      mbar_arrive_expect_tx(dfull, kSlot4);
+      for (int q = 0; q < nq; ++q) {
+        const int fs = q & (kFifoSlots - 1);
+        if (q + 1 < nq)
+          mbar_arrive_expect_tx(dfull + 8u * static_cast<uint32_t>((q + 1) & (kFifoSlots - 1)),
+                                kSlot4);
+        mbar_wait(dfull + 8u * static_cast<uint32_t>(fs), static_cast<uint32_t>(q / kFifoSlots) & 1u);
+        const float4* sp = reinterpret_cast<const float4*>(dfifo + fs * kSlot4);
+        float4* gp = reinterpret_cast<float4*>(dst + q * kQuad);
+#pragma unroll
+        for (int q4 = 0; q4 < kQuad / 4; ++q4) gp[q4] = sp[q4];
+        st_release_gpu(prog, q + 1);
+        if ((q + 1) % kQuadsPerStage == 0 || q + 1 == nq) {
+          const int m = q / kQuadsPerStage;
+          st_async_b32(lsink, static_cast<uint32_t>(m),
+                       lempty + 8u * static_cast<uint32_t>(m % kFifoIt4));
         }
       }
     }
@@ -441,7 +506,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
         mbar_arrive_expect_tx(bar, kStage4);
         tma_load_3d(base + SL.ring + static_cast<uint32_t>((w * N + st) * kStage4), &tmq,
                     m * kCols4, group, 0, bar, pol_q);
-        if (zero_fill) tma_store_2d(&tm_out, zero_tile, m * kCols4, orow);
+        if (zero_fill && m % kZStages == 0) tma_store_2d(&tm_out, zero_tile, m * kCols4, orow);
       }
       if (zero_fill) bulk_store_drain();
     }
@@ -453,7 +518,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   const int g = crank * W + warp;
   const int i0 = band + g * kRows4;
   const bool has_in = g > 0 || fed;
-  const bool last_in_band = g == a.K * W - 1;
+  const bool last_in_band = g == a.K * W - 1;  // its consumer is the band drain
   const bool live = i0 < t_b && s_b > 0;
   if (live) {
     const uint32_t bar0 = base + SL.bars + static_cast<uint32_t>(warp * N * 8);
@@ -461,9 +526,11 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     const uint32_t my_full = base + SL.full + static_cast<uint32_t>(warp * kFifoSlots * 8);
     const uint32_t my_empty = base + SL.empty + static_cast<uint32_t>(warp * kFifoIt4 * 8);
     uint8_t* const my_fifo = sbase + SL.fifo + warp * kFifoSlots * kSlot4;
-    const bool has_out = i0 + kRows4 < t_b && !last_in_band;
+    const bool has_out = i0 + kRows4 < t_b && (!last_in_band || drains);
     int nw = warp + 1, nr = crank;
-    if (nw == W) {
+    if (last_in_band) {
+      nw = W;  // staging FIFO W of this CTA
+    } else if (nw == W) {
       nw = 0;
       nr = crank + 1;
     }
@@ -488,9 +555,6 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     F.buf = my_fifo;
     F.has_in = has_in;
     F.has_out = has_out;
-    F.bnd_out = last_in_band && a.bnd_out != nullptr && i0 + kRows4 < t_b
-                    ? a.bnd_out + static_cast<size_t>(b) * a.bnd_pitch
-                    : nullptr;
 
     const uint8_t* ring_ptr = sbase + SL.ring + warp * N * kStage4;
     // Self-issued stage loads (a.self_tma): lane 0 refills a stage as soon as
@@ -507,7 +571,8 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       mbar_arrive_expect_tx(bar, kStage4);
       tma_load_3d(base + SL.ring + static_cast<uint32_t>((warp * N + st) * kStage4), &tmq,
                   mm * kCols4, tma_group, 0, bar, pol_q);
-      if (zero_fill) tma_store_2d(&tm_out, base + SL.zero, mm * kCols4, tma_orow);
+      if (zero_fill && mm % kZStages == 0)
+        tma_store_2d(&tm_out, base + SL.zero, mm * kCols4, tma_orow);
     };
     if (self_tma && lane == 0) {
       prefetch_tensormap(&tmq);
@@ -607,8 +672,10 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
         if (!self_tma) {
           mbar_arrive_local(ebar0 + 8u * slot);
         } else if (m + N < nit) {
-          fence_proxy_async_smem();  // this warp's reads of the slot before the TMA rewrite
-          issue_stage(m + N);
+#ifdef MAS_SELF_TMA_FENCE
+          fence_proxy_async_smem();
+#endif
+          issue_stage(m + N);  // the warp's reads of the slot completed before __syncwarp
         }
         if (has_in)
           st_async_b32(F.prev_sink, static_cast<uint32_t>(m),

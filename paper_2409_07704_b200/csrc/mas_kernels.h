@@ -21,6 +21,10 @@ constexpr int kQuadCols = 16;  // columns per boundary-row FIFO hand-off
 #endif
 constexpr int kFifoSlots = MAS_FIFO_SLOTS;  // boundary-row FIFO depth, in 16-column quads
 constexpr int kMaxWarpsPerCta = 8;
+#ifndef MAS_ZCOLS
+#define MAS_ZCOLS 128
+#endif
+constexpr int kZeroCols = MAS_ZCOLS;  // mas_fwd4: columns per fused zero-fill TMA store
 constexpr int kMaxClusterCtas = 16;
 
 struct FwdArgs {
@@ -41,13 +45,17 @@ struct FwdArgs {
   int l2_ahead;             // mas_fwd4: stages prefetched into L2 beyond the smem ring
   int self_tma;             // mas_fwd4: each compute warp issues its own stage loads
                             //   (no TMA producer warp competing for its SM sub-partition)
-  // mas_fwd4 banded mode (text longer than one cluster's rows): this launch
-  // computes rows [row_base, row_base + K*W*128); the row above row_base
-  // comes from bnd_in, this band's bottom row goes to bnd_out (both
-  // [B][bnd_pitch] floats, one value per column, or null).
-  int row_base;
-  const float* bnd_in;
-  float* bnd_out;
+  // mas_fwd4 bands (texts taller than one cluster): an item is `bands`
+  // clusters of band_rows rows each, all in ONE launch.  Clusters take
+  // (band, item) from a ticket counter in band-major order, so a cluster
+  // waiting for the band above only waits for clusters already running.
+  // The bottom row of band k goes through bnd [B][bands-1][bnd_pitch]
+  // floats, its progress (32-column quads published) through
+  // progress [B][bands-1]; ticket and progress are zeroed before the launch.
+  int bands, band_rows, nb;
+  float* bnd;
+  int* progress;
+  int* ticket;
   int bnd_pitch;
   uint32_t one;             // 1 and 0.0f passed at run time so ptxas keeps the
   float zero;               //   bit IMADs / NonFinite FFMAs on the FMA pipe
