@@ -38,20 +38,26 @@ namespace {
 
 // R = text rows per lane (4 or 2): a warp owns 32 R rows; a stage is one
 // [R residues][32 groups][32 cols] fp32 box (R * 4 KiB).
-constexpr int kCols4 = 32;  // columns per stage / direction word
+constexpr int kCols4 = 32;  // columns per TMA box / direction word ("chunk")
+#ifndef MAS_STAGE_COLS
+#define MAS_STAGE_COLS 32
+#endif
+constexpr int kSC = MAS_STAGE_COLS;     // columns per stage (32 or 64)
+constexpr int kChunks = kSC / kCols4;   // chunks (direction words per row) per stage
 // The output's fused zero fill: one TMA store of a {kZCols, 32 R} uint8
 // zero box every kZCols / 32 stages (128-byte row segments: whole L2 lines,
 // a quarter of the scattered 32-byte writes a per-stage box would make).
 constexpr int kZCols = kZeroCols;
-constexpr int kZStages = kZCols / kCols4;
+constexpr int kZStages = kZCols / kSC;
 __host__ __device__ constexpr int rows_of(int R) { return 32 * R; }
-__host__ __device__ constexpr int stage_bytes(int R) { return rows_of(R) * kCols4 * 4; }
+__host__ __device__ constexpr int chunk_bytes(int R) { return rows_of(R) * kCols4 * 4; }
+__host__ __device__ constexpr int stage_bytes(int R) { return chunk_bytes(R) * kChunks; }
 #ifndef MAS_QUAD4
 #define MAS_QUAD4 32
 #endif
 constexpr int kQuad = MAS_QUAD4;            // columns per FIFO hand-off (16 or 32)
 constexpr int kSlot4 = kQuad * 4;           // FIFO slot bytes
-constexpr int kQuadsPerStage = kCols4 / kQuad;
+constexpr int kQuadsPerStage = kSC / kQuad;
 constexpr int kFifoIt4 = kFifoSlots / kQuadsPerStage;  // FIFO depth in stages
 
 struct Smem4 {
@@ -80,7 +86,8 @@ __host__ __device__ inline Smem4 smem4_layout(int R, int W, int N) {
 template <int R>
 struct Lane4 {
   float o[R];   // Q of the lane's rows at the previous column
-  float acc;    // max.NaN of |q|: NaN / +inf iff a non-finite q was seen
+  float acc[R / 2];  // max.NaN of |q| (independent chains, one per row pair):
+                     // NaN / +inf iff a non-finite q was seen
   float vlast;  // producer's bottom row at the previous column
 };
 
@@ -190,8 +197,14 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
       }
     }
 #ifndef MAS_ABL_NOFOLD
+#ifndef MAS_FOLD_FFMA
 #pragma unroll
-    for (int r = 0; r + 1 < R; r += 2) fold_abs_max_nan(L.acc, q[r], q[r + 1]);
+    for (int r = 0; r + 1 < R; r += 2) fold_abs_max_nan(L.acc[r / 2], q[r], q[r + 1]);
+#else
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      asm("fma.rn.f32 %0, %1, 0f00000000, %0;" : "+f"(L.acc[r / 2]) : "f"(q[r]));
+#endif
 #endif
     ex[(U0 % kQuad) + e] = n[R - 1];
 #pragma unroll
@@ -215,7 +228,7 @@ struct Probes {
 template <int R, int MODE, bool GENERIC, int K>
 __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (&coff)[8],
                                          const Fifo4& F, float (&ex)[kQuad], Lane4<R>& L,
-                                         uint32_t (&w)[R], bool& ready, bool more, bool is31,
+                                         uint32_t (&w)[kChunks][R], bool& ready, bool more, bool is31,
                                          int lane, int srclane, int q, int c_base, int nvalid,
                                          int row0, float mnv, bool row0_is_zero,
                                          Probes& P) {
@@ -258,16 +271,18 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
       _Pragma("unroll") for (int r = 0; r < R; ++r) wf[r] = kBitsBase;                          \
     }                                                                                           \
     if (ok)                                                                                     \
-      ok = fwd4_group<R, MODE, GENERIC, U0>(stage, coff[(U0 / 4) & 7], slot, ex, L, wf, is31,   \
+      ok = fwd4_group<R, MODE, GENERIC, U0>(stage + (U0 / kCols4) * chunk_bytes(R),            \
+                                            coff[(U0 / 4) & 7], slot, ex, L, wf, is31,          \
                                             srclane, c_base, nvalid, row0, mnv, row0_is_zero);  \
     if constexpr (U0 % 16 == 12) {                                                              \
       _Pragma("unroll") for (int r = 0; r < R; ++r) {                                           \
         const uint32_t v = __float_as_uint(wf[r]) & 0xffffu;                                    \
-        w[r] |= U0 < 16 ? v << 16 : v;                                                          \
+        w[U0 / kCols4][r] |= U0 % kCols4 < 16 ? v << 16 : v;                                    \
       }                                                                                         \
     }                                                                                           \
   }
   MAS_G4(0) MAS_G4(1) MAS_G4(2) MAS_G4(3) MAS_G4(4) MAS_G4(5) MAS_G4(6) MAS_G4(7)
+  MAS_G4(8) MAS_G4(9) MAS_G4(10) MAS_G4(11) MAS_G4(12) MAS_G4(13) MAS_G4(14) MAS_G4(15)
 #undef MAS_G4
   ready = probe;
   if (K == 0) {
@@ -291,7 +306,7 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
 template <int R, int MODE, bool GENERIC>
 __device__ __forceinline__ void fwd4_stage(const uint8_t* stage, const uint32_t (&coff)[8],
                                           const Fifo4& F, float (&ex)[kQuad], Lane4<R>& L,
-                                          uint32_t (&w)[R], bool& ready, bool more, bool is31,
+                                          uint32_t (&w)[kChunks][R], bool& ready, bool more, bool is31,
                                           int lane, int srclane, int q0, int c_base, int nvalid,
                                           int row0, float mnv, bool row0_is_zero,
                                           Probes& P) {
@@ -353,7 +368,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   const int b = a.b0 + cl % a.nb;
   const int t_b = static_cast<int>(a.lengths[2 * b]);
   const int s_b = static_cast<int>(a.lengths[2 * b + 1]);
-  const int nit = (s_b + kCols4 - 1) / kCols4;
+  const int nit = (s_b + kSC - 1) / kSC;
 #ifdef MAS_FWD_TIMELINE
   unsigned long long tl_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_start));
@@ -434,7 +449,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
           mbar_arrive_expect_tx(eb, 4u);
           mbar_wait(eb, (static_cast<uint32_t>(m / kFifoIt4) & 1u) ^ 1u);
         }
-        const int nvalid = s_b - m * kCols4 < kCols4 ? s_b - m * kCols4 : kCols4;
+        const int nvalid = s_b - m * kSC < kSC ? s_b - m * kSC : kSC;
         for (int k = 0; k < kQuadsPerStage && k * kQuad < nvalid; ++k) {
           const int qq = kQuadsPerStage * m + k;
           const int fs = qq & (kFifoSlots - 1);
@@ -493,7 +508,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       const int group = (b * a.T_pad + i0w) / R;
       const int orow = b * a.T_cap + i0w;
       const int l2a = a.l2_ahead;
-      for (int m = 0; m < l2a && m < nit; ++m) tma_prefetch_3d(&tmq, m * kCols4, group, 0);
+      for (int m = 0; m < l2a && m < nit; ++m) tma_prefetch_3d(&tmq, m * kSC, group, 0);
       for (int m = 0; m < nit; ++m) {
         const int st = m % N;
         const uint32_t bar = base + SL.bars + static_cast<uint32_t>((w * N + st) * 8);
@@ -502,11 +517,14 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
           const uint32_t eb = base + SL.ebars + static_cast<uint32_t>((w * N + st) * 8);
           mbar_wait(eb, (static_cast<uint32_t>(m / N) & 1u) ^ 1u);
         }
-        if (l2a > 0 && m + l2a < nit) tma_prefetch_3d(&tmq, (m + l2a) * kCols4, group, 0);
+        if (l2a > 0 && m + l2a < nit) tma_prefetch_3d(&tmq, (m + l2a) * kSC, group, 0);
         mbar_arrive_expect_tx(bar, kStage4);
-        tma_load_3d(base + SL.ring + static_cast<uint32_t>((w * N + st) * kStage4), &tmq,
-                    m * kCols4, group, 0, bar, pol_q);
-        if (zero_fill && m % kZStages == 0) tma_store_2d(&tm_out, zero_tile, m * kCols4, orow);
+#pragma unroll
+        for (int c = 0; c < kChunks; ++c)
+          tma_load_3d(base + SL.ring +
+                          static_cast<uint32_t>((w * N + st) * kStage4 + c * chunk_bytes(R)),
+                      &tmq, m * kSC + c * kCols4, group, 0, bar, pol_q);
+        if (zero_fill && m % kZStages == 0) tma_store_2d(&tm_out, zero_tile, m * kSC, orow);
       }
       if (zero_fill) bulk_store_drain();
     }
@@ -569,10 +587,13 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       const int st = mm % N;
       const uint32_t bar = bar0 + 8u * static_cast<uint32_t>(st);
       mbar_arrive_expect_tx(bar, kStage4);
-      tma_load_3d(base + SL.ring + static_cast<uint32_t>((warp * N + st) * kStage4), &tmq,
-                  mm * kCols4, tma_group, 0, bar, pol_q);
+#pragma unroll
+      for (int c = 0; c < kChunks; ++c)
+        tma_load_3d(base + SL.ring +
+                        static_cast<uint32_t>((warp * N + st) * kStage4 + c * chunk_bytes(R)),
+                    &tmq, mm * kSC + c * kCols4, tma_group, 0, bar, pol_q);
       if (zero_fill && mm % kZStages == 0)
-        tma_store_2d(&tm_out, base + SL.zero, mm * kCols4, tma_orow);
+        tma_store_2d(&tm_out, base + SL.zero, mm * kSC, tma_orow);
     };
     if (self_tma && lane == 0) {
       prefetch_tensormap(&tmq);
@@ -591,7 +612,8 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     Lane4<R> L;
 #pragma unroll
     for (int r = 0; r < R; ++r) L.o[r] = 0.0f;
-    L.acc = 0.0f;
+#pragma unroll
+    for (int r = 0; r < R / 2; ++r) L.acc[r] = 0.0f;
     L.vlast = a.row0_up;
     float ex[kQuad];
 #pragma unroll
@@ -607,6 +629,14 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     long long pf_t0 = clock64(), pf_stage = 0, pf_empty = 0, pf_comp = 0, pf_rest = 0;
 #endif
 
+    auto store_words = [&](uint32_t* p, const uint32_t (&v)[R]) {
+      if constexpr (R == 4)
+        asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
+                     "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "l"(pol_dir));
+      else
+        asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(v[0]),
+                     "r"(v[1]), "l"(pol_dir));
+    };
     int slot = 0;
     uint32_t par = 0;
     for (int m = 0; m < nit; ++m) {
@@ -619,13 +649,15 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       pf_stage += pf_b - pf_a;
 #endif
       const uint8_t* stage = ring_ptr + slot * kStage4;
-      const int c_base = m * kCols4;
-      const int nvalid = s_b - c_base < kCols4 ? s_b - c_base : kCols4;
-      uint32_t w[R];
+      const int c_base = m * kSC;
+      const int nvalid = s_b - c_base < kSC ? s_b - c_base : kSC;
+      uint32_t w[kChunks][R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) w[r] = 0u;
+      for (int c = 0; c < kChunks; ++c)
+#pragma unroll
+        for (int r = 0; r < R; ++r) w[c][r] = 0u;
       const bool generic =
-          m == 0 || nvalid < kCols4 || (MODE == 1 && c_base < i0 + kRows4 - 1);
+          m == 0 || nvalid < kSC || (MODE == 1 && c_base < i0 + kRows4 - 1);
       if (has_out && m >= kFifoIt4 && !empty_ready) {
         // This iteration's slots in the consumer are free once it released
         // iteration m - kFifoIt4 (4-byte st.async on empty[m % kFifoIt4]).
@@ -655,7 +687,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
                                P);
       } else {
         fwd4_stage<R, MODE, false>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
-                                kQuadsPerStage * m, c_base, kCols4, row0, mnv, row0_is_zero,
+                                kQuadsPerStage * m, c_base, kSC, row0, mnv, row0_is_zero,
                                 P);
       }
       stage_ready = P.stage_ok;
@@ -685,16 +717,14 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       // steps above row 0 or left of column 0).
       if (m == 0) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) w[r] &= 0x7fffffffu;
+        for (int r = 0; r < R; ++r) w[0][r] &= 0x7fffffffu;
       }
-      if (row0_is_zero) w[0] = 0u;
-      if constexpr (R == 4)
-        asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dirs_ptr),
-                     "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "l"(pol_dir)
-                     : "memory");
-      else
-        st_global_v2_evict_last(dirs_ptr, w[0], w[1], pol_dir);
-      dirs_ptr += a.T_alloc;
+#pragma unroll
+      for (int c = 0; c < kChunks; ++c) {
+        if (row0_is_zero) w[c][0] = 0u;
+        if (c == 0 || m * kChunks + c < a.M) store_words(dirs_ptr + c * a.T_alloc, w[c]);
+      }
+      dirs_ptr += kChunks * a.T_alloc;
       slot = slot + 1 == N ? 0 : slot + 1;
       par ^= slot == 0 ? 1u : 0u;
 #ifdef MAS_FWD_PROFILE
@@ -711,7 +741,10 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     bool bad = false;
 #pragma unroll
     for (int r = 0; r < R; ++r) bad |= row0 + r < t_b;
-    bad = bad && !(L.acc < INFINITY);
+    bool nonfinite = false;
+#pragma unroll
+    for (int r = 0; r < R / 2; ++r) nonfinite |= !(L.acc[r] < INFINITY);
+    bad = bad && nonfinite;
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flags + b, 1);
   }
   __syncwarp();
