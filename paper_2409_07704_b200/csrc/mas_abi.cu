@@ -640,11 +640,6 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     }();
     // L2 prefetch lead (stages beyond the smem ring) when the ring is short.
     fa.l2_ahead = l2_ahead >= 0 ? l2_ahead : 0;  // measured: L2 prefetch only hurts
-    static const int self_tma = [] {
-      const char* e = std::getenv("MAS_SELF_TMA");  // experiment override
-      return e ? std::atoi(e) : -1;
-    }();
-    fa.self_tma = self_tma >= 0 ? self_tma : 0;
     fa.one = 1u;
     fa.zero = 0.0f;
     fa.T_cap = p->T;

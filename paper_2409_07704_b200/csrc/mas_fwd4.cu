@@ -289,11 +289,7 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
     P.stage_ok = p_stage;
     P.empty_ok = p_empty;
   }
-#ifndef MAS_ABL_NOFIFO
   if (F.has_out && is31) {
-#else
-  if (false) {
-#endif
     const uint32_t dst = F.next_fifo + static_cast<uint32_t>(fs * kSlot4);
     const uint32_t fbar = F.next_full + 8u * fs;
 #pragma unroll
@@ -500,7 +496,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
         }
       }
     }
-    if (w < W && s_b > 0 && i0w < t_b && !a.self_tma) {
+    if (w < W && s_b > 0 && i0w < t_b) {
       prefetch_tensormap(&tmq);
       const uint64_t pol_q = policy_evict_first();
       const bool zero_fill = a.zero_fill != 0;
@@ -575,30 +571,6 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     F.has_out = has_out;
 
     const uint8_t* ring_ptr = sbase + SL.ring + warp * N * kStage4;
-    // Self-issued stage loads (a.self_tma): lane 0 refills a stage as soon as
-    // the warp has consumed it, so no producer warp spins on this SM
-    // sub-partition.  The output's zero tiles ride along as before.
-    const bool self_tma = a.self_tma != 0;
-    const bool zero_fill = a.zero_fill != 0;
-    const int tma_group = (b * a.T_pad + i0) / R;
-    const int tma_orow = b * a.T_cap + i0;
-    const uint64_t pol_q = policy_evict_first();
-    auto issue_stage = [&](int mm) {
-      const int st = mm % N;
-      const uint32_t bar = bar0 + 8u * static_cast<uint32_t>(st);
-      mbar_arrive_expect_tx(bar, kStage4);
-#pragma unroll
-      for (int c = 0; c < kChunks; ++c)
-        tma_load_3d(base + SL.ring +
-                        static_cast<uint32_t>((warp * N + st) * kStage4 + c * chunk_bytes(R)),
-                    &tmq, mm * kSC + c * kCols4, tma_group, 0, bar, pol_q);
-      if (zero_fill && mm % kZStages == 0)
-        tma_store_2d(&tm_out, base + SL.zero, mm * kSC, tma_orow);
-    };
-    if (self_tma && lane == 0) {
-      prefetch_tensormap(&tmq);
-      for (int mm = 0; mm < N && mm < nit; ++mm) issue_stage(mm);
-    }
     uint32_t coff[8];
 #pragma unroll
     for (int a4 = 0; a4 < 8; ++a4) coff[a4] = lane * 128u + ((a4 ^ (lane & 7)) << 4);
@@ -608,6 +580,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     const int srclane = (lane + 31) & 31;
     const int row0 = i0 + R * lane;
     const bool row0_is_zero = row0 == 0;
+    const uint32_t row0_mask = row0_is_zero ? 0u : 0xffffffffu;
     const float mnv = a.mnv;
     Lane4<R> L;
 #pragma unroll
@@ -701,27 +674,21 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       // slots to the warp above.
       __syncwarp();
       if (lane == 0) {
-        if (!self_tma) {
-          mbar_arrive_local(ebar0 + 8u * slot);
-        } else if (m + N < nit) {
-#ifdef MAS_SELF_TMA_FENCE
-          fence_proxy_async_smem();
-#endif
-          issue_stage(m + N);  // the warp's reads of the slot completed before __syncwarp
-        }
+        mbar_arrive_local(ebar0 + 8u * slot);
         if (has_in)
           st_async_b32(F.prev_sink, static_cast<uint32_t>(m),
                        F.prev_empty + 8u * static_cast<uint32_t>(m % kFifoIt4));
       }
       // Row 0 and column -1 are stored as zero bits (the backtrack never
       // steps above row 0 or left of column 0).
-      if (m == 0) {
+      {
+        const uint32_t col_mask = m == 0 ? 0x7fffffffu : 0xffffffffu;
 #pragma unroll
-        for (int r = 0; r < R; ++r) w[0][r] &= 0x7fffffffu;
+        for (int r = 0; r < R; ++r) w[0][r] &= col_mask;
       }
 #pragma unroll
       for (int c = 0; c < kChunks; ++c) {
-        if (row0_is_zero) w[c][0] = 0u;
+        w[c][0] &= row0_mask;
         if (c == 0 || m * kChunks + c < a.M) store_words(dirs_ptr + c * a.T_alloc, w[c]);
       }
       dirs_ptr += kChunks * a.T_alloc;
@@ -736,7 +703,6 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       printf("fwd4 warp g=%d: total %lld, stage-wait %lld, empty-wait %lld, compute %lld (%.1f/col), rest %lld, nit %d\n",
              g, clock64() - pf_t0, pf_stage, pf_empty, pf_comp, (double)pf_comp / s_b, pf_rest, nit);
 #endif
-    if (self_tma && zero_fill && lane == 0) bulk_store_drain();
     __syncwarp();
     bool bad = false;
 #pragma unroll

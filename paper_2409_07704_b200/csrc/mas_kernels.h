@@ -43,8 +43,6 @@ struct FwdArgs {
   int zero_fill;            // 1: TMA-store zero tiles of the output (tm_out) as we go
   int T_cap, S_cap;         // output shape
   int l2_ahead;             // mas_fwd4: stages prefetched into L2 beyond the smem ring
-  int self_tma;             // mas_fwd4: each compute warp issues its own stage loads
-                            //   (no TMA producer warp competing for its SM sub-partition)
   // mas_fwd4 bands (texts taller than one cluster): an item is `bands`
   // clusters of band_rows rows each, all in ONE launch.  Clusters take
   // (band, item) from a ticket counter in band-major order, so a cluster

@@ -72,6 +72,23 @@ __device__ __forceinline__ void mbar_wait_all(uint32_t bar, uint32_t parity) {
 }
 #endif
 
+// Predicated forms (one guarded instruction instead of a branch around it:
+// the per-quad bookkeeping otherwise costs BSSY/ISETP/BRA per operation).
+__device__ __forceinline__ void mbar_arrive_expect_tx_if(bool c, uint32_t bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+      "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bar),
+      "r"(bytes), "r"(static_cast<int>(c))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_local_if(bool c, uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %1, 0;\n\t"
+      "@p mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(bar),
+      "r"(static_cast<int>(c))
+      : "memory");
+}
+
 // ---- TMA ------------------------------------------------------------------
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -150,6 +167,23 @@ __device__ __forceinline__ void st_async_v4(uint32_t addr, float a, float b, flo
       "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
       "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(__float_as_uint(c)),
       "r"(__float_as_uint(d)), "r"(remote_bar)
+      : "memory");
+}
+__device__ __forceinline__ void st_async_v4_if(bool c, uint32_t addr, float a, float b, float d0,
+                                               float d1, uint32_t remote_bar) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %6, 0;\n\t"
+      "@p st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];\n\t}" ::"r"(addr),
+      "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(__float_as_uint(d0)),
+      "r"(__float_as_uint(d1)), "r"(remote_bar), "r"(static_cast<int>(c))
+      : "memory");
+}
+__device__ __forceinline__ void st_async_b32_if(bool c, uint32_t addr, uint32_t v,
+                                                uint32_t remote_bar) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+      "@p st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n\t}" ::"r"(addr),
+      "r"(v), "r"(remote_bar), "r"(static_cast<int>(c))
       : "memory");
 }
 __device__ __forceinline__ void st_async_b32(uint32_t addr, uint32_t v, uint32_t remote_bar) {
