@@ -197,6 +197,24 @@ MAS_API int mas_validate_host(const float* values, int32_t batch, int32_t text_c
 MAS_API int mas_generate_device(uint64_t seed, int32_t batch, int32_t text_cap, int32_t speech_cap,
                         int64_t first_item, int64_t row_pitch, float* d_out, void* stream);
 
+/* ---- MASTENS v1 tensor files (tensor_io.hpp:11-23, tensor_io.cpp) --------
+ * Host-only.  Errors are MAS_E_IO with the reference's IoError code and text
+ * (IoFailure, BadMagic, UnsupportedVersion, TruncatedFile, DimensionOverflow).
+ * dtype: 0 = float32 (LikelihoodBatch), 1 = uint8 (AlignmentMatrix).
+ * The header is validated -- including the byte budget (read_tensor's
+ * byte_budget, default 1 GiB) -- before any payload is read. */
+#define MAS_IO_DEFAULT_BYTE_BUDGET (1ull << 30)
+MAS_API int mas_io_read_header(const char* path, uint64_t byte_budget, int32_t* dtype,
+                               int64_t dims[3], int32_t* lengths_present, mas_error_t* err);
+/* Payload into `values` (dims product x dtype size bytes) and the lengths
+ * table into `lengths` [B][2] (full lengths when the file has none). */
+MAS_API int mas_io_read(const char* path, uint64_t byte_budget, void* values, uint32_t* lengths,
+                        mas_error_t* err);
+/* write_tensor: header, payload, lengths table ([B][2] or NULL = full). */
+MAS_API int mas_io_write(const char* path, int32_t dtype, int64_t batch, int64_t text_cap,
+                         int64_t speech_cap, const void* values, const uint32_t* lengths,
+                         mas_error_t* err);
+
 MAS_API const char* mas_errc_name(int32_t errc);
 MAS_API int mas_abi_version(void);
 

@@ -161,7 +161,45 @@ class Reference:
         lib.ref_batch_time_align.restype = ctypes.c_double
         lib.ref_batch_time_align.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                              ctypes.POINTER(ctypes.c_int64)]
+        lib.ref_tensor_write.restype = ctypes.c_int
+        lib.ref_tensor_write.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_char_p, ctypes.c_int]
+        lib.ref_tensor_read.restype = ctypes.c_int
+        lib.ref_tensor_read.argtypes = [ctypes.c_char_p, ctypes.c_uint64,
+                                        ctypes.POINTER(ctypes.c_int),
+                                        ctypes.POINTER(ctypes.c_int64 * 3), ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int]
         self.lib = lib
+
+    def write_tensor(self, path, values, lengths=None):
+        """io::write_tensor (tensor_io.cpp).  Returns (errc, message); -1 = ok."""
+        v = np.ascontiguousarray(values)
+        if v.ndim == 2:
+            v = v[None]
+        B, T, S = v.shape
+        lens = None if lengths is None else np.ascontiguousarray(lengths, dtype=np.uint32)
+        msg = ctypes.create_string_buffer(512)
+        rc = self.lib.ref_tensor_write(os.fsencode(path), 0 if v.dtype == np.float32 else 1, B, T,
+                                       S, v.ctypes.data,
+                                       None if lens is None else lens.ctypes.data, msg, 512)
+        return rc, msg.value.decode()
+
+    def read_tensor(self, path, budget=1 << 30):
+        """io::read_tensor.  Returns (errc, message, values, lengths)."""
+        msg = ctypes.create_string_buffer(512)
+        dtype = ctypes.c_int()
+        dims = (ctypes.c_int64 * 3)()
+        rc = self.lib.ref_tensor_read(os.fsencode(path), budget, ctypes.byref(dtype),
+                                      ctypes.byref(dims), None, None, msg, 512)
+        if rc != -1:
+            return rc, msg.value.decode(), None, None
+        vals = np.empty(tuple(dims), np.float32 if dtype.value == 0 else np.uint8)
+        lens = np.empty((dims[0], 2), np.uint32)
+        rc = self.lib.ref_tensor_read(os.fsencode(path), budget, ctypes.byref(dtype),
+                                      ctypes.byref(dims), vals.ctypes.data, lens.ctypes.data,
+                                      msg, 512)
+        return rc, msg.value.decode(), vals, lens
 
     @staticmethod
     def available(path: str = REF_SO) -> bool:

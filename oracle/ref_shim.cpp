@@ -14,6 +14,7 @@
 //   path_from_matrix                     include/monoalign/types.hpp:155-158
 //   bench::generate_random_batch         include/monoalign/bench.hpp:58
 //   oracle::best_paths                   include/monoalign/oracle.hpp:33
+//   io::write_tensor / io::read_tensor   include/monoalign/tensor_io.hpp:29-36
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -24,6 +25,7 @@
 #include "monoalign/align.hpp"
 #include "monoalign/bench.hpp"
 #include "monoalign/oracle.hpp"
+#include "monoalign/tensor_io.hpp"
 
 namespace {
 
@@ -158,6 +160,67 @@ double ref_batch_time_align(void* batch, int engine, int threads, std::int64_t* 
     return std::chrono::duration<double, std::milli>(t1 - t0).count();
   } catch (...) {
     return -1.0;
+  }
+}
+
+/// io::write_tensor of a LikelihoodBatch (dtype 0) or AlignmentMatrix
+/// (dtype 1) built from values / lengths ([B][2] u32 or null = full).
+int ref_tensor_write(const char* path, int dtype, int B, int T, int S, const void* values,
+                     const std::uint32_t* lengths, char* msg, int msg_cap) {
+  try {
+    auto fill = [&](auto& c) {
+      std::memcpy(c.values.data(), values, c.values.size() * sizeof(c.values[0]));
+      if (lengths)
+        for (int b = 0; b < B; ++b) c.lengths[b] = {lengths[2 * b], lengths[2 * b + 1]};
+    };
+    if (dtype == 0) {
+      monoalign::LikelihoodBatch batch(B, T, S);
+      fill(batch);
+      monoalign::io::write_tensor(path, batch);
+    } else {
+      monoalign::AlignmentMatrix m(B, T, S);
+      fill(m);
+      monoalign::io::write_tensor(path, m);
+    }
+    return -1;
+  } catch (const monoalign::Error& e) {
+    put_msg(e.what(), msg, msg_cap);
+    return static_cast<int>(e.code());
+  } catch (const std::exception& e) {
+    put_msg(e.what(), msg, msg_cap);
+    return 1000;
+  }
+}
+
+/// io::read_tensor(path, budget): dtype, dims and (if non-null) the payload
+/// and lengths table copied out.
+int ref_tensor_read(const char* path, std::uint64_t budget, int* dtype, std::int64_t* dims,
+                    void* values, std::uint32_t* lengths, char* msg, int msg_cap) {
+  try {
+    const monoalign::io::Tensor t = monoalign::io::read_tensor(path, budget);
+    auto out = [&](const auto& c, int code) {
+      *dtype = code;
+      dims[0] = c.batch;
+      dims[1] = c.text_cap;
+      dims[2] = c.speech_cap;
+      if (values) std::memcpy(values, c.values.data(), c.values.size() * sizeof(c.values[0]));
+      if (lengths)
+        for (int b = 0; b < c.batch; ++b) {
+          lengths[2 * b] = c.lengths[b].text;
+          lengths[2 * b + 1] = c.lengths[b].speech;
+        }
+    };
+    if (const auto* batch = std::get_if<monoalign::LikelihoodBatch>(&t))
+      out(*batch, 0);
+    else
+      out(std::get<monoalign::AlignmentMatrix>(t), 1);
+    return -1;
+  } catch (const monoalign::Error& e) {
+    put_msg(e.what(), msg, msg_cap);
+    return static_cast<int>(e.code());
+  } catch (const std::exception& e) {
+    put_msg(e.what(), msg, msg_cap);
+    return 1000;
   }
 }
 

@@ -16,6 +16,8 @@ from .api import (
     align_paths,
     generate_device,
     generate_random_batch,
+    read_tensor,
+    write_tensor,
 )
 
 __all__ = [
@@ -26,4 +28,6 @@ __all__ = [
     "generate_random_batch",
     "generate_device",
     "Plan",
+    "read_tensor",
+    "write_tensor",
 ]

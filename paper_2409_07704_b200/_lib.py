@@ -25,6 +25,7 @@ MAS_FLAG_UNCHECKED = 0x1
 MAS_PART_FORWARD = 0x1
 MAS_PART_BACKTRACK = 0x2
 MAS_PART_ALL = 0x3
+MAS_IO_DEFAULT_BYTE_BUDGET = 1 << 30
 
 # include/monoalign/errors.hpp:8-30 of the reference, declaration order.
 ERRC_NAMES = (
@@ -91,6 +92,15 @@ _SIGS = {
     "mas_validate_config": (ctypes.c_int, [ctypes.POINTER(MasConfig), ctypes.POINTER(MasError)]),
     "mas_validate_host": (ctypes.c_int, [_VP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _VP,
                                          ctypes.c_int32, ctypes.POINTER(MasError)]),
+    "mas_io_read_header": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint64,
+                                          ctypes.POINTER(ctypes.c_int32),
+                                          ctypes.POINTER(ctypes.c_int64 * 3),
+                                          ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(MasError)]),
+    "mas_io_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint64, _VP, _VP,
+                                   ctypes.POINTER(MasError)]),
+    "mas_io_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int64,
+                                    ctypes.c_int64, ctypes.c_int64, _VP, _VP,
+                                    ctypes.POINTER(MasError)]),
     "mas_errc_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "mas_abi_version": (ctypes.c_int, []),
 }

@@ -11,6 +11,7 @@ stay on the device (no host copy).
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -189,6 +190,52 @@ def _align_unchecked(values, lengths=None, engine="parallel", max_neg_val=_DEFAU
     out, _, _, was_2d, _, _, _ = _align_impl(values, lengths, engine, max_neg_val, threads, True,
                                              True, False)
     return out[0] if was_2d else out
+
+
+# ---- MASTENS v1 tensor files (module.cpp:156-190, tensor_io.hpp) ----------
+def read_tensor(path):
+    """Read a tensor file; returns (values, lengths) where values is float32 or
+    uint8 [B, T, S] and lengths is uint32 [B, 2].  (module.cpp:237-239;
+    OSError with the reference's IoError text on a bad or truncated file.)"""
+    lib = _lib.load()
+    p = os.fsencode(path)
+    err = _lib.MasError()
+    dtype = ctypes.c_int32()
+    dims = (ctypes.c_int64 * 3)()
+    has_len = ctypes.c_int32()
+    rc = lib.mas_io_read_header(p, _lib.MAS_IO_DEFAULT_BYTE_BUDGET, ctypes.byref(dtype),
+                                ctypes.byref(dims), ctypes.byref(has_len), ctypes.byref(err))
+    _lib.raise_for(rc, err)
+    shape = (dims[0], dims[1], dims[2])
+    values = np.empty(shape, np.float32 if dtype.value == 0 else np.uint8)
+    lengths = np.empty((dims[0], 2), np.uint32)
+    rc = lib.mas_io_read(p, _lib.MAS_IO_DEFAULT_BYTE_BUDGET, values.ctypes.data,
+                         lengths.ctypes.data, ctypes.byref(err))
+    _lib.raise_for(rc, err)
+    return values, lengths
+
+
+def write_tensor(path, values, lengths=None):
+    """Write a float32 (likelihood) or uint8 (alignment) array as a tensor
+    file (module.cpp:169-190, 241-243): [T, S] or [B, T, S], optional [B, 2]
+    lengths checked as in align; any other dtype raises ValueError."""
+    if _is_torch(values):
+        values = values.detach().cpu().numpy()
+    values = np.asarray(values)
+    if values.dtype == np.float32:
+        dtype = 0
+    elif values.dtype == np.uint8:
+        dtype = 1
+    else:
+        raise ValueError("values dtype must be float32 or uint8")
+    values = np.ascontiguousarray(values)
+    _, b, t, s = _check_dims(values.shape)
+    lens = None if lengths is None else _parse_lengths(lengths, b, t, s)
+    lib = _lib.load()
+    err = _lib.MasError()
+    rc = lib.mas_io_write(os.fsencode(path), dtype, b, t, s, values.ctypes.data,
+                          None if lens is None else lens.ctypes.data, ctypes.byref(err))
+    _lib.raise_for(rc, err)
 
 
 def generate_random_batch(b, t, s, seed):

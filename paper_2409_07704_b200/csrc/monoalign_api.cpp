@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "monoalign/align.hpp"
+#include "monoalign/tensor_io.hpp"
 #include "../../include/monoalign_b200.h"
 
 namespace monoalign {
@@ -231,5 +232,63 @@ AlignmentMatrix detail::align_unchecked(const LikelihoodBatch& batch, const MasC
 }
 
 }  // namespace reference
+
+namespace io {
+
+namespace {
+std::vector<std::uint32_t> flat(const std::vector<ValidLengths>& lengths) {
+  std::vector<std::uint32_t> v(2 * lengths.size());
+  for (std::size_t b = 0; b < lengths.size(); ++b) {
+    v[2 * b] = lengths[b].text;
+    v[2 * b + 1] = lengths[b].speech;
+  }
+  return v;
+}
+}  // namespace
+
+void write_tensor(const std::filesystem::path& path, const LikelihoodBatch& batch) {
+  const std::vector<std::uint32_t> lens = flat(batch.lengths);
+  mas_error_t err;
+  const int rc = mas_io_write(path.string().c_str(), 0, batch.batch, batch.text_cap,
+                              batch.speech_cap, batch.values.data(), lens.data(), &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+}
+
+void write_tensor(const std::filesystem::path& path, const AlignmentMatrix& m) {
+  const std::vector<std::uint32_t> lens = flat(m.lengths);
+  mas_error_t err;
+  const int rc = mas_io_write(path.string().c_str(), 1, m.batch, m.text_cap, m.speech_cap,
+                              m.values.data(), lens.data(), &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+}
+
+Tensor read_tensor(const std::filesystem::path& path, std::size_t byte_budget) {
+  const std::string p = path.string();
+  mas_error_t err;
+  std::int32_t dtype = 0, has_lengths = 0;
+  std::int64_t dims[3] = {0, 0, 0};
+  int rc = mas_io_read_header(p.c_str(), byte_budget, &dtype, dims, &has_lengths, &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+  const int b = static_cast<int>(dims[0]), t = static_cast<int>(dims[1]),
+            s = static_cast<int>(dims[2]);
+  std::vector<std::uint32_t> lens(2 * static_cast<std::size_t>(b));
+  auto unflat = [&](std::vector<ValidLengths>& out) {
+    for (int i = 0; i < b; ++i) out[static_cast<std::size_t>(i)] = {lens[2 * i], lens[2 * i + 1]};
+  };
+  if (dtype == 0) {
+    LikelihoodBatch batch(b, t, s);
+    rc = mas_io_read(p.c_str(), byte_budget, batch.values.data(), lens.data(), &err);
+    if (rc != MAS_OK) throw_for(rc, err);
+    unflat(batch.lengths);
+    return batch;
+  }
+  AlignmentMatrix m(b, t, s);
+  rc = mas_io_read(p.c_str(), byte_budget, m.values.data(), lens.data(), &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+  unflat(m.lengths);
+  return m;
+}
+
+}  // namespace io
 
 }  // namespace monoalign
