@@ -12,7 +12,10 @@
 #include <vector>
 
 #include "monoalign/align.hpp"
+#include "monoalign/bench.hpp"
 #include "monoalign/tensor_io.hpp"
+
+#include <cuda_runtime.h>
 #include "../../include/monoalign_b200.h"
 
 namespace monoalign {
@@ -232,6 +235,35 @@ AlignmentMatrix detail::align_unchecked(const LikelihoodBatch& batch, const MasC
 }
 
 }  // namespace reference
+
+namespace bench {
+
+LikelihoodBatch generate_random_batch(int b, int t, int s, std::uint64_t seed) {
+  if (b < 1 || t < 1 || s < 1)
+    throw ValidationError(Errc::ZeroDim, "batch dimensions must be at least 1");
+  if (t > s) throw ValidationError(Errc::InfeasibleLengths, "text length t exceeds speech length s");
+  LikelihoodBatch batch(b, t, s);
+  const size_t bytes = batch.values.size() * sizeof(float);
+  float* d = nullptr;
+  cudaStream_t st = cudaStreamPerThread;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), bytes, st);
+  if (e == cudaSuccess &&
+      mas_generate_device(seed, b, t, s, 0, s, d, st) != MAS_OK)
+    e = cudaErrorLaunchFailure;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(batch.values.data(), d, bytes, cudaMemcpyDeviceToHost, st);
+  if (d) cudaFreeAsync(d, st);
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  if (e != cudaSuccess || e2 != cudaSuccess)
+    throw DeviceError(std::string("generate_random_batch: ") +
+                      cudaGetErrorString(e != cudaSuccess ? e : e2));
+  return batch;
+}
+
+const char* engine_name(EngineKind engine) {
+  return engine == EngineKind::Reference ? "reference" : "parallel";
+}
+
+}  // namespace bench
 
 namespace io {
 

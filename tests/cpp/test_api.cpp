@@ -13,6 +13,11 @@
 #include <string>
 
 #include "monoalign/align.hpp"
+#include "monoalign/bench.hpp"
+#include "monoalign/tensor_io.hpp"
+
+#include <filesystem>
+#include <variant>
 
 namespace ma = monoalign;
 
@@ -147,6 +152,44 @@ int main() {
   {
     const ma::PathVector p{0, 0, 1, 2, 2, 3};
     EXPECT(ma::path_from_matrix(ma::matrix_from_path(p, 4, 6), 0) == p);
+  }
+  // bench::generate_random_batch: the counter-addressed splitmix64 stream.
+  {
+    const auto g = ma::bench::generate_random_batch(2, 3, 5, 7);
+    std::uint64_t st = ma::bench::detail::mix_seed(7, 0);
+    bool same = true;
+    for (float v : g.values) {
+      const double u = static_cast<double>(ma::bench::detail::splitmix64(st) >> 11) * 0x1.0p-53;
+      same = same && v == static_cast<float>(-5.0 + 10.0 * u);
+    }
+    EXPECT(same);
+    EXPECT(throws_with([] { ma::bench::generate_random_batch(1, 6, 5, 0); },
+                       ma::Errc::InfeasibleLengths, "text length t exceeds speech length s"));
+  }
+  // io::write_tensor / read_tensor round trip and a budget rejection
+  // (test_io.cpp cases), through include/monoalign/tensor_io.hpp.
+  {
+    const auto path = std::filesystem::temp_directory_path() / "mas_b200_cpp_io.bin";
+    auto batch = ma::bench::generate_random_batch(2, 3, 4, 1);
+    batch.lengths[1] = {2, 3};
+    ma::io::write_tensor(path, batch);
+    const ma::io::Tensor t = ma::io::read_tensor(path);
+    const auto* back = std::get_if<ma::LikelihoodBatch>(&t);
+    EXPECT(back && back->values == batch.values && back->lengths[1].text == 2 &&
+           back->lengths[1].speech == 3);
+    bool rejected = false;
+    try {
+      ma::io::read_tensor(path, 8);
+    } catch (const ma::IoError& e) {
+      rejected = e.code() == ma::Errc::DimensionOverflow;
+    }
+    EXPECT(rejected);
+    const auto m = ma::align(batch);
+    ma::io::write_tensor(path, m);
+    const ma::io::Tensor t2 = ma::io::read_tensor(path);
+    const auto* m2 = std::get_if<ma::AlignmentMatrix>(&t2);
+    EXPECT(m2 && m2->values == m.values);
+    std::filesystem::remove(path);
   }
   if (g_fail) {
     std::fprintf(stderr, "%d expectation(s) failed\n", g_fail);
