@@ -26,6 +26,11 @@
 //   * NonFinite (types.cpp:107-115) folded as max.NaN over |q| (one
 //     3-input FMNMX per two values); the output's zero fill rides along as
 //     TMA stores of a zero tile.
+//
+// Measurement builds (never the default; DESIGN.md 3 quotes their results):
+// MAS_FWD_PROFILE prints per-warp clock64 breakdowns, MAS_FWD_TIMELINE per-CTA
+// globaltimer spans; MAS_ABL_{NOQLDS,NOSHFL,NOBITS,NOFOLD,NOPROBE} remove one
+// part of the per-column work (results are wrong) to price it.
 #include <cstdio>
 #include <mutex>
 
@@ -234,22 +239,15 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
                                          Probes& P) {
   if (GENERIC && K * kQuad >= nvalid) return false;
   const int fs = q & (kFifoSlots - 1);
-#ifndef MAS_ABL_NOFIFO
   if (F.has_in && !ready) mbar_wait_all(F.full + 8u * fs, static_cast<uint32_t>(q / kFifoSlots) & 1u);
-#endif
   const bool next = K + 1 < kQuadsPerStage ? (!GENERIC || (K + 1) * kQuad < nvalid) : more;
   const int q1 = q + 1;
   const uint32_t bar1 = F.full + 8u * (q1 & (kFifoSlots - 1));
-#ifndef MAS_ABL_NOFIFO
   if (lane == 0 && next && F.has_in) mbar_arrive_expect_tx(bar1, kSlot4);
 #ifndef MAS_ABL_NOPROBE
   const bool probe = mbar_test_wait_all(bar1, static_cast<uint32_t>(q1 / kFifoSlots) & 1u);
 #else
-  const bool probe = false;
-#endif
-#else
-  const bool probe = true;
-  (void)bar1;
+  const bool probe = false;  // ablation: always the blocking wait
 #endif
   bool p_stage = false, p_empty = false;
   if (K == 0) {
@@ -425,11 +423,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     // ring's lead.
     const int w = lane;
     const int i0w = band + (crank * W + w) * kRows4;
-#ifndef MAS_ABL_NOFEED
     if (w == W && fed && crank == 0 && s_b > 0 && band < t_b) {
-#else
-    if (false) {
-#endif
       // Band feeder: the band's first warp (warp 0 of rank 0) gets the row
       // above the band, written by the previous band's last warp, through
       // its ordinary FIFO: 64-byte bulk copies completing its "full"
