@@ -384,6 +384,8 @@ for eng in ('parallel', 'reference'):
     ep = o.align(q, lens, engine=eng)[4]
     for b in range({B}):
         assert np.array_equal(gp[b], ep[b, :ls[b]]), (eng, b)
+    gd = m.align_durations(q, lengths=lens, engine=eng)
+    assert np.array_equal(gd, exp.sum(axis=2, dtype=np.int64).astype(np.int32)), eng
 print('OK')
 """
     env = dict(os.environ, MAS_BAND_WARPS="2")
