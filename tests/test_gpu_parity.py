@@ -113,6 +113,28 @@ def test_reference_smoke_suite(mas, cuda):
     assert a.min() >= -5.0 and a.max() <= 5.0
 
 
+def test_reference_smoke_suite_io(mas, cuda, tmp_path):
+    """The reference's test_smoke.py tensor-file cases (:73-103)."""
+    path = str(tmp_path / "batch.bin")
+    rng = np.random.default_rng(11)
+    values = rng.uniform(-5, 5, size=(3, 4, 9)).astype(np.float32)
+    lengths = np.array([[2, 5], [4, 9], [1, 1]], dtype=np.uint32)
+    mas.write_tensor(path, values, lengths=lengths)
+    got_values, got_lengths = mas.read_tensor(path)
+    np.testing.assert_array_equal(got_values, values)
+    np.testing.assert_array_equal(got_lengths, lengths)
+    path = str(tmp_path / "matrix.bin")
+    out = mas.align(np.zeros((2, 3, 5), dtype=np.float32))
+    mas.write_tensor(path, out)
+    got_values, _ = mas.read_tensor(path)
+    assert got_values.dtype == np.uint8
+    np.testing.assert_array_equal(got_values, out)
+    with pytest.raises(OSError):
+        mas.read_tensor(str(tmp_path / "absent.bin"))
+    with pytest.raises(ValueError):
+        mas.write_tensor(str(tmp_path / "bad.bin"), np.zeros((1, 2, 3), dtype=np.int64))
+
+
 @pytest.mark.parametrize("tag", cases("gen_"))
 def test_device_generator_pinned(mas, cuda, tag):
     _, b, t, s, seed = tag.split("_")
