@@ -837,7 +837,17 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
   // of chunk c+1 runs while chunk c computes and copies its alignment back
   // (PCIe is full duplex): the call costs about one pass over the input on
   // the bus instead of input + output + compute in sequence.
-  const int nchunk = std::min(batch, 4);
+  // Chunks of at least ~8 MB of input (launch costs stay small), up to one
+  // item each: the finer the chunks, the shorter the un-overlapped head
+  // (first H2D) and tail (last compute + D2H).  B32 T1024 S8192: 32 chunks,
+  // 13.1 Gcells/s vs 12.2 with 4 (PCIe-bound either way).
+  static const int chunk_env = [] {
+    const char* e = std::getenv("MAS_HOST_CHUNKS");  // experiment override
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  const int64_t in_bytes = static_cast<int64_t>(batch) * text_cap * speech_cap * 4;
+  const int by_size = static_cast<int>(std::max<int64_t>(1, in_bytes / (8ll << 20)));
+  const int nchunk = std::min(batch, chunk_env > 0 ? chunk_env : std::min(by_size, 64));
   const int per = (batch + nchunk - 1) / nchunk;
   cudaStream_t st[2] = {nullptr, nullptr};
   float* d_q = nullptr;
