@@ -312,6 +312,22 @@ def run_ours(args):
     for _ in range(e2e_steps):
         host_dur_call()
     e2e_dur_s = time.perf_counter() - t0
+    # ---- the reference binding's own path: numpy (pageable) in, numpy out
+    import numpy as np
+
+    q_np = np.array(hq.numpy(), copy=True)  # pageable, like monoalign.align(values)
+    mas.align(q_np)
+    t0 = time.perf_counter()
+    np_steps = 3
+    for _ in range(np_steps):
+        out_np = mas.align(q_np)
+    np_s = (time.perf_counter() - t0) / np_steps
+    assert np.array_equal(out_np, hout.numpy()), "numpy path differs from the device path"
+    del q_np, out_np
+    numpy_line = {"value": round(world * cells / np_s / 1e9, 3), "unit": "Gcells/s",
+                  "ms_per_step": round(np_s * 1e3, 2),
+                  "path": "paper_2409_07704_b200.align(numpy float32 [B,T,S]) -> numpy uint8, "
+                          "pageable host memory (the reference binding's call)"}
     durations_line = {
         "value": round(world * cells / (dur_ms / 1e3) / 1e9, 2), "unit": "Gcells/s",
         "ms_per_step": round(dur_ms, 4), "bytes_per_cell": 4.125,
@@ -365,7 +381,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "path": "mas_align_host (C-ABI), pinned host in/out, H2D+kernels+D2H+checks"},
         "gpu_launches": K * launches_per_step,
-        "variants": {"durations_only": durations_line},
+        "variants": {"durations_only": durations_line, "numpy_e2e": numpy_line},
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
     }

@@ -12,7 +12,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <atomic>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <new>
 #include <sstream>
 #include <string>
@@ -808,6 +811,136 @@ int mas_align_device_ex(const float* d_values, int64_t row_pitch, int32_t batch,
 
 namespace {
 
+// ---- pageable host buffers --------------------------------------------
+// A numpy array (the reference binding's input) is pageable memory, which
+// the copy engines only reach through the driver's small bounce buffers.
+// Such calls stage every chunk through pinned buffers instead: host threads
+// copy the chunk into a pinned slot while the copy engine moves the previous
+// one, and the alignment comes back the same way.
+
+bool is_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Fixed pool of host copy threads; copy() splits one memcpy over them.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  void copy(void* dst, const void* src, size_t bytes) {
+    if (bytes < (4u << 20) || workers_.empty()) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    std::lock_guard<std::mutex> one_job(job_mu_);  // one parallel copy at a time
+    const size_t parts = workers_.size() + 1;
+    const size_t chunk = ((bytes + parts - 1) / parts + 63) & ~size_t(63);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      dst_ = static_cast<char*>(dst);
+      src_ = static_cast<const char*>(src);
+      bytes_ = bytes;
+      chunk_ = chunk;
+      next_.store(0);
+      pending_ = parts;
+      ++gen_;
+    }
+    cv_.notify_all();
+    run_parts();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  CopyPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const unsigned n = std::min(15u, hw > 1 ? hw - 1 : 0u);
+    for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void run_parts() {
+    while (true) {
+      const size_t i = next_.fetch_add(1);
+      const size_t off = i * chunk_;
+      if (off < bytes_) std::memcpy(dst_ + off, src_ + off, std::min(chunk_, bytes_ - off));
+      if (off >= bytes_) break;
+    }
+    std::lock_guard<std::mutex> lk(mu_);
+    if (--pending_ == 0) done_cv_.notify_all();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    while (true) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      run_parts();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex job_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t bytes_ = 0, chunk_ = 0, pending_ = 0;
+  std::atomic<size_t> next_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// Pinned buffers kept for reuse across calls (pinning costs milliseconds).
+class PinnedPool {
+ public:
+  static PinnedPool& get() {
+    static PinnedPool pool;
+    return pool;
+  }
+  void* take(size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (size_t i = 0; i < free_.size(); ++i)
+      if (free_[i].second >= bytes) {
+        void* p = free_[i].first;
+        free_.erase(free_.begin() + static_cast<long>(i));
+        return p;
+      }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    sizes_.push_back({p, bytes});
+    return p;
+  }
+  void give(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(mu_);
+    for (const auto& e : sizes_)
+      if (e.first == p) free_.push_back(e);
+  }
+
+ private:
+  std::mutex mu_;
+  std::vector<std::pair<void*, size_t>> free_, sizes_;
+};
+
 int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_t speech_cap,
                     const uint32_t* lengths, const mas_config_t* cfg, uint8_t* out,
                     int32_t* paths, int32_t* durations, int item_base, mas_error_t* err) {
@@ -849,6 +982,24 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
   const int by_size = static_cast<int>(std::max<int64_t>(1, in_bytes / (8ll << 20)));
   const int nchunk = std::min(batch, chunk_env > 0 ? chunk_env : std::min(by_size, 64));
   const int per = (batch + nchunk - 1) / nchunk;
+  // Pageable input / output: stage through pinned slots (two each).
+  const size_t in_chunk = static_cast<size_t>(per) * o_item * sizeof(float);
+  const size_t out_chunk = static_cast<size_t>(per) * o_item;
+  const bool stage_in = nchunk > 1 && !is_pinned(values);
+  const bool stage_out = nchunk > 1 && out && !is_pinned(out);
+  void* pin_in[2] = {nullptr, nullptr};
+  void* pin_out[2] = {nullptr, nullptr};
+  cudaEvent_t in_done[2] = {nullptr, nullptr}, out_done[2] = {nullptr, nullptr};
+  bool staged = true;
+  for (int k = 0; k < 2 && staged; ++k) {
+    if (stage_in) staged = (pin_in[k] = PinnedPool::get().take(in_chunk)) != nullptr &&
+                           cudaEventCreateWithFlags(&in_done[k], cudaEventDisableTiming) ==
+                               cudaSuccess;
+    if (stage_out && staged)
+      staged = (pin_out[k] = PinnedPool::get().take(out_chunk)) != nullptr &&
+               cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming) == cudaSuccess;
+  }
+  const bool use_in = stage_in && staged, use_out = stage_out && staged;
   cudaStream_t st[2] = {nullptr, nullptr};
   float* d_q = nullptr;
   uint8_t* d_out = nullptr;
@@ -877,33 +1028,56 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
     const int nb = std::min(per, batch - b0);
     if (nb <= 0) break;
     cudaStream_t s = st[c & 1];
-    for (int b = b0; b < b0 + nb && e == cudaSuccess; ++b)
-      e = cudaMemcpy2DAsync(d_q + b * q_item, pitch * 4, values + b * o_item,
+    const float* src = values + b0 * o_item;
+    if (use_in) {
+      // the slot's previous chunk (c - 2) must have left it
+      if (c >= 2 && (e = cudaEventSynchronize(in_done[c & 1])) != cudaSuccess) {
+        rc = cuda_error(err, e, "host staging");
+        break;
+      }
+      CopyPool::get().copy(pin_in[c & 1], src, static_cast<size_t>(nb) * o_item * sizeof(float));
+      src = static_cast<const float*>(pin_in[c & 1]);
+    }
+    for (int b = 0; b < nb && e == cudaSuccess; ++b)
+      e = cudaMemcpy2DAsync(d_q + (b0 + b) * q_item, pitch * 4, src + b * o_item,
                             static_cast<size_t>(speech_cap) * 4,
                             static_cast<size_t>(speech_cap) * 4, text_cap, cudaMemcpyHostToDevice,
                             s);
+    if (use_in && e == cudaSuccess) e = cudaEventRecord(in_done[c & 1], s);
     if (e != cudaSuccess) {
       rc = cuda_error(err, e, "host->device staging");
       break;
     }
     rc = enqueue_items(plan, MAS_PART_ALL, b0, nb, d_q, d_out, d_paths, d_dur, s, err);
     if (rc != MAS_OK) break;
-    if (out &&
-        (e = cudaMemcpyAsync(out + b0 * o_item, d_out + b0 * o_item, nb * o_item,
-                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    if (out && use_out) {
+      // slot c & 1 held chunk c - 2, copied out at iteration c - 1
+      if ((e = cudaMemcpyAsync(pin_out[c & 1], d_out + b0 * o_item, nb * o_item,
+                               cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+          (e = cudaEventRecord(out_done[c & 1], s)) != cudaSuccess)
+        rc = cuda_error(err, e, "device->host out");
+    } else if (out &&
+               (e = cudaMemcpyAsync(out + b0 * o_item, d_out + b0 * o_item, nb * o_item,
+                                    cudaMemcpyDeviceToHost, s)) != cudaSuccess) {
       rc = cuda_error(err, e, "device->host out");
-    if (rc == MAS_OK && paths &&
-        (e = cudaMemcpyAsync(paths + static_cast<size_t>(b0) * speech_cap,
-                             d_paths + static_cast<size_t>(b0) * speech_cap,
-                             static_cast<size_t>(nb) * speech_cap * sizeof(int32_t),
-                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-      rc = cuda_error(err, e, "device->host paths");
-    if (rc == MAS_OK && durations &&
-        (e = cudaMemcpyAsync(durations + static_cast<size_t>(b0) * text_cap,
-                             d_dur + static_cast<size_t>(b0) * text_cap,
-                             static_cast<size_t>(nb) * text_cap * sizeof(int32_t),
-                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-      rc = cuda_error(err, e, "device->host durations");
+    }
+    // the previous chunk's alignment: from its pinned slot to the caller
+    if (rc == MAS_OK && use_out && c >= 1) {
+      const int pb0 = (c - 1) * per, pnb = std::min(per, batch - pb0);
+      if ((e = cudaEventSynchronize(out_done[(c - 1) & 1])) != cudaSuccess)
+        rc = cuda_error(err, e, "device->host out");
+      else
+        CopyPool::get().copy(out + pb0 * o_item, pin_out[(c - 1) & 1], pnb * o_item);
+    }
+
+  }
+  if (rc == MAS_OK && use_out) {  // the last chunk's alignment
+    const int c = (batch + per - 1) / per - 1;
+    const int pb0 = c * per, pnb = std::min(per, batch - pb0);
+    if ((e = cudaEventSynchronize(out_done[c & 1])) != cudaSuccess)
+      rc = cuda_error(err, e, "device->host out");
+    else
+      CopyPool::get().copy(out + pb0 * o_item, pin_out[c & 1], pnb * o_item);
   }
   // Join the second stream into the first; the NonFinite check and the
   // frees follow on st[0].
@@ -911,6 +1085,16 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
     cudaEventRecord(ready, st[1]);
     cudaStreamWaitEvent(st[0], ready, 0);
   }
+  // paths and durations are small: one copy each after the last chunk (a
+  // per-chunk copy into pageable memory would serialise the pipeline)
+  if (rc == MAS_OK && paths &&
+      (e = cudaMemcpyAsync(paths, d_paths, static_cast<size_t>(batch) * speech_cap * sizeof(int32_t),
+                           cudaMemcpyDeviceToHost, st[0])) != cudaSuccess)
+    rc = cuda_error(err, e, "device->host paths");
+  if (rc == MAS_OK && durations &&
+      (e = cudaMemcpyAsync(durations, d_dur, static_cast<size_t>(batch) * text_cap * sizeof(int32_t),
+                           cudaMemcpyDeviceToHost, st[0])) != cudaSuccess)
+    rc = cuda_error(err, e, "device->host durations");
   if (rc == MAS_OK) rc = mas_plan_finish(plan, d_q, st[0], err);
   if (d_q) cudaFreeAsync(d_q, st[0]);
   if (d_out) cudaFreeAsync(d_out, st[0]);
@@ -918,8 +1102,13 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
   if (d_dur) cudaFreeAsync(d_dur, st[0]);
   if (st[0]) cudaStreamSynchronize(st[0]);
   if (ready) cudaEventDestroy(ready);
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < 2; ++k) {
     if (st[k]) cudaStreamDestroy(st[k]);
+    if (in_done[k]) cudaEventDestroy(in_done[k]);
+    if (out_done[k]) cudaEventDestroy(out_done[k]);
+    PinnedPool::get().give(pin_in[k]);
+    PinnedPool::get().give(pin_out[k]);
+  }
   mas_plan_destroy(plan);
   return rc;
 }
