@@ -375,6 +375,12 @@ struct mas_plan {
   int device = 0;
   int bt_rows = 64;       // backtrack window rows
   float* d_bnd = nullptr; // bands: [B][bands-1][bnd_pitch] boundary rows
+  // tensor maps of the last input / output buffers enqueued (reused)
+  CUtensorMap tm_in, tm_out;
+  const float* tm_in_ptr = nullptr;
+  int64_t tm_in_pitch = 0;
+  int tm_in_tpad = 0;
+  const uint8_t* tm_out_ptr = nullptr;
   int* d_sync = nullptr;  // bands: tickets [B] (one per launch, at its first item) +
                           //        progress [B][bands-1]
   int bnd_pitch = 0;
@@ -578,11 +584,23 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
   if (parts & MAS_PART_FORWARD) {
     CUtensorMap tm0, tm1;
     const bool r4 = !g.legacy;
-    if (r4 ? !encode_map4(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, g.R,
-                          &tm0)
-           : !encode_maps(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, &tm0,
-                          &tm1))
+    // Tensor maps depend only on the buffers and the plan's layout: encoded
+    // once per input pointer and reused by later enqueues (host cost).
+    const bool reuse_in = r4 && p->tm_in_ptr == d_values && p->tm_in_pitch == p->pitch &&
+                          p->tm_in_tpad == p->T_pad;
+    if (reuse_in) {
+      tm0 = p->tm_in;
+    } else if (r4 ? !encode_map4(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S,
+                                 g.R, &tm0)
+                  : !encode_maps(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S,
+                                 &tm0, &tm1)) {
       return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled failed");
+    } else if (r4) {
+      p->tm_in = tm0;
+      p->tm_in_ptr = d_values;
+      p->tm_in_pitch = p->pitch;
+      p->tm_in_tpad = p->T_pad;
+    }
     MAS_CUDA(cudaMemsetAsync(p->d_flags + b0, 0, sizeof(int) * nb, stream),
              "cudaMemsetAsync(flags)");
     mas::FwdArgs fa;
@@ -631,11 +649,17 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     }
     CUtensorMap tm_out;
     std::memset(&tm_out, 0, sizeof(tm_out));
-    if (fused_zero && !(r4 ? encode_out_map4(d_out, static_cast<int64_t>(p->B) * p->T, p->S, g.R,
+    if (fused_zero && r4 && p->tm_out_ptr == d_out) {
+      tm_out = p->tm_out;
+    } else if (fused_zero && !(r4 ? encode_out_map4(d_out, static_cast<int64_t>(p->B) * p->T, p->S, g.R,
                                              &tm_out)
                            : encode_out_map(d_out, static_cast<int64_t>(p->B) * p->T, p->S,
                                             &tm_out)))
       return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled(out) failed");
+    else if (fused_zero && r4 && p->tm_out_ptr != d_out) {
+      p->tm_out = tm_out;
+      p->tm_out_ptr = d_out;
+    }
     fa.zero_fill = fused_zero ? 1 : 0;
     static const int l2_ahead = [] {
       const char* e = std::getenv("MAS_L2_AHEAD");  // experiment override
