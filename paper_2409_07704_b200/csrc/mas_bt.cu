@@ -241,17 +241,28 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
           // once x has no bit it stays 0, and an exit at the pair's position
           // 0 (bit 63) is recorded and leaves x = 0.  So four steps run
           // without a branch, and the row reached is y - popc(exits).
-#define MAS_BT_STEP(Q, OFF)                    \
+#define MAS_BT_STEP(Q, OFF, PAIR)              \
   {                                            \
     const uint64_t d = x - 1u;                 \
     exw |= x & ~d;                             \
     x = (Q) & ~(x ^ d);                        \
-    (Q) = ld64(pb - (OFF), pair);              \
+    (Q) = ld64(pb - (OFF), PAIR);              \
   }
-          while (true) {
-            MAS_BT_STEP(q1, 20u) MAS_BT_STEP(q2, 24u) MAS_BT_STEP(q3, 28u) MAS_BT_STEP(q4, 32u)
-            pb -= 16u;
-            if ((x & 0x7fffffffffffffffull) == 0u) break;
+          // (the common paired case runs with unconditional loads)
+          if (pair) {
+            while (true) {
+              MAS_BT_STEP(q1, 20u, true) MAS_BT_STEP(q2, 24u, true) MAS_BT_STEP(q3, 28u, true)
+              MAS_BT_STEP(q4, 32u, true)
+              pb -= 16u;
+              if ((x & 0x7fffffffffffffffull) == 0u) break;
+            }
+          } else {
+            while (true) {
+              MAS_BT_STEP(q1, 20u, false) MAS_BT_STEP(q2, 24u, false)
+              MAS_BT_STEP(q3, 28u, false) MAS_BT_STEP(q4, 32u, false)
+              pb -= 16u;
+              if ((x & 0x7fffffffffffffffull) == 0u) break;
+            }
           }
 #undef MAS_BT_STEP
           exw |= x;  // a pending exit at the pair's position 0
