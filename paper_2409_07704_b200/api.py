@@ -90,9 +90,26 @@ def _ptr(a, attr):
     return None if a is None else getattr(a, attr)
 
 
+def _host_array(shape, dtype):
+    """A numpy array in page-locked memory when it is large (the copy engine
+    then writes it directly instead of through staging buffers); the pinned
+    block comes from torch's caching host allocator and lives as long as the
+    array."""
+    nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    if nbytes >= (64 << 20):
+        try:
+            import torch
+
+            tdt = {np.uint8: torch.uint8, np.int32: torch.int32}[dtype]
+            return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+        except Exception:  # no CUDA host allocator available: plain memory
+            pass
+    return np.empty(shape, dtype)
+
+
 def _run_host(values, lens, cfg, b, t, s, want_out, want_paths, want_dur=False):
     lib = _lib.load()
-    out = np.empty((b, t, s), np.uint8) if want_out else None
+    out = _host_array((b, t, s), np.uint8) if want_out else None
     paths = np.empty((b, s), np.int32) if want_paths else None
     dur = np.empty((b, t), np.int32) if want_dur else None
     err = _lib.MasError()
