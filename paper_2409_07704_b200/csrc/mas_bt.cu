@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
     uint32_t ph_full = 0, ph_free = 0, pend = 0;
 #ifdef MAS_BT_PROFILE
     long long pr_t0 = clock64(), pr_free = 0, pr_full = 0, pr_recenter = 0, pr_words = 0;
+    long long pr_inner = 0;
     __shared__ unsigned pr_ts[300];
     __shared__ unsigned char pr_ex[300];
 #define PR_T(v) long long v = clock64()
@@ -249,6 +250,9 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
     (Q) = ld64(pb - (OFF), PAIR);              \
   }
           // (the common paired case runs with unconditional loads)
+#ifdef MAS_BT_PROFILE
+          const long long pr_in0 = clock64();
+#endif
           if (pair) {
             while (true) {
               MAS_BT_STEP(q1, 20u, true) MAS_BT_STEP(q2, 24u, true) MAS_BT_STEP(q3, 28u, true)
@@ -265,6 +269,9 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
             }
           }
 #undef MAS_BT_STEP
+#ifdef MAS_BT_PROFILE
+          pr_inner += clock64() - pr_in0;
+#endif
           exw |= x;  // a pending exit at the pair's position 0
           const int ex_lo = __popc(static_cast<uint32_t>(exw));
           const int ex = ex_lo + __popc(static_cast<uint32_t>(exw >> 32));
@@ -309,8 +316,8 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
       if (pend & (1u << k)) mbar_wait(full_s + 8u * k, (ph_full >> k) & 1u);
 #ifdef MAS_BT_PROFILE
     if (b < 2) {
-      printf("bt item %d: total %lld cyc, wait free %lld, wait full %lld, recenters %lld, words %lld\n",
-             b, clock64() - pr_t0, pr_free, pr_full, pr_recenter, pr_words);
+      printf("bt item %d: total %lld cyc, wait free %lld, wait full %lld, recenters %lld, words %lld, inner %lld\n",
+             b, clock64() - pr_t0, pr_free, pr_full, pr_recenter, pr_words, pr_inner);
       if (b == 0)
         for (int i = 1; i < 300 && i < pr_words; ++i)
           printf("word %d t=%u dt=%u ex=%d\n", i, pr_ts[i], pr_ts[i] - pr_ts[i - 1], pr_ex[i]);
