@@ -29,8 +29,12 @@ namespace mas {
 
 namespace {
 
-constexpr int kBtStages = 4;   // ring depth (stages of direction words in flight)
-constexpr int kBtWords = 8;    // direction words per stage = 256 speech positions
+#ifndef MAS_BT_WORDS
+#define MAS_BT_WORDS 8
+#endif
+constexpr int kBtWords = MAS_BT_WORDS;          // direction words per stage (32 columns each)
+constexpr int kBtStages = 32 / MAS_BT_WORDS;    // ring depth (stages of direction words in flight)
+constexpr int kBtCols = 32 * kBtWords;          // speech positions per stage
 constexpr int kBtMaxRows = 256;  // rows per window (TMA box limit)
 
 // Window load of stage n: words [8n, 8n + 8) (those < M) of rows
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
       for (int j = threadIdx.x; j < a.S_cap; j += 64) path[j] = -1;
     return;
   }
-  const int n_top = (s - 1) >> 8;
+  const int n_top = (s - 1) / kBtCols;
 
   const uint32_t* dirs = a.dirs + static_cast<size_t>(b) * M * T_alloc;
   if (warp == 0) {
@@ -365,7 +369,7 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
     }
 #pragma unroll
     for (int i = 0; i < kBtWords; ++i) {
-      const int j = 256 * n + 32 * i + lane - 1;
+      const int j = kBtCols * n + 32 * i + lane - 1;
       const bool valid = j >= 0 && j <= s - 2;
       // exits at positions >= lane are bits <= 31 - lane
       const int row = valid ? ry[i] - __popc(rx[i] << lane) : -1;
