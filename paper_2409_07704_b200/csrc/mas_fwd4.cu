@@ -54,6 +54,10 @@ constexpr int kChunks = kSC / kCols4;   // chunks (direction words per row) per 
 // a quarter of the scattered 32-byte writes a per-stage box would make).
 constexpr int kZCols = kZeroCols;
 constexpr int kZStages = kZCols / kSC;
+#ifndef MAS_BAND_PUB
+#define MAS_BAND_PUB 4
+#endif
+constexpr int kBandPub = MAS_BAND_PUB;  // quads per band-progress publication
 __host__ __device__ constexpr int rows_of(int R) { return 32 * R; }
 __host__ __device__ constexpr int chunk_bytes(int R) { return rows_of(R) * kCols4 * 4; }
 __host__ __device__ constexpr int stage_bytes(int R) { return chunk_bytes(R) * kChunks; }
@@ -445,7 +449,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
           const int fs = qq & (kFifoSlots - 1);
           while (avail <= qq) {
             avail = ld_acquire_gpu(prog);
-            if (avail <= qq) __nanosleep(256);
+            if (avail <= qq) __nanosleep(128);
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");
           asm volatile(
@@ -482,7 +486,9 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
         float4* gp = reinterpret_cast<float4*>(dst + q * kQuad);
 #pragma unroll
         for (int q4 = 0; q4 < kQuad / 4; ++q4) gp[q4] = sp[q4];
-        st_release_gpu(prog, q + 1);
+        // publish every kBandPub quads: a release at GPU scope waits for the
+        // stores to be performed (~1 us), longer than a quad takes to compute
+        if ((q + 1) % kBandPub == 0 || q + 1 == nq) st_release_gpu(prog, q + 1);
         if ((q + 1) % kQuadsPerStage == 0 || q + 1 == nq) {
           const int m = q / kQuadsPerStage;
           st_async_b32(lsink, static_cast<uint32_t>(m),
