@@ -316,7 +316,8 @@ def run_ours(args):
     import numpy as np
 
     q_np = np.array(hq.numpy(), copy=True)  # pageable, like monoalign.align(values)
-    mas.align(q_np)
+    for _ in range(2):  # steady state: the pinned output blocks are cached after two calls
+        out_np = mas.align(q_np)
     t0 = time.perf_counter()
     np_steps = 3
     for _ in range(np_steps):
