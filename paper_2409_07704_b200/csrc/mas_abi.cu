@@ -16,6 +16,8 @@
 #include <condition_variable>
 #include <mutex>
 #include <thread>
+
+#include <unistd.h>
 #include <new>
 #include <sstream>
 #include <string>
@@ -860,7 +862,8 @@ class CopyPool {
     return pool;
   }
   void copy(void* dst, const void* src, size_t bytes) {
-    if (bytes < (4u << 20) || workers_.empty()) {
+    // (a forked child inherits this object but not its threads)
+    if (bytes < (4u << 20) || workers_.empty() || getpid() != owner_) {
       std::memcpy(dst, src, bytes);
       return;
     }
@@ -884,7 +887,7 @@ class CopyPool {
   }
 
  private:
-  CopyPool() {
+  CopyPool() : owner_(getpid()) {
     const unsigned hw = std::thread::hardware_concurrency();
     const unsigned n = std::min(15u, hw > 1 ? hw - 1 : 0u);
     for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
@@ -928,6 +931,7 @@ class CopyPool {
   std::atomic<size_t> next_{0};
   uint64_t gen_ = 0;
   bool stop_ = false;
+  pid_t owner_;
 };
 
 // Pinned buffers kept for reuse across calls (pinning costs milliseconds).
