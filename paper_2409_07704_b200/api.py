@@ -96,7 +96,7 @@ def _host_array(shape, dtype):
     block comes from torch's caching host allocator and lives as long as the
     array."""
     nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
-    if nbytes >= (64 << 20):
+    if nbytes >= (1 << 20):
         try:
             import torch
 
