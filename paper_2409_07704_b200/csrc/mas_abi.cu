@@ -969,6 +969,26 @@ class PinnedPool {
   std::vector<std::pair<void*, size_t>> free_, sizes_;
 };
 
+// Two non-blocking streams and a join event per (host thread, device),
+// created once: stream creation and destruction are a visible part of a
+// small call's latency.
+struct HostStreams {
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t ready = nullptr;
+};
+cudaError_t host_streams(int dev, HostStreams** out) {
+  constexpr int kMaxDevices = 64;
+  thread_local HostStreams cache[kMaxDevices];
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  HostStreams& h = cache[dev];
+  cudaError_t e = cudaSuccess;
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k)
+    if (!h.st[k]) e = cudaStreamCreateWithFlags(&h.st[k], cudaStreamNonBlocking);
+  if (e == cudaSuccess && !h.ready) e = cudaEventCreateWithFlags(&h.ready, cudaEventDisableTiming);
+  *out = &h;
+  return e;
+}
+
 int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_t speech_cap,
                     const uint32_t* lengths, const mas_config_t* cfg, uint8_t* out,
                     int32_t* paths, int32_t* durations, int item_base, mas_error_t* err) {
@@ -1037,8 +1057,12 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
   int32_t* d_paths = nullptr;
   int32_t* d_dur = nullptr;
   cudaError_t e = cudaSuccess;
-  for (int k = 0; k < 2 && e == cudaSuccess; ++k)
-    e = cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
+  HostStreams* hs = nullptr;
+  e = host_streams(plan->device, &hs);
+  if (e == cudaSuccess) {
+    st[0] = hs->st[0];
+    st[1] = hs->st[1];
+  }
   if (e == cudaSuccess)
     e = cudaMallocAsync(reinterpret_cast<void**>(&d_q), batch * q_item * sizeof(float), st[0]);
   if (e == cudaSuccess && out)
@@ -1049,8 +1073,7 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
   if (e == cudaSuccess && durations)
     e = cudaMallocAsync(reinterpret_cast<void**>(&d_dur),
                         static_cast<size_t>(batch) * text_cap * sizeof(int32_t), st[0]);
-  cudaEvent_t ready = nullptr;
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  cudaEvent_t ready = hs ? hs->ready : nullptr;
   if (e == cudaSuccess) e = cudaEventRecord(ready, st[0]);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(st[1], ready, 0);
   if (e != cudaSuccess) rc = cuda_error(err, e, "host path setup");
@@ -1132,9 +1155,7 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
   if (d_paths) cudaFreeAsync(d_paths, st[0]);
   if (d_dur) cudaFreeAsync(d_dur, st[0]);
   if (st[0]) cudaStreamSynchronize(st[0]);
-  if (ready) cudaEventDestroy(ready);
   for (int k = 0; k < 2; ++k) {
-    if (st[k]) cudaStreamDestroy(st[k]);
     if (in_done[k]) cudaEventDestroy(in_done[k]);
     if (out_done[k]) cudaEventDestroy(out_done[k]);
     PinnedPool::get().give(pin_in[k]);
