@@ -377,6 +377,7 @@ struct mas_plan {
   int device = 0;
   int bt_rows = 64;       // backtrack window rows
   float* d_bnd = nullptr; // bands: [B][bands-1][bnd_pitch] boundary rows
+  cudaEvent_t ws_ready = nullptr;  // deferred plans: workspace set-up recorded here
   // tensor maps of the last input / output buffers enqueued (reused)
   CUtensorMap tm_in, tm_out;
   const float* tm_in_ptr = nullptr;
@@ -423,6 +424,7 @@ void mas_plan_destroy(mas_plan_t* p) {
   cudaFreeAsync(p->d_locate, st);
   if (p->d_bnd) cudaFreeAsync(p->d_bnd, st);
   if (p->d_sync) cudaFreeAsync(p->d_sync, st);
+  if (p->ws_ready) cudaEventDestroy(p->ws_ready);
   cudaSetDevice(prev);
   delete p;
 }
@@ -432,7 +434,7 @@ void mas_plan_destroy(mas_plan_t* p) {
 namespace {
 int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row_pitch,
                 const uint32_t* lengths, const mas_config_t* cfg_in, int item_base,
-                mas_plan_t** plan_out, mas_error_t* err);
+                mas_plan_t** plan_out, mas_error_t* err, bool deferred = false);
 }  // namespace
 
 extern "C" {
@@ -447,9 +449,12 @@ int mas_plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t
 
 namespace {
 
+// deferred: the workspace set-up is ordered before the plan's first
+// enqueue by an event instead of a host synchronisation (internal plans of
+// mas_align_host / _device, whose enqueues are never captured).
 int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row_pitch,
                 const uint32_t* lengths, const mas_config_t* cfg_in, int item_base,
-                mas_plan_t** plan_out, mas_error_t* err) {
+                mas_plan_t** plan_out, mas_error_t* err, bool deferred) {
   clear_error(err);
   *plan_out = nullptr;
   mas_config_t cfg;
@@ -547,7 +552,13 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
   if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_locate), sizeof(unsigned long long),
                            st)) != cudaSuccess)
     return fail(e, "cudaMallocAsync(locate)");
-  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail(e, "plan workspace");
+  if (deferred) {
+    if ((e = cudaEventCreateWithFlags(&p->ws_ready, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventRecord(p->ws_ready, st)) != cudaSuccess)
+      return fail(e, "plan workspace");
+  } else if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
+    return fail(e, "plan workspace");
+  }
   *plan_out = p;
   return MAS_OK;
 }
@@ -582,6 +593,7 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
                      "device layout needs a 16-byte base, pitch % 4 == 0 and text_cap % 4 == 0");
   const Geometry& g = p->geo;
+  if (p->ws_ready) MAS_CUDA(cudaStreamWaitEvent(stream, p->ws_ready, 0), "workspace wait");
   int nfwd = 0, nbt = 0;
   if (parts & MAS_PART_FORWARD) {
     CUtensorMap tm0, tm1;
@@ -742,7 +754,8 @@ int mas_plan_enqueue_ex(mas_plan_t* p, uint32_t parts, const float* d_values, ui
 int mas_plan_finish(mas_plan_t* p, const float* d_values, void* stream_v, mas_error_t* err) {
   clear_error(err);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
-  MAS_CUDA(cudaStreamSynchronize(stream), "kernel execution");
+  // (a device-to-pageable copy returns once the stream's earlier work and
+  // the copy are done: one host round trip)
   std::vector<int> flags(p->B);
   MAS_CUDA(cudaMemcpyAsync(flags.data(), p->d_flags, sizeof(int) * p->B, cudaMemcpyDeviceToHost,
                            stream),
@@ -794,7 +807,7 @@ int mas_align_device_ex(const float* d_values, int64_t row_pitch, int32_t batch,
   clear_error(err);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   mas_plan_t* plan = nullptr;
-  int rc = mas_plan_create(batch, text_cap, speech_cap, row_pitch, lengths, cfg, &plan, err);
+  int rc = plan_create(batch, text_cap, speech_cap, row_pitch, lengths, cfg, 0, &plan, err, true);
   if (rc) return rc;
   plan->internal = true;
   const float* q = d_values;
@@ -1009,7 +1022,8 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
   const size_t q_item = static_cast<size_t>(T_pad) * pitch;  // floats per item on the device
   const size_t o_item = static_cast<size_t>(text_cap) * speech_cap;
   mas_plan_t* plan = nullptr;
-  int rc = plan_create(batch, text_cap, speech_cap, pitch, lengths, cfg, item_base, &plan, err);
+  int rc = plan_create(batch, text_cap, speech_cap, pitch, lengths, cfg, item_base, &plan, err,
+                       true);
   if (rc) return rc;
   plan->internal = true;
   plan->T_pad = T_pad;
