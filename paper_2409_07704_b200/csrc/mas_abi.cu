@@ -305,6 +305,34 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
   return true;
 }
 
+// choose_geometry queries the occupancy API for every candidate (tens of
+// microseconds per call); plans of the same shape on the same device reuse
+// the answer.
+bool cached_geometry(int B, int t_max, int S_cap, Geometry* g) {
+  struct Entry {
+    int dev, B, t, S;
+    Geometry g;
+    bool ok;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Entry& e : cache)
+      if (e.dev == dev && e.B == B && e.t == t_max && e.S == S_cap) {
+        *g = e.g;
+        return e.ok;
+      }
+  }
+  const bool ok = choose_geometry(B, t_max, S_cap, g);
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() >= 256) cache.erase(cache.begin());
+  cache.push_back({dev, B, t_max, S_cap, *g, ok});
+  return ok;
+}
+
 // The input [B*T_pad][pitch] as a 3-D tensor {columns, row groups of R,
 // row residue mod R}: one {32, 32, R} box is a 32R-row x 32-column stage of
 // mas_fwd4.cu laid out [residue][group][column] (128-byte swizzle).
@@ -503,7 +531,7 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
     delete p;
     return set_error(err, MAS_E_CUDA, -1, -1, "forward kernel configuration failed");
   }
-  if (!choose_geometry(batch, std::max(t_max, 1), speech_cap, &p->geo)) {
+  if (!cached_geometry(batch, std::max(t_max, 1), speech_cap, &p->geo)) {
     delete p;
     return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
                      "text length above 8192 rows is not supported by the device path");
