@@ -643,8 +643,9 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
       p->tm_in_pitch = p->pitch;
       p->tm_in_tpad = p->T_pad;
     }
-    MAS_CUDA(cudaMemsetAsync(p->d_flags + b0, 0, sizeof(int) * nb, stream),
-             "cudaMemsetAsync(flags)");
+    if (!r4)  // mas_fwd4 zeroes each item's flag itself
+      MAS_CUDA(cudaMemsetAsync(p->d_flags + b0, 0, sizeof(int) * nb, stream),
+               "cudaMemsetAsync(flags)");
     mas::FwdArgs fa;
     fa.b0 = b0;
     fa.lengths = p->d_lengths;

@@ -411,6 +411,10 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
         mbar_init(base + SL.full + static_cast<uint32_t>((W * kFifoSlots + s) * 8), 1u);
     }
   }
+  // the item's NonFinite flag starts at 0 (set by atomicOr only after the
+  // cluster barrier below, and in the bands below after this band's
+  // progress releases)
+  if (band_idx == 0 && crank == 0 && threadIdx.x == 0) a.flags[b] = 0;
   fence_proxy_async_smem();
   fence_mbar_init();
   cluster_sync_all();  // every CTA's FIFO / stage barriers exist before any use
