@@ -138,11 +138,12 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
 #ifndef MAS_BT_NO_PDL
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-  // Durations (row sums of the alignment): zeroed here, accumulated by the
-  // expander below one run of equal rows per word at a time.
+  // Durations (row sums of the alignment): the buffer first holds each
+  // row's last column (-1 = before column 0), written by the expander at the
+  // walk's exits, and is turned into differences at the end.
   int32_t* dur = a.dur ? a.dur + static_cast<size_t>(b) * a.T_cap : nullptr;
   if (dur) {
-    for (int i = threadIdx.x; i < a.T_cap; i += 64) dur[i] = 0;
+    for (int i = threadIdx.x; i < a.T_cap; i += 64) dur[i] = t > 0 && s > 0 ? -1 : 0;
     __threadfence_block();
   }
   __syncthreads();
@@ -338,9 +339,26 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
   if (lane == 0) {  // backtrack.hpp:23-24
     if (path) path[s - 1] = t - 1;
     if (out) out[static_cast<size_t>(t - 1) * a.S_cap + s - 1] = 1;
-    if (dur) atomicAdd(dur + (t - 1), 1);
+    if (dur) dur[t - 1] = s - 1;  // the last row ends at the last column
   }
-  if (s == 1) return;
+  // last columns -> durations: dur[r] = last[r] - last[r - 1], 0 past t
+  auto finish_durations = [&]() {
+    __syncwarp();
+    __threadfence_block();
+    int carry = -1;  // last column of the row before this chunk
+    for (int r0 = 0; r0 < a.T_cap; r0 += 32) {
+      const int r = r0 + lane;
+      const int v = r < t ? dur[r] : 0;
+      const int up = __shfl_up_sync(0xffffffffu, v, 1);
+      const int prev = lane == 0 ? carry : up;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+      if (r < a.T_cap) dur[r] = r < t ? v - prev : 0;
+    }
+  };
+  if (s == 1) {
+    if (dur) finish_durations();
+    return;
+  }
   uint32_t ph_done = 0;
   for (int n = n_top; n >= 0; --n) {
     const int slot = n & (kBtStages - 1);
@@ -377,20 +395,12 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
         if (path) path[j] = row;
         if (out) out[static_cast<size_t>(row) * a.S_cap + j] = 1;
       }
-      if (dur) {
-        // one atomic per run of equal rows among these 32 columns
-        const int prev = __shfl_up_sync(0xffffffffu, row, 1);
-        const int next = __shfl_down_sync(0xffffffffu, row, 1);
-        const bool start = valid && (lane == 0 || prev != row);
-        const bool end = valid && (lane == 31 || next != row);
-        const uint32_t starts = __ballot_sync(0xffffffffu, start);
-        if (end) {
-          const int first = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
-          atomicAdd(dur + row, lane - first + 1);
-        }
-      }
+      // an exit at this position: the row's last column (the row above
+      // continues from the next column)
+      if (dur && valid && ((rx[i] >> (31 - lane)) & 1u)) dur[row] = j;
     }
   }
+  if (dur) finish_durations();
 }
 
 // Reference-order serial walk, one thread per item -- kept as a
