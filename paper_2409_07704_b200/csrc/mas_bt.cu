@@ -282,6 +282,19 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
           const int ex = ex_lo + __popc(static_cast<uint32_t>(exw >> 32));
           // next pair: two words (or one) to the left, ex rows up
           const uint32_t pn = pw - static_cast<uint32_t>(ex * 4) - (pair ? 2u : 1u) * wstride;
+          const int y_n = y - ex, ml_n = ml - (pair ? 2 : 1);
+          const bool more = y_n != 0 && ml_n >= 0;
+          const bool recenter_n = more && y_n - 72 < ylo && ylo > 0;
+          // the next pair's first words are loaded before this pair's records
+          // are stored (the loads, not the stores, are on the walk's path)
+          if (more && !recenter_n) {
+            const bool pair_n = ml_n > 0;
+            x = ld64(pn, pair_n);
+            q1 = ld64(pn - 4, pair_n);
+            q2 = ld64(pn - 8, pair_n);
+            q3 = ld64(pn - 12, pair_n);
+            q4 = ld64(pn - 16, pair_n);
+          }
           rec_ex[slot][ml] = static_cast<uint32_t>(exw);
           if (pair) {
             rec_ex[slot][ml - 1] = static_cast<uint32_t>(exw >> 32);
@@ -291,20 +304,20 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
           if (pr_words < 300) { pr_ts[pr_words] = static_cast<unsigned>(clock64() - pr_t0); pr_ex[pr_words] = static_cast<unsigned char>(ex); }
           ++pr_words;
 #endif
-          y -= ex;
-          ml -= pair ? 2 : 1;
-          if (y == 0 || ml < 0) break;
+          y = y_n;
+          ml = ml_n;
+          if (!more) break;
           pair = ml > 0;
           pw = pn;
-          if (y - 72 < ylo && ylo > 0) {
+          if (recenter_n) {
             recenter();
             pw = slot_base + static_cast<uint32_t>((ml * R + (y - ylo)) * 4);
+            x = ld64(pw, pair);
+            q1 = ld64(pw - 4, pair);
+            q2 = ld64(pw - 8, pair);
+            q3 = ld64(pw - 12, pair);
+            q4 = ld64(pw - 16, pair);
           }
-          x = ld64(pw, pair);
-          q1 = ld64(pw - 4, pair);
-          q2 = ld64(pw - 8, pair);
-          q3 = ld64(pw - 12, pair);
-          q4 = ld64(pw - 16, pair);
         }
       }
       for (; ml >= 0; --ml) {  // the walk reached row 0: the rest stays there
