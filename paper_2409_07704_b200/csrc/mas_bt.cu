@@ -40,8 +40,10 @@ constexpr int kBtMaxRows = 256;  // rows per window (TMA box limit)
 // Window load of stage n: words [8n, 8n + 8) (those < M) of rows
 // [row0, row0 + R), as one bulk copy per word (a word's rows are contiguous
 // in the [B][M][T_alloc] layout), completing on `bar`.
+template <int WORDS>
 __device__ __forceinline__ void bt_issue(uint32_t dst, uint32_t bar, const uint32_t* item_dirs,
                                          int row0, int n, int M, int T_alloc, int R) {
+  constexpr int kBtWords = WORDS;
   const int words = min(kBtWords, M - kBtWords * n);
   const uint32_t wbytes = static_cast<uint32_t>(R * 4);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
@@ -105,7 +107,14 @@ __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
 //
 // A window miss (the walk descending more than ~R - 35 rows within four
 // stages) re-centres the window with a synchronous reload.
+// WORDS direction words (32 columns each) per stage, 32 / WORDS stages in
+// the ring: 8 for steep paths (a window row count bounds the rows a stage
+// can climb), 16 for shallow ones (half the stage transitions).
+template <int WORDS>
 __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
+  constexpr int kBtWords = WORDS;
+  constexpr int kBtStages = 32 / WORDS;
+  constexpr int kBtCols = 32 * WORDS;
   // Guard words in front: a block may read up to 8 rows below row 0, and the
   // speculative next-word load one word (R rows) before the first word.
   constexpr int kGuard = kBtMaxRows + 32;
@@ -176,7 +185,7 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
     for (int k = 0; k < kBtStages && n_top - k >= 0; ++k) {
       const int n = n_top - k, slot = n & (kBtStages - 1);
       s_ylo[slot] = bt_row0(y, R, T_alloc);
-      bt_issue(win_s + slot * kSlotBytes, full_s + 8u * slot, dirs, s_ylo[slot], n, M, T_alloc,
+      bt_issue<kBtWords>(win_s + slot * kSlotBytes, full_s + 8u * slot, dirs, s_ylo[slot], n, M, T_alloc,
                R);
       pend |= 1u << slot;
     }
@@ -214,7 +223,7 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           ylo = bt_row0(y, R, T_alloc);
           s_ylo[slot] = ylo;
-          bt_issue(slot_base, full_s + 8u * slot, dirs, ylo, n, M, T_alloc, R);
+          bt_issue<kBtWords>(slot_base, full_s + 8u * slot, dirs, ylo, n, M, T_alloc, R);
           mbar_wait(full_s + 8u * slot, (ph_full >> slot) & 1u);
           ph_full ^= 1u << slot;
         };
@@ -394,7 +403,7 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         const int row0 = bt_row0(yend, R, T_alloc);
         s_ylo[slot] = row0;
-        bt_issue(win_s + slot * kSlotBytes, full_s + 8u * slot, dirs, row0, n - kBtStages, M,
+        bt_issue<kBtWords>(win_s + slot * kSlotBytes, full_s + 8u * slot, dirs, row0, n - kBtStages, M,
                  T_alloc, R);
       }
     }
@@ -532,7 +541,14 @@ cudaError_t launch_backtrack(const BtArgs& a, cudaStream_t stream, int* launches
   cfg.numAttrs = 1;
 #endif
   if (launches) *launches = 1;
-  return cudaLaunchKernelEx(&cfg, bt_walk_kernel, a);
+  // shallow paths (at most one text row per four speech frames): wider stages
+  static const int words_env = [] {
+    const char* e = std::getenv("MAS_BT_WORDS");  // A/B override: 8 or 16
+    return e ? std::atoi(e) : 0;
+  }();
+  const bool wide = words_env ? words_env == 16 : 4 * a.T_cap <= a.S_cap;
+  return wide ? cudaLaunchKernelEx(&cfg, bt_walk_kernel<16>, a)
+              : cudaLaunchKernelEx(&cfg, bt_walk_kernel<8>, a);
 }
 
 cudaError_t bt_configure(int /*T_alloc*/, int /*L*/) { return cudaSuccess; }
