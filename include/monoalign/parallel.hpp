@@ -11,6 +11,12 @@ namespace monoalign::parallel {
 /// Lane count the reference would use (parallel.cpp:14-19); informational.
 MONOALIGN_API int pad_lanes(int t, LanePadding policy);
 
+/// In-place score table of the parallel engine (reference parallel.hpp:17,
+/// parallel.cpp:95-108), bit-identical; computed on the GPU
+/// (forward_scores_kernel via mas_forward_scores), the item round-tripping
+/// through device memory.
+MONOALIGN_API void forward_parallel(MutableLikelihoodView q, const MasConfig& cfg = {});
+
 MONOALIGN_API AlignmentMatrix align_parallel(const LikelihoodBatch& batch,
                                              const MasConfig& cfg = {});
 

@@ -197,6 +197,16 @@ MAS_API int mas_validate_host(const float* values, int32_t batch, int32_t text_c
 MAS_API int mas_generate_device(uint64_t seed, int32_t batch, int32_t text_cap, int32_t speech_cap,
                         int64_t first_item, int64_t row_pitch, float* d_out, void* stream);
 
+/* parallel::forward_parallel (parallel.hpp:17, parallel.cpp:95-108) over a
+ * device batch, in place: every item's [t][s] region of d_values becomes the
+ * parallel engine's score table Q, bit-identical to the reference (std::max
+ * tie rule, signed zeros).  lengths [B][2] host (t, s) or NULL = full; items
+ * with t or s = 0 are left untouched.  Stream-ordered; nothing is validated
+ * beyond shapes (forward_parallel validates nothing). */
+MAS_API int mas_forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_t text_cap,
+                               int32_t speech_cap, const uint32_t* lengths, float max_neg_val,
+                               void* stream, mas_error_t* err);
+
 /* ---- MASTENS v1 tensor files (tensor_io.hpp:11-23, tensor_io.cpp) --------
  * Host-only.  Errors are MAS_E_IO with the reference's IoError code and text
  * (IoFailure, BadMagic, UnsupportedVersion, TruncatedFile, DimensionOverflow).

@@ -154,6 +154,9 @@ class Reference:
                                        ctypes.POINTER(ctypes.c_int), ctypes.c_void_p,
                                        ctypes.c_int]
         lib.ref_hardware_threads.restype = ctypes.c_uint
+        lib.ref_forward_parallel.restype = None
+        lib.ref_forward_parallel.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_int64, ctypes.c_float]
         lib.ref_batch_create.restype = ctypes.c_void_p
         lib.ref_batch_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint64]
         lib.ref_batch_destroy.restype = None
@@ -171,6 +174,14 @@ class Reference:
                                         ctypes.POINTER(ctypes.c_int64 * 3), ctypes.c_void_p,
                                         ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int]
         self.lib = lib
+
+    def forward_parallel(self, q, t=None, s=None, max_neg_val=-1e32):
+        """parallel::forward_parallel on a copy of the 2-D item q (its [t, s] region)."""
+        q = np.array(q, dtype=np.float32, copy=True, order="C")
+        T, S = q.shape
+        self.lib.ref_forward_parallel(q.ctypes.data, T if t is None else t, S if s is None else s,
+                                      S, ctypes.c_float(max_neg_val))
+        return q
 
     def write_tensor(self, path, values, lengths=None):
         """io::write_tensor (tensor_io.cpp).  Returns (errc, message); -1 = ok."""

@@ -15,6 +15,7 @@
 //   bench::generate_random_batch         include/monoalign/bench.hpp:58
 //   oracle::best_paths                   include/monoalign/oracle.hpp:33
 //   io::write_tensor / io::read_tensor   include/monoalign/tensor_io.hpp:29-36
+//   parallel::forward_parallel           include/monoalign/parallel.hpp:17
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -25,6 +26,7 @@
 #include "monoalign/align.hpp"
 #include "monoalign/bench.hpp"
 #include "monoalign/oracle.hpp"
+#include "monoalign/parallel.hpp"
 #include "monoalign/tensor_io.hpp"
 
 namespace {
@@ -123,6 +125,14 @@ int ref_best_paths(const float* q, int t, int s, double* max_score, int* n_paths
   } catch (const monoalign::Error& e) {
     return static_cast<int>(e.code());
   }
+}
+
+/// parallel::forward_parallel on one [t][s] item (row stride `stride`), in
+/// place: the parallel engine's score table.
+void ref_forward_parallel(float* q, int t, int s, std::int64_t stride, float max_neg_val) {
+  monoalign::MasConfig cfg;
+  cfg.max_neg_val = max_neg_val;
+  monoalign::parallel::forward_parallel(monoalign::MutableLikelihoodView{q, t, s, stride}, cfg);
 }
 
 unsigned ref_hardware_threads() { return std::thread::hardware_concurrency(); }

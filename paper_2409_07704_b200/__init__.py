@@ -14,6 +14,7 @@ from .api import (
     align,
     align_durations,
     align_paths,
+    forward_parallel,
     generate_device,
     generate_random_batch,
     read_tensor,
@@ -27,6 +28,7 @@ __all__ = [
     "align_durations",
     "generate_random_batch",
     "generate_device",
+    "forward_parallel",
     "Plan",
     "read_tensor",
     "write_tensor",

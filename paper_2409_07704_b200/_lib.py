@@ -101,6 +101,9 @@ _SIGS = {
     "mas_io_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int64,
                                     ctypes.c_int64, ctypes.c_int64, _VP, _VP,
                                     ctypes.POINTER(MasError)]),
+    "mas_forward_scores": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.c_int32, _VP, ctypes.c_float, _VP,
+                                          ctypes.POINTER(MasError)]),
     "mas_errc_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "mas_abi_version": (ctypes.c_int, []),
 }

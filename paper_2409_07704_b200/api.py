@@ -289,6 +289,48 @@ def generate_device(b, t, s, seed, first_item=0, device=None, out=None, row_pitc
     return out if pitch == s else out[:, :, :s]
 
 
+def forward_parallel(values, lengths=None, max_neg_val=_DEFAULT_MAX_NEG_VAL):
+    """parallel::forward_parallel (reference parallel.hpp:17, parallel.cpp:95-108):
+    overwrites each item's [t, s] region of ``values`` with the parallel
+    engine's cumulative score table, in place, and returns ``values``.
+    Bit-identical to the reference (std::max tie rule, signed zeros).  A torch
+    CUDA float32 tensor is updated on its device (stream-ordered on the current
+    stream); a numpy float32 C-contiguous array round-trips through the GPU and
+    is written back in place.  Computed by forward_scores_kernel
+    (csrc/mas_scores.cu); there is no host implementation."""
+    import torch
+
+    lib = _lib.load()
+    was_2d, b, t, s = _check_dims(tuple(values.shape))
+    lens = None if lengths is None else _parse_lengths(lengths, b, t, s)
+    lens_ptr = None if lens is None else lens.ctypes.data
+    err = _lib.MasError()
+    if _is_torch(values):
+        if values.dtype != torch.float32 or not values.is_cuda:
+            raise ValueError("values must be a float32 CUDA tensor")
+        if values.stride(-1) != 1 or (not was_2d and values.stride(0) != t * values.stride(1)):
+            raise ValueError("values must have unit column stride and packed items")
+        pitch = values.stride(-2)
+        with torch.cuda.device(values.device):
+            stream = torch.cuda.current_stream(values.device)
+            rc = lib.mas_forward_scores(values.data_ptr(), pitch, b, t, s, lens_ptr,
+                                        float(np.float32(max_neg_val)),
+                                        ctypes.c_void_p(stream.cuda_stream), ctypes.byref(err))
+        _lib.raise_for(rc, err)
+        return values
+    if not isinstance(values, np.ndarray) or values.dtype != np.float32 or \
+            not values.flags.c_contiguous or not values.flags.writeable:
+        raise ValueError("values must be a writeable C-contiguous float32 array (updated in place)")
+    dev = torch.empty((b, t, s), dtype=torch.float32, device="cuda")
+    dev.copy_(torch.from_numpy(values.reshape(b, t, s)))
+    stream = torch.cuda.current_stream(dev.device)
+    rc = lib.mas_forward_scores(dev.data_ptr(), s, b, t, s, lens_ptr, float(np.float32(max_neg_val)),
+                                ctypes.c_void_p(stream.cuda_stream), ctypes.byref(err))
+    _lib.raise_for(rc, err)
+    values.reshape(b, t, s)[...] = dev.cpu().numpy()
+    return values
+
+
 class Plan:
     """Enqueue-only execution of the maximum-path call on device buffers
     (mas_plan_* in include/monoalign_b200.h): validation and workspace once,

@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 HOST_CXX = "/usr/bin/g++"  # dynamic libstdc++ 
 
 SOURCES = ["mas_abi.cu", "mas_fwd.cu", "mas_fwd4.cu", "mas_bt.cu", "monoalign_api.cpp",
-           "mas_io.cpp"]
+           "mas_io.cpp", "mas_scores.cu"]
 HEADERS = ["mas_kernels.h", "mas_ptx.cuh"]
 
 

@@ -1,0 +1,236 @@
+// mas_scores.cu -- score-table export: the parallel
+// engine's forward pass written back in place, as the reference's
+// parallel::forward_parallel does on a MutableLikelihoodView
+// (include/monoalign/parallel.hpp:17, src/parallel.cpp:95-108):
+//
+//   Q[i][0] = mnv                            i >= 1   (Q[0][0] = q[0][0])
+//   Q[0][j] = q[0][j] + max(mnv, Q[0][j-1])           j >= 1
+//   Q[i][j] = q[i][j] + max(Q[i-1][j-1], Q[i][j-1])   i, j >= 1
+//
+// with max(a, b) = (a < b) ? b : a (std::max, first argument on ties), so the
+// table is bit-identical to the reference's, signed zeros included.  This is
+// the call tests use to check scores cell by cell (test_parallel.cpp:91-103);
+// it is not on the maximum-path call, which never materialises Q (K1 keeps it
+// in registers and emits direction bits).  Costs 8 B/cell (read q, write Q).
+//
+// Layout: one CTA of 16 warps per item; a warp owns 32 consecutive rows (one
+// per lane) and walks the item in 32-column tiles.  Within a warp the value of
+// the row above comes from a shuffle (tiles are read and written coalesced,
+// lane = column, and transposed through shared memory; reads are cp.async
+// prefetches two tiles ahead into a 3-buffer ring per warp); across warps, the last row of warp w-1
+// is handed to warp w through a 4-tile shared-memory ring with per-warp
+// progress counters, so the 16 warps run as a skewed wavefront.  Texts longer
+// than 512 rows run as consecutive 512-row strips, the first warp of a strip
+// reading the finished last row of the previous strip back from the table.
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "monoalign_b200.h"
+
+namespace {
+
+constexpr int kWarps = 16;
+constexpr int kTile = 32;
+constexpr int kRing = 4;
+constexpr int kBufs = 3;  // per-warp tile buffers: prefetch distance 2
+constexpr int kTileFloats = 32 * (kTile + 1);
+constexpr int kTileSmem = kWarps * kBufs * kTileFloats * sizeof(float);
+
+__device__ __forceinline__ float ref_max(float a, float b) { return a < b ? b : a; }
+
+// 4-byte cp.async; src_bytes = 0 zero-fills without reading.
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, int src_bytes) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Rows r0..r0+31, columns j0..j0+31 of the item into buf[row][col]: lane =
+// column, so each warp-wide copy reads one contiguous 128-byte segment.
+__device__ __forceinline__ void prefetch_tile(float (*buf)[kTile + 1], const float* item,
+                                              int64_t pitch, int r0, int j0, int t, int s,
+                                              int lane) {
+  const bool col_ok = j0 + lane < s;
+#pragma unroll 8
+  for (int i = 0; i < 32; ++i) {
+    const bool ok = col_ok && r0 + i < t;
+    const float* src = ok ? item + static_cast<int64_t>(r0 + i) * pitch + j0 + lane : item;
+    cp_async4(&buf[i][lane], src, ok ? 4 : 0);
+  }
+}
+
+__global__ void __launch_bounds__(kWarps * 32, 1)
+forward_scores_kernel(float* __restrict__ q, int64_t pitch, int T_cap, int S_cap,
+                      const uint32_t* __restrict__ lengths, float mnv) {
+  extern __shared__ float tiles_raw[];  // [kWarps][kBufs][32][kTile + 1]
+  __shared__ float ring[kWarps][kRing][kTile];
+  __shared__ volatile int published[kWarps];  // tiles warp w has put in its ring
+  __shared__ volatile int consumed[kWarps];   // tiles warp w has read from warp w-1's ring
+  const int b = blockIdx.x;
+  const int t = lengths ? static_cast<int>(lengths[2 * b]) : T_cap;
+  const int s = lengths ? static_cast<int>(lengths[2 * b + 1]) : S_cap;
+  if (t < 1 || s < 1) return;  // uniform per CTA
+  float* item = q + static_cast<int64_t>(b) * T_cap * pitch;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = (s + kTile - 1) / kTile;
+  auto buf = [&](int c) {
+    return reinterpret_cast<float(*)[kTile + 1]>(tiles_raw + (warp * kBufs + c % kBufs) * kTileFloats);
+  };
+
+  for (int base = 0; base < t; base += kWarps * 32) {
+    if (threadIdx.x < kWarps) {
+      published[threadIdx.x] = 0;
+      consumed[threadIdx.x] = 0;
+    }
+    __syncthreads();
+    const int r0 = base + warp * 32;
+    if (r0 < t) {
+      const int r = r0 + lane;
+      const bool has_next = warp + 1 < kWarps && r0 + 32 < t;
+      const float* above = base > 0 ? item + static_cast<int64_t>(base - 1) * pitch : nullptr;
+      float prev = 0.f;        // Q[r][j-1]
+      float prev_above = mnv;  // lane 0: Q[r0-1][j-1]
+#pragma unroll 1
+      for (int c = 0; c < kBufs - 1; ++c) {
+        if (c < ntiles) prefetch_tile(buf(c), item, pitch, r0, c * kTile, t, s, lane);
+        cp_async_commit();
+      }
+      for (int c = 0; c < ntiles; ++c) {
+        const int j0 = c * kTile;
+        // the buffer of tile c+2 was drained by tile c-1's stores (synced below)
+        if (c + kBufs - 1 < ntiles)
+          prefetch_tile(buf(c + kBufs - 1), item, pitch, r0, j0 + (kBufs - 1) * kTile, t, s, lane);
+        cp_async_commit();
+        // lane k: Q[r0-1][j0+k] (row 0 has the sentinel above it)
+        float bnd = mnv;
+        if (warp > 0) {
+          if (lane == 0)
+            while (published[warp - 1] <= c) {
+            }
+          __syncwarp();
+          __threadfence_block();
+          bnd = ring[warp - 1][c % kRing][lane];
+          __syncwarp();
+          if (lane == 0) consumed[warp] = c + 1;
+        } else if (above) {
+          bnd = j0 + lane < s ? above[j0 + lane] : 0.f;
+        }
+        cp_async_wait<kBufs - 1>();
+        __syncwarp();
+        float(*tile)[kTile + 1] = buf(c);
+        float v[kTile];
+#pragma unroll
+        for (int k = 0; k < kTile; ++k) v[k] = tile[lane][k];
+#pragma unroll
+        for (int k = 0; k < kTile; ++k) {
+          const int j = j0 + k;
+          float up = __shfl_up_sync(0xffffffffu, prev, 1);
+          const float b_prev = __shfl_sync(0xffffffffu, bnd, (k + 31) & 31);
+          if (lane == 0) up = k == 0 ? prev_above : b_prev;
+          float n;
+          if (j == 0)
+            n = r == 0 ? v[k] : mnv;
+          else
+            n = v[k] + ref_max(up, prev);
+          v[k] = n;
+          prev = n;
+        }
+        prev_above = __shfl_sync(0xffffffffu, bnd, 31);
+        // hand the last row to the next warp before writing the tile back
+        if (has_next && lane == 31) {
+          while (consumed[warp + 1] + kRing <= c) {
+          }
+          float* slot = ring[warp][c % kRing];
+#pragma unroll
+          for (int k = 0; k < kTile; ++k) slot[k] = v[k];
+          __threadfence_block();
+          published[warp] = c + 1;
+        }
+#pragma unroll
+        for (int k = 0; k < kTile; ++k) tile[lane][k] = v[k];
+        __syncwarp();
+        const bool col_ok = j0 + lane < s;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (col_ok && r0 + i < t) item[static_cast<int64_t>(r0 + i) * pitch + j0 + lane] = tile[i][lane];
+        __syncwarp();  // the buffer is refilled by the prefetch two tiles on
+      }
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+  }
+}
+
+int fail(mas_error_t* err, int status, int errc, const std::string& msg) {
+  if (err) {
+    std::memset(err, 0, sizeof(*err));
+    err->status = status;
+    err->errc = errc;
+    err->item = -1;
+    err->i = err->j = -1;
+    std::snprintf(err->message, sizeof(err->message), "%s", msg.c_str());
+  }
+  return status;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mas_forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_t text_cap,
+                       int32_t speech_cap, const uint32_t* lengths, float max_neg_val,
+                       void* stream_v, mas_error_t* err) {
+  if (err) {
+    std::memset(err, 0, sizeof(*err));
+    err->item = -1;
+    err->i = err->j = -1;
+  }
+  if (batch < 1 || text_cap < 1 || speech_cap < 1)
+    return fail(err, MAS_E_VALIDATION, MAS_ERRC_ZERO_DIM, "batch and capacities must be at least 1");
+  if (row_pitch < speech_cap)
+    return fail(err, MAS_E_VALIDATION, MAS_ERRC_SHAPE_MISMATCH,
+                "row pitch is smaller than the speech capacity");
+  if (lengths)
+    for (int32_t b = 0; b < batch; ++b)
+      if (lengths[2 * b] > static_cast<uint32_t>(text_cap) ||
+          lengths[2 * b + 1] > static_cast<uint32_t>(speech_cap)) {
+        const int rc = fail(err, MAS_E_VALIDATION, MAS_ERRC_LENGTHS_OUT_OF_RANGE,
+                            "item " + std::to_string(b) + ": lengths exceed the capacities");
+        if (err) err->item = b;
+        return rc;
+      }
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  uint32_t* d_len = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (lengths) {
+    const size_t bytes = static_cast<size_t>(batch) * 2 * sizeof(uint32_t);
+    e = cudaMallocAsync(reinterpret_cast<void**>(&d_len), bytes, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_len, lengths, bytes, cudaMemcpyHostToDevice, stream);
+  }
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      forward_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
+  if (e == cudaSuccess) e = attr;
+  if (e == cudaSuccess) {
+    forward_scores_kernel<<<batch, kWarps * 32, kTileSmem, stream>>>(d_values, row_pitch, text_cap,
+                                                              speech_cap, d_len, max_neg_val);
+    e = cudaGetLastError();
+  }
+  if (d_len) {
+    const cudaError_t f = cudaFreeAsync(d_len, stream);
+    if (e == cudaSuccess) e = f;
+  }
+  if (e != cudaSuccess)
+    return fail(err, MAS_E_CUDA, -1, std::string("forward_scores: ") + cudaGetErrorString(e));
+  return MAS_OK;
+}
+
+}  // extern "C"

@@ -206,6 +206,34 @@ int pad_lanes(int t, LanePadding policy) {
   return static_cast<int>(v);
 }
 
+void forward_parallel(MutableLikelihoodView q, const MasConfig& cfg) {
+  // The item round-trips through device memory; forward_scores_kernel
+  // computes the table (mas_forward_scores), nothing is computed here.
+  if (q.text < 1 || q.speech < 1) return;
+  const size_t row_bytes = static_cast<size_t>(q.speech) * sizeof(float);
+  const size_t bytes = row_bytes * q.text;
+  float* d = nullptr;
+  auto check = [&](cudaError_t e) {
+    if (e != cudaSuccess) {
+      if (d) cudaFree(d);
+      throw DeviceError(std::string("monoalign device path failed: ") + cudaGetErrorString(e));
+    }
+  };
+  check(cudaMalloc(reinterpret_cast<void**>(&d), bytes));
+  check(cudaMemcpy2D(d, row_bytes, q.data, q.row_stride * sizeof(float), row_bytes, q.text,
+                     cudaMemcpyHostToDevice));
+  mas_error_t err;
+  const int rc = mas_forward_scores(d, q.speech, 1, q.text, q.speech, nullptr, cfg.max_neg_val,
+                                    nullptr, &err);
+  if (rc != MAS_OK) {
+    cudaFree(d);
+    throw_for(rc, err);
+  }
+  check(cudaMemcpy2D(q.data, q.row_stride * sizeof(float), d, row_bytes, row_bytes, q.text,
+                     cudaMemcpyDeviceToHost));
+  cudaFree(d);
+}
+
 AlignmentMatrix align_parallel(const LikelihoodBatch& batch, const MasConfig& cfg) {
   MasConfig c = cfg;
   c.engine = EngineKind::Parallel;

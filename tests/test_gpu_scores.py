@@ -1,0 +1,107 @@
+"""Score-table export: forward_parallel on the GPU
+(csrc/mas_scores.cu through mas_forward_scores) against the reference's
+parallel::forward_parallel (oracle/_ref, parallel.cpp:95-108) and the C
+restatement (oracle/mas_oracle.c), bit for bit -- every cell of every item,
+signed zeros included.  Cases follow test_parallel.cpp:44-103."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+def test_reference_examples(mas, cuda):
+    # test_parallel.cpp:44-52 -- the 2x3 example
+    q = np.arange(1, 7, dtype=np.float32).reshape(2, 3)
+    mas.forward_parallel(q)
+    assert q[0].tolist() == [1.0, 3.0, 6.0]
+    assert q[1, 0] <= -1e30 and q[1, 1] == 6.0 and q[1, 2] == 12.0
+    # :54-62 -- an all-zero feasible region stays zero
+    z = np.zeros((3, 5), np.float32)
+    mas.forward_parallel(z)
+    assert all(z[i, j] == 0.0 for i in range(3) for j in range(i, 5))
+    # :64-68 -- a single cell is a no-op
+    one = np.array([[7.0]], np.float32)
+    mas.forward_parallel(one)
+    assert one[0, 0] == 7.0
+
+
+@pytest.mark.parametrize("t,s", [(1, 1), (1, 37), (5, 5), (12, 24), (31, 33), (33, 100),
+                                 (64, 256), (200, 800), (511, 513), (512, 700), (513, 600),
+                                 (1100, 1200), (2049, 2100)])
+def test_items_bit_exact(mas, reference, oracle, cuda, t, s):
+    rng = np.random.default_rng(t * 7919 + s)
+    q = rng.uniform(-5, 5, (t, s)).astype(np.float32)
+    want = reference.forward_parallel(q)
+    assert _bits(oracle.forward_parallel(q)).tobytes() == _bits(want).tobytes()
+    got = q.copy()
+    assert mas.forward_parallel(got) is got
+    np.testing.assert_array_equal(_bits(got), _bits(want))
+
+
+def test_signed_zeros_and_ties(mas, reference, cuda):
+    rng = np.random.default_rng(3)
+    for it in range(6):
+        t, s = int(rng.integers(2, 70)), int(rng.integers(70, 140))
+        q = np.zeros((t, s), np.float32)
+        q[rng.random((t, s)) < 0.5] = -0.0
+        q[rng.random((t, s)) < 0.1] = 1.0
+        want = reference.forward_parallel(q)
+        got = mas.forward_parallel(q.copy())
+        np.testing.assert_array_equal(_bits(got), _bits(want))
+
+
+@pytest.mark.parametrize("mnv", [-1e32, -1e30, float("-inf")])
+def test_sentinels(mas, reference, cuda, mnv):
+    rng = np.random.default_rng(5)
+    q = rng.uniform(-5, 5, (40, 90)).astype(np.float32)
+    want = reference.forward_parallel(q, max_neg_val=mnv)
+    got = mas.forward_parallel(q.copy(), max_neg_val=mnv)
+    np.testing.assert_array_equal(_bits(got), _bits(want))
+
+
+def test_ragged_batch_leaves_padding_untouched(mas, reference, cuda):
+    rng = np.random.default_rng(11)
+    B, T, S = 6, 300, 900
+    q = rng.uniform(-5, 5, (B, T, S)).astype(np.float32)
+    lens = np.array([[300, 900], [1, 1], [17, 40], [299, 777], [0, 0], [150, 151]])
+    got = q.copy()
+    mas.forward_parallel(got, lengths=lens)
+    for b in range(B):
+        t, s = lens[b]
+        want = q[b].copy()
+        if t and s:
+            want[:t, :s] = reference.forward_parallel(q[b, :t, :s])
+        np.testing.assert_array_equal(_bits(got[b]), _bits(want), err_msg=f"item {b}")
+
+
+def test_torch_in_place_pitched(mas, reference, cuda):
+    import torch
+
+    rng = np.random.default_rng(13)
+    B, T, S, P = 3, 520, 1000, 1040
+    q = rng.uniform(-5, 5, (B, T, S)).astype(np.float32)
+    buf = torch.full((B, T, P), 123.0, dtype=torch.float32, device="cuda")
+    view = buf[:, :, :S]
+    view.copy_(torch.from_numpy(q))
+    assert mas.forward_parallel(view) is view
+    torch.cuda.synchronize()
+    got = buf.cpu().numpy()
+    assert (got[:, :, S:] == 123.0).all()
+    for b in range(B):
+        np.testing.assert_array_equal(_bits(got[b, :, :S]), _bits(reference.forward_parallel(q[b])))
+
+
+def test_rejects_bad_input(mas, cuda):
+    with pytest.raises(ValueError):
+        mas.forward_parallel(np.zeros((2, 3), np.float64))
+    with pytest.raises(ValueError):
+        mas.forward_parallel(np.zeros((2, 3), np.float32), lengths=[[3, 3]])
+    with pytest.raises(ValueError):
+        mas.forward_parallel(np.zeros((2, 3), np.float32)[:, ::2])

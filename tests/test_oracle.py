@@ -123,3 +123,20 @@ def test_generator_vs_reference(oracle, reference):
     for (b, t, s, seed) in [(2, 17, 40, 3), (1, 64, 256, 0), (4, 3, 9, 2**64 - 1)]:
         np.testing.assert_array_equal(oracle.generate(b, t, s, seed),
                                       reference.generate(b, t, s, seed))
+
+
+def test_forward_parallel_matches_reference(oracle, reference):
+    """The score-table restatement (oracle_forward_parallel) against the
+    reference's parallel::forward_parallel, bit for bit (test_parallel.cpp:91-103)."""
+    rng = np.random.default_rng(21)
+    for it in range(40):
+        t = int(rng.integers(1, 40))
+        s = int(rng.integers(t, 90))
+        q = rng.uniform(-5, 5, (t, s)).astype(np.float32)
+        if it % 4 == 0:
+            q[rng.random((t, s)) < 0.5] = 0.0
+            q[rng.random((t, s)) < 0.3] = -0.0
+        mnv = [-1e32, -1e30, float("-inf")][it % 3]
+        a = oracle.forward_parallel(q, max_neg_val=mnv)
+        b = reference.forward_parallel(q, max_neg_val=mnv)
+        assert a.view(np.uint32).tobytes() == b.view(np.uint32).tobytes(), it
