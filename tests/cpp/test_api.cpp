@@ -14,6 +14,7 @@
 
 #include "monoalign/align.hpp"
 #include "monoalign/bench.hpp"
+#include "monoalign/parallel.hpp"
 #include "monoalign/tensor_io.hpp"
 
 #include <filesystem>
@@ -190,6 +191,20 @@ int main() {
     const auto* m2 = std::get_if<ma::AlignmentMatrix>(&t2);
     EXPECT(m2 && m2->values == m.values);
     std::filesystem::remove(path);
+  }
+  // forward_parallel score table, in place (test_parallel.cpp:44-68).
+  {
+    auto b = item(2, 3, {1, 2, 3, 4, 5, 6});
+    ma::parallel::forward_parallel(ma::item_view(b, 0));
+    EXPECT(b.values[0] == 1.0f && b.values[1] == 3.0f && b.values[2] == 6.0f);
+    EXPECT(b.values[3] <= -1e30f && b.values[4] == 6.0f && b.values[5] == 12.0f);
+    auto z = item(3, 5, std::vector<float>(15, 0.0f));
+    ma::parallel::forward_parallel(ma::item_view(z, 0));
+    for (int i = 0; i < 3; ++i)
+      for (int j = i; j < 5; ++j) EXPECT(z.values[i * 5 + j] == 0.0f);
+    auto one = item(1, 1, {7.0f});
+    ma::parallel::forward_parallel(ma::item_view(one, 0));
+    EXPECT(one.values[0] == 7.0f);
   }
   if (g_fail) {
     std::fprintf(stderr, "%d expectation(s) failed\n", g_fail);
