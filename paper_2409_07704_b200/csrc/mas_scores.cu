@@ -13,15 +13,17 @@
 // it is not on the maximum-path call, which never materialises Q (K1 keeps it
 // in registers and emits direction bits).  Costs 8 B/cell (read q, write Q).
 //
-// Layout: one CTA of 16 warps per item; a warp owns 32 consecutive rows (one
+// Layout: CTAs of 8 warps; a warp owns 32 consecutive rows (one
 // per lane) and walks the item in 32-column tiles.  Within a warp the value of
 // the row above comes from a shuffle (tiles are read and written coalesced,
 // lane = column, and transposed through shared memory; reads are cp.async
 // prefetches two tiles ahead into a 3-buffer ring per warp); across warps, the last row of warp w-1
 // is handed to warp w through a 4-tile shared-memory ring with per-warp
-// progress counters, so the 16 warps run as a skewed wavefront.  Texts longer
-// than 512 rows run as consecutive 512-row strips, the first warp of a strip
-// reading the finished last row of the previous strip back from the table.
+// progress counters, so the 8 warps run as a skewed wavefront.  Texts longer
+// than 256 rows are split into 256-row strips, one CTA each, running
+// concurrently: the first warp of a strip reads the last row of the strip
+// above back from the table (L2) as soon as that strip's progress counter
+// (release/acquire, global) says the tile is stored.
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -33,7 +35,9 @@
 
 namespace {
 
-constexpr int kWarps = 16;
+constexpr int kWarps = 8;
+constexpr int kStripRows = kWarps * 32;
+constexpr int kStripPub = 8;  // tiles per cross-strip progress release
 constexpr int kTile = 32;
 constexpr int kRing = 4;
 constexpr int kBufs = 3;  // per-warp tile buffers: prefetch distance 2
@@ -41,6 +45,15 @@ constexpr int kTileFloats = 32 * (kTile + 1);
 constexpr int kTileSmem = kWarps * kBufs * kTileFloats * sizeof(float);
 
 __device__ __forceinline__ float ref_max(float a, float b) { return a < b ? b : a; }
+
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // 4-byte cp.async; src_bytes = 0 zero-fills without reading.
 __device__ __forceinline__ void cp_async4(float* dst, const float* src, int src_bytes) {
@@ -68,14 +81,21 @@ __device__ __forceinline__ void prefetch_tile(float (*buf)[kTile + 1], const flo
   }
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 1)
+__global__ void __launch_bounds__(kWarps * 32, 2)
 forward_scores_kernel(float* __restrict__ q, int64_t pitch, int T_cap, int S_cap,
-                      const uint32_t* __restrict__ lengths, float mnv) {
+                      const uint32_t* __restrict__ lengths, float mnv, int nstrips,
+                      int strips_per_cta, int* __restrict__ ticket, int* __restrict__ progress) {
   extern __shared__ float tiles_raw[];  // [kWarps][kBufs][32][kTile + 1]
   __shared__ float ring[kWarps][kRing][kTile];
   __shared__ volatile int published[kWarps];  // tiles warp w has put in its ring
   __shared__ volatile int consumed[kWarps];   // tiles warp w has read from warp w-1's ring
-  const int b = blockIdx.x;
+  __shared__ int vblock;
+  // Strips are taken in ticket order, so the strip above is always running or
+  // done before a strip waits on it (no reliance on block dispatch order).
+  if (threadIdx.x == 0) vblock = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int ngroups = (nstrips + strips_per_cta - 1) / strips_per_cta;
+  const int b = vblock / ngroups, first_strip = vblock % ngroups * strips_per_cta;
   const int t = lengths ? static_cast<int>(lengths[2 * b]) : T_cap;
   const int s = lengths ? static_cast<int>(lengths[2 * b + 1]) : S_cap;
   if (t < 1 || s < 1) return;  // uniform per CTA
@@ -86,7 +106,11 @@ forward_scores_kernel(float* __restrict__ q, int64_t pitch, int T_cap, int S_cap
     return reinterpret_cast<float(*)[kTile + 1]>(tiles_raw + (warp * kBufs + c % kBufs) * kTileFloats);
   };
 
-  for (int base = 0; base < t; base += kWarps * 32) {
+  const int last_strip = min(nstrips, first_strip + strips_per_cta);
+  for (int strip = first_strip; strip < last_strip; ++strip) {
+    const int base = strip * kStripRows;
+    if (base >= t) break;  // uniform per CTA
+    int* const my_progress = progress + static_cast<int64_t>(b) * nstrips + strip;
     if (threadIdx.x < kWarps) {
       published[threadIdx.x] = 0;
       consumed[threadIdx.x] = 0;
@@ -96,7 +120,9 @@ forward_scores_kernel(float* __restrict__ q, int64_t pitch, int T_cap, int S_cap
     if (r0 < t) {
       const int r = r0 + lane;
       const bool has_next = warp + 1 < kWarps && r0 + 32 < t;
-      const float* above = base > 0 ? item + static_cast<int64_t>(base - 1) * pitch : nullptr;
+      const float* above =
+          warp == 0 && base > 0 ? item + static_cast<int64_t>(base - 1) * pitch : nullptr;
+      const bool publish_down = warp == kWarps - 1 && base + kStripRows < t;
       float prev = 0.f;        // Q[r][j-1]
       float prev_above = mnv;  // lane 0: Q[r0-1][j-1]
 #pragma unroll 1
@@ -114,15 +140,24 @@ forward_scores_kernel(float* __restrict__ q, int64_t pitch, int T_cap, int S_cap
         float bnd = mnv;
         if (warp > 0) {
           if (lane == 0)
-            while (published[warp - 1] <= c) {
-            }
+            while (published[warp - 1] <= c) __nanosleep(32);
           __syncwarp();
           __threadfence_block();
           bnd = ring[warp - 1][c % kRing][lane];
           __syncwarp();
           if (lane == 0) consumed[warp] = c + 1;
         } else if (above) {
-          bnd = j0 + lane < s ? above[j0 + lane] : 0.f;
+          // the strip above publishes tile c after its last row is stored
+          // relaxed polling (an acquire load per poll invalidates L1), one
+          // acquire fence once the count is seen
+          if (lane == 0) {
+            if (ld_relaxed(my_progress - 1) <= c) {
+              while (ld_relaxed(my_progress - 1) <= c) __nanosleep(64);
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          }
+          __syncwarp();
+          bnd = j0 + lane < s ? __ldcg(above + j0 + lane) : 0.f;
         }
         cp_async_wait<kBufs - 1>();
         __syncwarp();
@@ -147,8 +182,7 @@ forward_scores_kernel(float* __restrict__ q, int64_t pitch, int T_cap, int S_cap
         prev_above = __shfl_sync(0xffffffffu, bnd, 31);
         // hand the last row to the next warp before writing the tile back
         if (has_next && lane == 31) {
-          while (consumed[warp + 1] + kRing <= c) {
-          }
+          while (consumed[warp + 1] + kRing <= c) __nanosleep(32);
           float* slot = ring[warp][c % kRing];
 #pragma unroll
           for (int k = 0; k < kTile; ++k) slot[k] = v[k];
@@ -163,6 +197,10 @@ forward_scores_kernel(float* __restrict__ q, int64_t pitch, int T_cap, int S_cap
         for (int i = 0; i < 32; ++i)
           if (col_ok && r0 + i < t) item[static_cast<int64_t>(r0 + i) * pitch + j0 + lane] = tile[i][lane];
         __syncwarp();  // the buffer is refilled by the prefetch two tiles on
+        if (publish_down && lane == 0 && ((c + 1) % kStripPub == 0 || c + 1 == ntiles)) {
+          __threadfence();
+          st_release(my_progress, c + 1);
+        }
       }
       cp_async_wait<0>();
     }
@@ -209,23 +247,46 @@ int mas_forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_
         return rc;
       }
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
-  uint32_t* d_len = nullptr;
-  cudaError_t e = cudaSuccess;
-  if (lengths) {
-    const size_t bytes = static_cast<size_t>(batch) * 2 * sizeof(uint32_t);
-    e = cudaMallocAsync(reinterpret_cast<void**>(&d_len), bytes, stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_len, lengths, bytes, cudaMemcpyHostToDevice, stream);
+  const int nstrips = (text_cap + kStripRows - 1) / kStripRows;
+  // Strips run concurrently (one CTA each, handing rows down through L2)
+  // while the batch alone would not fill the GPU; otherwise each CTA walks
+  // its item's strips in order and the hand-downs are all local.
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  const int strips_per_cta = batch >= sms ? nstrips : 1;
+  const int64_t blocks = static_cast<int64_t>(batch) * ((nstrips + strips_per_cta - 1) / strips_per_cta);
+  const int64_t nprogress = static_cast<int64_t>(batch) * nstrips;
+  if (blocks > 0x7fffffff)
+    return fail(err, MAS_E_UNSUPPORTED, -1, "forward_scores: batch x strips exceeds the grid");
+  // workspace: [B][2] uint32 lengths | ticket | progress[B * nstrips]
+  const size_t len_bytes = lengths ? static_cast<size_t>(batch) * 2 * sizeof(uint32_t) : 0;
+  const size_t sync_bytes = (1 + static_cast<size_t>(nprogress)) * sizeof(int);
+  char* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), len_bytes + sync_bytes, stream);
+  uint32_t* d_len = lengths ? reinterpret_cast<uint32_t*>(ws) : nullptr;
+  int* sync = reinterpret_cast<int*>(ws + len_bytes);
+  if (e == cudaSuccess && lengths)
+    e = cudaMemcpyAsync(d_len, lengths, len_bytes, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(sync, 0, sync_bytes, stream);
+  // A grid that fits the GPU once over is spread one CTA per SM (the
+  // shared-memory request alone keeps a second CTA off): the strips of an
+  // item are latency-bound chains, co-residency only slows them.
+  constexpr int kSpreadSmem = 160 * 1024;
   static const cudaError_t attr = cudaFuncSetAttribute(
-      forward_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
+      forward_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpreadSmem);
+  const int smem = blocks <= sms ? kSpreadSmem : kTileSmem;
   if (e == cudaSuccess) e = attr;
   if (e == cudaSuccess) {
-    forward_scores_kernel<<<batch, kWarps * 32, kTileSmem, stream>>>(d_values, row_pitch, text_cap,
-                                                              speech_cap, d_len, max_neg_val);
+    forward_scores_kernel<<<static_cast<unsigned>(blocks), kWarps * 32, smem, stream>>>(
+        d_values, row_pitch, text_cap, speech_cap, d_len, max_neg_val, nstrips, strips_per_cta, sync, sync + 1);
     e = cudaGetLastError();
   }
-  if (d_len) {
-    const cudaError_t f = cudaFreeAsync(d_len, stream);
+  if (ws) {
+    const cudaError_t f = cudaFreeAsync(ws, stream);
     if (e == cudaSuccess) e = f;
   }
   if (e != cudaSuccess)

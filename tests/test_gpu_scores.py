@@ -105,3 +105,19 @@ def test_rejects_bad_input(mas, cuda):
         mas.forward_parallel(np.zeros((2, 3), np.float32), lengths=[[3, 3]])
     with pytest.raises(ValueError):
         mas.forward_parallel(np.zeros((2, 3), np.float32)[:, ::2])
+
+
+def test_large_batch_sequential_strips(mas, reference, cuda):
+    """B >= SM count: each CTA walks its item's strips in order (the other
+    scheduling mode of mas_forward_scores)."""
+    rng = np.random.default_rng(17)
+    B, T, S = 160, 600, 70
+    q = rng.uniform(-5, 5, (B, T, S)).astype(np.float32)
+    lens = np.stack([rng.integers(1, T + 1, B), np.full(B, S)], 1)
+    got = q.copy()
+    mas.forward_parallel(got, lengths=lens)
+    for b in range(0, B, 7):
+        t, s = lens[b]
+        want = q[b].copy()
+        want[:t, :s] = reference.forward_parallel(q[b, :t, :s])
+        np.testing.assert_array_equal(_bits(got[b]), _bits(want), err_msg=f"item {b}")
