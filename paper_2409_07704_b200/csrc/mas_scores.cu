@@ -13,13 +13,13 @@
 // it is not on the maximum-path call, which never materialises Q (K1 keeps it
 // in registers and emits direction bits).  Costs 8 B/cell (read q, write Q).
 //
-// Layout: CTAs of 8 warps; a warp owns 32 consecutive rows (one
-// per lane) and walks the item in 32-column tiles.  Within a warp the value of
+// Layout: CTAs of 8/R warps; a warp owns 32R rows (lane l: rows l, l+32, ...;
+// R = 2 for grids that fit the GPU once, else 1) and walks the item in 32-column tiles.  Within a warp the value of
 // the row above comes from a shuffle (tiles are read and written coalesced,
 // lane = column, and transposed through shared memory; reads are cp.async
 // prefetches two tiles ahead into a 3-buffer ring per warp); across warps, the last row of warp w-1
 // is handed to warp w through a 4-tile shared-memory ring with per-warp
-// progress counters, so the 8 warps run as a skewed wavefront.  Texts longer
+// progress counters, so the warps run as a skewed wavefront.  Texts longer
 // than 256 rows are split into 256-row strips, one CTA each, running
 // concurrently: the first warp of a strip reads the last row of the strip
 // above back from the table (L2) as soon as that strip's progress counter
@@ -35,14 +35,22 @@
 
 namespace {
 
-constexpr int kWarps = 8;
-constexpr int kStripRows = kWarps * 32;
+// R rows per lane: lane l owns rows l, l + 32, ... of its warp's 32R-row
+// block; CTAs of 8/R warps, so a strip is 256 rows either way.
+constexpr int kStripRows = 256;
 constexpr int kStripPub = 8;  // tiles per cross-strip progress release
 constexpr int kTile = 32;
 constexpr int kRing = 4;
-constexpr int kBufs = 3;  // per-warp tile buffers: prefetch distance 2
-constexpr int kTileFloats = 32 * (kTile + 1);
-constexpr int kTileSmem = kWarps * kBufs * kTileFloats * sizeof(float);
+template <int R>
+struct Geo {
+  static constexpr int kWarps = 8 / R;
+  static constexpr int kWarpRows = 32 * R;
+  static constexpr int kBufs = R == 1 ? 3 : 2;  // per-warp tile buffers (prefetch distance kBufs-1)
+  static constexpr int kTileFloats = kWarpRows * (kTile + 1);
+  static constexpr int kTileSmem = kWarps * kBufs * kTileFloats * sizeof(float);
+};
+static_assert(Geo<1>::kWarps * Geo<1>::kWarpRows == kStripRows, "strip");
+static_assert(Geo<2>::kWarps * Geo<2>::kWarpRows == kStripRows, "strip");
 
 __device__ __forceinline__ float ref_max(float a, float b) { return a < b ? b : a; }
 
@@ -67,25 +75,29 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Rows r0..r0+31, columns j0..j0+31 of the item into buf[row][col]: lane =
+// Rows r0..r0+63, columns j0..j0+31 of the item into buf[row][col]: lane =
 // column, so each warp-wide copy reads one contiguous 128-byte segment.
+template <int ROWS>
 __device__ __forceinline__ void prefetch_tile(float (*buf)[kTile + 1], const float* item,
                                               int64_t pitch, int r0, int j0, int t, int s,
                                               int lane) {
   const bool col_ok = j0 + lane < s;
 #pragma unroll 8
-  for (int i = 0; i < 32; ++i) {
+  for (int i = 0; i < ROWS; ++i) {
     const bool ok = col_ok && r0 + i < t;
     const float* src = ok ? item + static_cast<int64_t>(r0 + i) * pitch + j0 + lane : item;
     cp_async4(&buf[i][lane], src, ok ? 4 : 0);
   }
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 2)
+template <int R>
+__global__ void __launch_bounds__(Geo<R>::kWarps * 32, 1)
 forward_scores_kernel(float* __restrict__ q, int64_t pitch, int T_cap, int S_cap,
                       const uint32_t* __restrict__ lengths, float mnv, int nstrips,
                       int strips_per_cta, int* __restrict__ ticket, int* __restrict__ progress) {
-  extern __shared__ float tiles_raw[];  // [kWarps][kBufs][32][kTile + 1]
+  constexpr int kWarps = Geo<R>::kWarps, kWarpRows = Geo<R>::kWarpRows, kBufs = Geo<R>::kBufs;
+  constexpr int kTileFloats = Geo<R>::kTileFloats;
+  extern __shared__ float tiles_raw[];  // [kWarps][kBufs][kWarpRows][kTile + 1]
   __shared__ float ring[kWarps][kRing][kTile];
   __shared__ volatile int published[kWarps];  // tiles warp w has put in its ring
   __shared__ volatile int consumed[kWarps];   // tiles warp w has read from warp w-1's ring
@@ -116,25 +128,27 @@ forward_scores_kernel(float* __restrict__ q, int64_t pitch, int T_cap, int S_cap
       consumed[threadIdx.x] = 0;
     }
     __syncthreads();
-    const int r0 = base + warp * 32;
+    const int r0 = base + warp * kWarpRows;
     if (r0 < t) {
       const int r = r0 + lane;
-      const bool has_next = warp + 1 < kWarps && r0 + 32 < t;
+      const bool has_next = warp + 1 < kWarps && r0 + kWarpRows < t;
       const float* above =
           warp == 0 && base > 0 ? item + static_cast<int64_t>(base - 1) * pitch : nullptr;
       const bool publish_down = warp == kWarps - 1 && base + kStripRows < t;
-      float prev = 0.f;        // Q[r][j-1]
-      float prev_above = mnv;  // lane 0: Q[r0-1][j-1]
+      float prev[R];  // Q[r + 32m][j-1]
+#pragma unroll
+      for (int m = 0; m < R; ++m) prev[m] = 0.f;
+      float prev_above = mnv;          // lane 0: Q[r0-1][j-1]
 #pragma unroll 1
       for (int c = 0; c < kBufs - 1; ++c) {
-        if (c < ntiles) prefetch_tile(buf(c), item, pitch, r0, c * kTile, t, s, lane);
+        if (c < ntiles) prefetch_tile<kWarpRows>(buf(c), item, pitch, r0, c * kTile, t, s, lane);
         cp_async_commit();
       }
       for (int c = 0; c < ntiles; ++c) {
         const int j0 = c * kTile;
         // the buffer of tile c+2 was drained by tile c-1's stores (synced below)
         if (c + kBufs - 1 < ntiles)
-          prefetch_tile(buf(c + kBufs - 1), item, pitch, r0, j0 + (kBufs - 1) * kTile, t, s, lane);
+          prefetch_tile<kWarpRows>(buf(c + kBufs - 1), item, pitch, r0, j0 + (kBufs - 1) * kTile, t, s, lane);
         cp_async_commit();
         // lane k: Q[r0-1][j0+k] (row 0 has the sentinel above it)
         float bnd = mnv;
@@ -162,22 +176,33 @@ forward_scores_kernel(float* __restrict__ q, int64_t pitch, int T_cap, int S_cap
         cp_async_wait<kBufs - 1>();
         __syncwarp();
         float(*tile)[kTile + 1] = buf(c);
-        float v[kTile];
+        float v[R][kTile];
 #pragma unroll
-        for (int k = 0; k < kTile; ++k) v[k] = tile[lane][k];
+        for (int m = 0; m < R; ++m)
+#pragma unroll
+          for (int k = 0; k < kTile; ++k) v[m][k] = tile[lane + 32 * m][k];
 #pragma unroll
         for (int k = 0; k < kTile; ++k) {
           const int j = j0 + k;
-          float up = __shfl_up_sync(0xffffffffu, prev, 1);
+          // row r + 32m's upper neighbour is lane l-1's row m, except lane
+          // 0's, which is lane 31's row m-1 (or the row above the block)
+          float up[R];
+          up[0] = __shfl_up_sync(0xffffffffu, prev[0], 1);
+#pragma unroll
+          for (int m = 1; m < R; ++m)
+            up[m] = __shfl_sync(0xffffffffu, lane == 31 ? prev[m - 1] : prev[m], (lane + 31) & 31);
           const float b_prev = __shfl_sync(0xffffffffu, bnd, (k + 31) & 31);
-          if (lane == 0) up = k == 0 ? prev_above : b_prev;
-          float n;
-          if (j == 0)
-            n = r == 0 ? v[k] : mnv;
-          else
-            n = v[k] + ref_max(up, prev);
-          v[k] = n;
-          prev = n;
+          if (lane == 0) up[0] = k == 0 ? prev_above : b_prev;
+#pragma unroll
+          for (int m = 0; m < R; ++m) {
+            float n;
+            if (j == 0)
+              n = (m == 0 && r == 0) ? v[m][k] : mnv;
+            else
+              n = v[m][k] + ref_max(up[m], prev[m]);
+            v[m][k] = n;
+            prev[m] = n;
+          }
         }
         prev_above = __shfl_sync(0xffffffffu, bnd, 31);
         // hand the last row to the next warp before writing the tile back
@@ -185,16 +210,18 @@ forward_scores_kernel(float* __restrict__ q, int64_t pitch, int T_cap, int S_cap
           while (consumed[warp + 1] + kRing <= c) __nanosleep(32);
           float* slot = ring[warp][c % kRing];
 #pragma unroll
-          for (int k = 0; k < kTile; ++k) slot[k] = v[k];
+          for (int k = 0; k < kTile; ++k) slot[k] = v[R - 1][k];
           __threadfence_block();
           published[warp] = c + 1;
         }
 #pragma unroll
-        for (int k = 0; k < kTile; ++k) tile[lane][k] = v[k];
+        for (int m = 0; m < R; ++m)
+#pragma unroll
+          for (int k = 0; k < kTile; ++k) tile[lane + 32 * m][k] = v[m][k];
         __syncwarp();
         const bool col_ok = j0 + lane < s;
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
+#pragma unroll 16
+        for (int i = 0; i < kWarpRows; ++i)
           if (col_ok && r0 + i < t) item[static_cast<int64_t>(r0 + i) * pitch + j0 + lane] = tile[i][lane];
         __syncwarp();  // the buffer is refilled by the prefetch two tiles on
         if (publish_down && lane == 0 && ((c + 1) % kStripPub == 0 || c + 1 == ntiles)) {
@@ -272,17 +299,27 @@ int mas_forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_
   if (e == cudaSuccess && lengths)
     e = cudaMemcpyAsync(d_len, lengths, len_bytes, cudaMemcpyHostToDevice, stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(sync, 0, sync_bytes, stream);
-  // A grid that fits the GPU once over is spread one CTA per SM (the
-  // shared-memory request alone keeps a second CTA off): the strips of an
-  // item are latency-bound chains, co-residency only slows them.
+  // A grid that fits the GPU once over runs R = 2 rows per lane spread one
+  // CTA per SM (the shared-memory request alone keeps a second CTA off: the
+  // strips are latency-bound chains, co-residency only slows them); larger
+  // grids run R = 1 with three 8-warp CTAs per SM.
   constexpr int kSpreadSmem = 160 * 1024;
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      forward_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpreadSmem);
-  const int smem = blocks <= sms ? kSpreadSmem : kTileSmem;
-  if (e == cudaSuccess) e = attr;
+  static const cudaError_t attr1 = cudaFuncSetAttribute(
+      forward_scores_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<1>::kTileSmem);
+  static const cudaError_t attr2 = cudaFuncSetAttribute(
+      forward_scores_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpreadSmem);
+  if (e == cudaSuccess) e = attr1 != cudaSuccess ? attr1 : attr2;
   if (e == cudaSuccess) {
-    forward_scores_kernel<<<static_cast<unsigned>(blocks), kWarps * 32, smem, stream>>>(
-        d_values, row_pitch, text_cap, speech_cap, d_len, max_neg_val, nstrips, strips_per_cta, sync, sync + 1);
+    if (blocks <= sms)
+      forward_scores_kernel<2><<<static_cast<unsigned>(blocks), Geo<2>::kWarps * 32, kSpreadSmem,
+                                 stream>>>(d_values, row_pitch, text_cap, speech_cap, d_len,
+                                           max_neg_val, nstrips, strips_per_cta, sync, sync + 1);
+    else
+      forward_scores_kernel<1><<<static_cast<unsigned>(blocks), Geo<1>::kWarps * 32,
+                                 Geo<1>::kTileSmem, stream>>>(d_values, row_pitch, text_cap,
+                                                              speech_cap, d_len, max_neg_val,
+                                                              nstrips, strips_per_cta, sync,
+                                                              sync + 1);
     e = cudaGetLastError();
   }
   if (ws) {
