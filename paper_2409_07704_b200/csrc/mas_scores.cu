@@ -38,6 +38,9 @@ namespace {
 // R rows per lane: lane l owns rows l, l + 32, ... of its warp's 32R-row
 // block; CTAs of 8/R warps, so a strip is 256 rows either way.
 constexpr int kStripRows = 256;
+#ifndef MAS_SCORES_R
+#define MAS_SCORES_R 2  // rows per lane of the spread launch (R = 4 measured 1.6x slower at c3)
+#endif
 constexpr int kStripPub = 8;  // tiles per cross-strip progress release
 constexpr int kTile = 32;
 constexpr int kRing = 4;
@@ -51,6 +54,7 @@ struct Geo {
 };
 static_assert(Geo<1>::kWarps * Geo<1>::kWarpRows == kStripRows, "strip");
 static_assert(Geo<2>::kWarps * Geo<2>::kWarpRows == kStripRows, "strip");
+static_assert(Geo<4>::kWarps * Geo<4>::kWarpRows == kStripRows, "strip");
 
 __device__ __forceinline__ float ref_max(float a, float b) { return a < b ? b : a; }
 
@@ -307,11 +311,11 @@ int mas_forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_
   static const cudaError_t attr1 = cudaFuncSetAttribute(
       forward_scores_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<1>::kTileSmem);
   static const cudaError_t attr2 = cudaFuncSetAttribute(
-      forward_scores_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpreadSmem);
+      forward_scores_kernel<MAS_SCORES_R>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpreadSmem);
   if (e == cudaSuccess) e = attr1 != cudaSuccess ? attr1 : attr2;
   if (e == cudaSuccess) {
     if (blocks <= sms)
-      forward_scores_kernel<2><<<static_cast<unsigned>(blocks), Geo<2>::kWarps * 32, kSpreadSmem,
+      forward_scores_kernel<MAS_SCORES_R><<<static_cast<unsigned>(blocks), Geo<MAS_SCORES_R>::kWarps * 32, kSpreadSmem,
                                  stream>>>(d_values, row_pitch, text_cap, speech_cap, d_len,
                                            max_neg_val, nstrips, strips_per_cta, sync, sync + 1);
     else
