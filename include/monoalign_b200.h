@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define MAS_ABI_VERSION 2
+#define MAS_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define MAS_API __attribute__((visibility("default")))
@@ -206,6 +206,35 @@ MAS_API int mas_generate_device(uint64_t seed, int32_t batch, int32_t text_cap, 
 MAS_API int mas_forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_t text_cap,
                                int32_t speech_cap, const uint32_t* lengths, float max_neg_val,
                                void* stream, mas_error_t* err);
+
+/* ABI 3.  The same table in either engine's arithmetic: engine
+ * MAS_ENGINE_PARALLEL is mas_forward_scores; MAS_ENGINE_REFERENCE is
+ * reference::forward_reference (reference.hpp:33, reference.cpp:9-36): row 0
+ * the running sum 0 + q[0][0] + ... + q[0][j], cells with i > j exactly
+ * max_neg_val, every other cell max(Q[i-1][j-1], Q[i][j-1]) + q[i][j]. */
+MAS_API int mas_forward_scores_ex(float* d_values, int64_t row_pitch, int32_t batch,
+                                  int32_t text_cap, int32_t speech_cap, const uint32_t* lengths,
+                                  int32_t engine, float max_neg_val, void* stream,
+                                  mas_error_t* err);
+
+/* ABI 3.  parallel::backward_parallel / reference::backward_reference
+ * (parallel.hpp:21, reference.hpp:37; the shared walk of backtrack.hpp:21-32):
+ * the argmax walk from (t-1, s-1) to column 0 over a device score table
+ * (either engine's), strict > (ties keep the current row).  d_paths
+ * [batch][speech_cap] int32, -1 past each item's speech length.  The
+ * decisions Q[i-1][j] > Q[i][j] are packed into direction words on the device
+ * and walked by the same backtrack kernel as the maximum-path call.
+ * Stream-ordered. */
+MAS_API int mas_backtrack_scores(const float* d_scores, int64_t row_pitch, int32_t batch,
+                                 int32_t text_cap, int32_t speech_cap, const uint32_t* lengths,
+                                 int32_t* d_paths, void* stream, mas_error_t* err);
+
+/* ABI 3.  parallel::detail::relax_column (parallel.hpp:39, parallel.cpp:25-31)
+ * on device columns: cur[0] += max(sentinel, prev[0]);
+ * cur[i] += max(prev[i-1], prev[i]), max(a, b) = (a < b) ? b : a.
+ * Stream-ordered. */
+MAS_API int mas_relax_column(const float* d_prev, float* d_cur, int32_t lanes, float sentinel,
+                             void* stream, mas_error_t* err);
 
 /* ---- MASTENS v1 tensor files (tensor_io.hpp:11-23, tensor_io.cpp) --------
  * Host-only.  Errors are MAS_E_IO with the reference's IoError code and text

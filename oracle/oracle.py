@@ -38,14 +38,23 @@ ERRC_NAMES = [
 
 
 def build(force: bool = False) -> None:
-    """Build the C oracle, and the reference .so when its sources exist."""
+    """Build the C oracle, and -- when the reference sources exist -- the
+    reference .so and the drop-in programs (the reference's own binding and
+    test suites compiled against include/monoalign/ + libmonoalign_b200.so;
+    the product library must be built first)."""
     targets = ["oracle"]
     if os.path.isdir(REF_SRC):
-        targets.append("ref")
+        targets += ["ref", "dropin"]
     if not os.path.isdir(REF_SRC) and os.path.exists(ORACLE_SO) and not force:
         return  # GPU box: use the prebuilt checkers that travelled with the repo
-    subprocess.run(["make", "-s", "-C", HERE] + (["clean"] if force else []) + targets,
-                   check=True)
+    import sysconfig
+
+    import pybind11
+
+    pyinc = f"-I{pybind11.get_include()} -I{sysconfig.get_paths()['include']}"
+    ext = sysconfig.get_config_var("EXT_SUFFIX")
+    subprocess.run(["make", "-s", "-C", HERE] + (["clean"] if force else []) + targets
+                   + [f"PYINC={pyinc}", f"EXT={ext}"], check=True)
 
 
 class _OracleError(ctypes.Structure):

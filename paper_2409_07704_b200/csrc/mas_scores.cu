@@ -28,10 +28,14 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <algorithm>
+#include <mutex>
+#include <vector>
 
 #include <cuda_runtime.h>
 
 #include "monoalign_b200.h"
+#include "mas_kernels.h"
 
 namespace {
 
@@ -41,6 +45,7 @@ constexpr int kStripRows = 256;
 #ifndef MAS_SCORES_R
 #define MAS_SCORES_R 2  // rows per lane of the spread launch (R = 4 measured 1.6x slower at c3)
 #endif
+constexpr int kSpreadSmem = 160 * 1024;  // one CTA per SM for the spread launch
 constexpr int kStripPub = 8;  // tiles per cross-strip progress release
 constexpr int kTile = 32;
 constexpr int kRing = 4;
@@ -94,7 +99,11 @@ __device__ __forceinline__ void prefetch_tile(float (*buf)[kTile + 1], const flo
   }
 }
 
-template <int R>
+// MODE 0: parallel::forward_parallel (parallel.cpp:95-108).  MODE 1: the
+// reference engine's cache (reference.cpp:9-36): row 0 the running sum
+// 0 + q[0][0] + q[0][1] + ..., cells with i > j stay exactly mnv, every
+// other cell max(Q[i-1][j-1], Q[i][j-1]) + q[i][j].
+template <int R, int MODE>
 __global__ void __launch_bounds__(Geo<R>::kWarps * 32, 1)
 forward_scores_kernel(float* __restrict__ q, int64_t pitch, int T_cap, int S_cap,
                       const uint32_t* __restrict__ lengths, float mnv, int nstrips,
@@ -200,10 +209,20 @@ forward_scores_kernel(float* __restrict__ q, int64_t pitch, int T_cap, int S_cap
 #pragma unroll
           for (int m = 0; m < R; ++m) {
             float n;
-            if (j == 0)
-              n = (m == 0 && r == 0) ? v[m][k] : mnv;
-            else
-              n = v[m][k] + ref_max(up[m], prev[m]);
+            const int row = r + 32 * m;
+            if (MODE == 0) {
+              if (j == 0)
+                n = row == 0 ? v[m][k] : mnv;
+              else
+                n = v[m][k] + ref_max(up[m], prev[m]);
+            } else {
+              if (row == 0)
+                n = (j == 0 ? 0.f : prev[m]) + v[m][k];  // run += q[0][j]
+              else if (j < row)
+                n = mnv;
+              else
+                n = ref_max(up[m], prev[m]) + v[m][k];
+            }
             v[m][k] = n;
             prev[m] = n;
           }
@@ -251,18 +270,52 @@ int fail(mas_error_t* err, int status, int errc, const std::string& msg) {
   return status;
 }
 
-}  // namespace
+// Kernel attributes are per device: set them once on each device before its
+// first launch.
+cudaError_t scores_configure() {
+  constexpr int kMaxDevices = 64;
+  static std::once_flag once[kMaxDevices];
+  static cudaError_t status[kMaxDevices];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::call_once(once[dev], [dev] {
+    cudaError_t r = cudaSuccess;
+    const void* spread[2] = {reinterpret_cast<const void*>(forward_scores_kernel<MAS_SCORES_R, 0>),
+                             reinterpret_cast<const void*>(forward_scores_kernel<MAS_SCORES_R, 1>)};
+    const void* dense[2] = {reinterpret_cast<const void*>(forward_scores_kernel<1, 0>),
+                            reinterpret_cast<const void*>(forward_scores_kernel<1, 1>)};
+    for (int m = 0; m < 2 && r == cudaSuccess; ++m) {
+      r = cudaFuncSetAttribute(dense[m], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Geo<1>::kTileSmem);
+      if (r == cudaSuccess)
+        r = cudaFuncSetAttribute(spread[m], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSpreadSmem);
+    }
+    status[dev] = r;
+  });
+  return status[dev];
+}
 
-extern "C" {
+int sm_count() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
 
-int mas_forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_t text_cap,
-                       int32_t speech_cap, const uint32_t* lengths, float max_neg_val,
-                       void* stream_v, mas_error_t* err) {
+void clear(mas_error_t* err) {
   if (err) {
     std::memset(err, 0, sizeof(*err));
     err->item = -1;
     err->i = err->j = -1;
   }
+}
+
+// Shape checks shared by the score-table entry points.
+int check_table(int64_t row_pitch, int32_t batch, int32_t text_cap, int32_t speech_cap,
+                const uint32_t* lengths, mas_error_t* err) {
   if (batch < 1 || text_cap < 1 || speech_cap < 1)
     return fail(err, MAS_E_VALIDATION, MAS_ERRC_ZERO_DIM, "batch and capacities must be at least 1");
   if (row_pitch < speech_cap)
@@ -277,27 +330,72 @@ int mas_forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_
         if (err) err->item = b;
         return rc;
       }
+  return MAS_OK;
+}
+
+// Direction words of a score table in the backtrack kernel's layout
+// (DESIGN.md 2): word m of row i holds the decisions of columns
+// 32m-1 ... 32m+30, column 32m+p-1 at bit 31-p, bit(i, c) = Q[i-1][c] > Q[i][c]
+// (the strict compare of backtrack.hpp:26); row 0, column -1 and cells past
+// the item's lengths are 0.  One warp per (item, row, word): lane p reads
+// column 32m+p-1 of rows i-1 and i (coalesced), the ballot is the word.
+__global__ void scores_to_dirs_kernel(const float* __restrict__ q, int64_t pitch, int T_cap,
+                                      int S_cap, const uint32_t* __restrict__ lengths, int M,
+                                      int T_alloc, int B, uint32_t* __restrict__ dirs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t total = static_cast<int64_t>(B) * M * T_alloc;
+  for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < total;
+       w += nwarps) {
+    const int i = static_cast<int>(w % T_alloc);
+    const int64_t bm = w / T_alloc;
+    const int m = static_cast<int>(bm % M);
+    const int b = static_cast<int>(bm / M);
+    const int t = lengths ? static_cast<int>(lengths[2 * b]) : T_cap;
+    const int s = lengths ? static_cast<int>(lengths[2 * b + 1]) : S_cap;
+    const int c = 32 * m + lane - 1;
+    bool bit = false;
+    if (i >= 1 && i < t && c >= 0 && c < s) {
+      const float* row = q + (static_cast<int64_t>(b) * T_cap + i) * pitch;
+      bit = row[c - pitch] > row[c];
+    }
+    const uint32_t word = __brev(__ballot_sync(0xffffffffu, bit));
+    if (lane == 0) dirs[w] = word;  // w = (b * M + m) * T_alloc + i
+  }
+}
+
+// parallel::detail::relax_column (parallel.cpp:25-31): one thread per text lane.
+__global__ void relax_column_kernel(const float* __restrict__ prev, float* __restrict__ cur,
+                                    int lanes, float sentinel) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < lanes; i += gridDim.x * blockDim.x)
+    cur[i] += ref_max(i == 0 ? sentinel : prev[i - 1], prev[i]);
+}
+
+int forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_t text_cap,
+                   int32_t speech_cap, const uint32_t* lengths, int mode, float max_neg_val,
+                   void* stream_v, mas_error_t* err) {
+  clear(err);
+  int rc = check_table(row_pitch, batch, text_cap, speech_cap, lengths, err);
+  if (rc != MAS_OK) return rc;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   const int nstrips = (text_cap + kStripRows - 1) / kStripRows;
   // Strips run concurrently (one CTA each, handing rows down through L2)
   // while the batch alone would not fill the GPU; otherwise each CTA walks
   // its item's strips in order and the hand-downs are all local.
-  int sms = 148;
-  {
-    int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess)
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = sm_count();
   const int strips_per_cta = batch >= sms ? nstrips : 1;
   const int64_t blocks = static_cast<int64_t>(batch) * ((nstrips + strips_per_cta - 1) / strips_per_cta);
   const int64_t nprogress = static_cast<int64_t>(batch) * nstrips;
   if (blocks > 0x7fffffff)
     return fail(err, MAS_E_UNSUPPORTED, -1, "forward_scores: batch x strips exceeds the grid");
+  cudaError_t e = scores_configure();
+  if (e != cudaSuccess)
+    return fail(err, MAS_E_CUDA, -1, std::string("forward_scores: ") + cudaGetErrorString(e));
   // workspace: [B][2] uint32 lengths | ticket | progress[B * nstrips]
   const size_t len_bytes = lengths ? static_cast<size_t>(batch) * 2 * sizeof(uint32_t) : 0;
   const size_t sync_bytes = (1 + static_cast<size_t>(nprogress)) * sizeof(int);
   char* ws = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), len_bytes + sync_bytes, stream);
+  e = cudaMallocAsync(reinterpret_cast<void**>(&ws), len_bytes + sync_bytes, stream);
   uint32_t* d_len = lengths ? reinterpret_cast<uint32_t*>(ws) : nullptr;
   int* sync = reinterpret_cast<int*>(ws + len_bytes);
   if (e == cudaSuccess && lengths)
@@ -307,23 +405,19 @@ int mas_forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_
   // CTA per SM (the shared-memory request alone keeps a second CTA off: the
   // strips are latency-bound chains, co-residency only slows them); larger
   // grids run R = 1 with three 8-warp CTAs per SM.
-  constexpr int kSpreadSmem = 160 * 1024;
-  static const cudaError_t attr1 = cudaFuncSetAttribute(
-      forward_scores_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<1>::kTileSmem);
-  static const cudaError_t attr2 = cudaFuncSetAttribute(
-      forward_scores_kernel<MAS_SCORES_R>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpreadSmem);
-  if (e == cudaSuccess) e = attr1 != cudaSuccess ? attr1 : attr2;
   if (e == cudaSuccess) {
-    if (blocks <= sms)
-      forward_scores_kernel<MAS_SCORES_R><<<static_cast<unsigned>(blocks), Geo<MAS_SCORES_R>::kWarps * 32, kSpreadSmem,
-                                 stream>>>(d_values, row_pitch, text_cap, speech_cap, d_len,
-                                           max_neg_val, nstrips, strips_per_cta, sync, sync + 1);
-    else
-      forward_scores_kernel<1><<<static_cast<unsigned>(blocks), Geo<1>::kWarps * 32,
-                                 Geo<1>::kTileSmem, stream>>>(d_values, row_pitch, text_cap,
-                                                              speech_cap, d_len, max_neg_val,
-                                                              nstrips, strips_per_cta, sync,
-                                                              sync + 1);
+    const unsigned g = static_cast<unsigned>(blocks);
+    if (blocks <= sms) {
+      auto k = mode ? forward_scores_kernel<MAS_SCORES_R, 1> : forward_scores_kernel<MAS_SCORES_R, 0>;
+      k<<<g, Geo<MAS_SCORES_R>::kWarps * 32, kSpreadSmem, stream>>>(
+          d_values, row_pitch, text_cap, speech_cap, d_len, max_neg_val, nstrips, strips_per_cta,
+          sync, sync + 1);
+    } else {
+      auto k = mode ? forward_scores_kernel<1, 1> : forward_scores_kernel<1, 0>;
+      k<<<g, Geo<1>::kWarps * 32, Geo<1>::kTileSmem, stream>>>(
+          d_values, row_pitch, text_cap, speech_cap, d_len, max_neg_val, nstrips, strips_per_cta,
+          sync, sync + 1);
+    }
     e = cudaGetLastError();
   }
   if (ws) {
@@ -332,6 +426,100 @@ int mas_forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_
   }
   if (e != cudaSuccess)
     return fail(err, MAS_E_CUDA, -1, std::string("forward_scores: ") + cudaGetErrorString(e));
+  return MAS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mas_forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_t text_cap,
+                       int32_t speech_cap, const uint32_t* lengths, float max_neg_val,
+                       void* stream, mas_error_t* err) {
+  return forward_scores(d_values, row_pitch, batch, text_cap, speech_cap, lengths, 0, max_neg_val,
+                        stream, err);
+}
+
+int mas_forward_scores_ex(float* d_values, int64_t row_pitch, int32_t batch, int32_t text_cap,
+                          int32_t speech_cap, const uint32_t* lengths, int32_t engine,
+                          float max_neg_val, void* stream, mas_error_t* err) {
+  if (engine != MAS_ENGINE_REFERENCE && engine != MAS_ENGINE_PARALLEL) {
+    clear(err);
+    return fail(err, MAS_E_VALIDATION, MAS_ERRC_INVALID_CONFIG, "unknown engine");
+  }
+  return forward_scores(d_values, row_pitch, batch, text_cap, speech_cap, lengths,
+                        engine == MAS_ENGINE_REFERENCE ? 1 : 0, max_neg_val, stream, err);
+}
+
+int mas_backtrack_scores(const float* d_scores, int64_t row_pitch, int32_t batch, int32_t text_cap,
+                         int32_t speech_cap, const uint32_t* lengths, int32_t* d_paths,
+                         void* stream_v, mas_error_t* err) {
+  clear(err);
+  int rc = check_table(row_pitch, batch, text_cap, speech_cap, lengths, err);
+  if (rc != MAS_OK) return rc;
+  if (!d_paths) return MAS_OK;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  // The backtrack kernel's window copies need 16-byte row groups: rows per
+  // item padded to a multiple of 16, windows of up to 256 rows.
+  const int T_alloc = (text_cap + 15) & ~15;
+  const int M = (speech_cap + 31) / 32;
+  const size_t len_bytes = static_cast<size_t>(batch) * 2 * sizeof(uint32_t);
+  const size_t dir_bytes = static_cast<size_t>(batch) * M * T_alloc * sizeof(uint32_t);
+  std::vector<uint32_t> full;
+  if (!lengths) {
+    full.resize(static_cast<size_t>(batch) * 2);
+    for (int32_t b = 0; b < batch; ++b) {
+      full[2 * b] = static_cast<uint32_t>(text_cap);
+      full[2 * b + 1] = static_cast<uint32_t>(speech_cap);
+    }
+    lengths = full.data();
+  }
+  char* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), dir_bytes + len_bytes, stream);
+  uint32_t* d_dirs = reinterpret_cast<uint32_t*>(ws);
+  uint32_t* d_len = reinterpret_cast<uint32_t*>(ws + dir_bytes);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_len, lengths, len_bytes, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) {
+    const int64_t warps = static_cast<int64_t>(batch) * M * T_alloc;
+    const int64_t blocks = std::min<int64_t>((warps + 7) / 8, static_cast<int64_t>(sm_count()) * 16);
+    scores_to_dirs_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        d_scores, row_pitch, text_cap, speech_cap, d_len, M, T_alloc, batch, d_dirs);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) {
+    mas::BtArgs ba = {};
+    ba.b0 = 0;
+    ba.lengths = d_len;
+    ba.dirs = d_dirs;
+    ba.path = d_paths;
+    ba.B = batch;
+    ba.T_cap = text_cap;
+    ba.S_cap = speech_cap;
+    ba.M = M;
+    ba.T_alloc = T_alloc;
+    ba.R = std::min(256, T_alloc);
+    e = mas::launch_backtrack(ba, stream, nullptr);
+  }
+  if (ws) {
+    const cudaError_t f = cudaFreeAsync(ws, stream);
+    if (e == cudaSuccess) e = f;
+  }
+  if (e != cudaSuccess)
+    return fail(err, MAS_E_CUDA, -1, std::string("backtrack_scores: ") + cudaGetErrorString(e));
+  return MAS_OK;
+}
+
+int mas_relax_column(const float* d_prev, float* d_cur, int32_t lanes, float sentinel,
+                     void* stream_v, mas_error_t* err) {
+  clear(err);
+  if (lanes < 1) return MAS_OK;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  const int blocks = std::min((lanes + 255) / 256, sm_count() * 8);
+  relax_column_kernel<<<blocks, 256, 0, stream>>>(d_prev, d_cur, lanes, sentinel);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return fail(err, MAS_E_CUDA, -1, std::string("relax_column: ") + cudaGetErrorString(e));
   return MAS_OK;
 }
 

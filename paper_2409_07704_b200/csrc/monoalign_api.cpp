@@ -76,6 +76,72 @@ AlignmentMatrix run(const LikelihoodBatch& batch, const MasConfig& cfg, bool unc
   return out;
 }
 
+
+// Device scratch for the table round trips below (forward_parallel,
+// forward_reference, backward_*, relax_column): stream-ordered on the calling
+// thread's per-thread stream, freed on scope exit.
+class DeviceScratch {
+ public:
+  explicit DeviceScratch(std::size_t bytes) : stream_(cudaStreamPerThread) {
+    if (bytes) check(cudaMallocAsync(&p_, bytes, stream_));
+  }
+  ~DeviceScratch() {
+    if (p_) cudaFreeAsync(p_, stream_);
+    cudaStreamSynchronize(stream_);
+  }
+  DeviceScratch(const DeviceScratch&) = delete;
+  DeviceScratch& operator=(const DeviceScratch&) = delete;
+  template <typename T>
+  T* as(std::size_t byte_offset = 0) const {
+    return reinterpret_cast<T*>(static_cast<char*>(p_) + byte_offset);
+  }
+  cudaStream_t stream() const { return stream_; }
+  static void check(cudaError_t e) {
+    if (e != cudaSuccess)
+      throw DeviceError(std::string("monoalign device path failed: ") + cudaGetErrorString(e));
+  }
+  void sync() const { check(cudaStreamSynchronize(stream_)); }
+
+ private:
+  void* p_ = nullptr;
+  cudaStream_t stream_;
+};
+
+// Host -> device copy of a [t][s] table with row stride `src_stride` into a
+// dense [t][dst_pitch] device table.
+void put_table(float* d, std::ptrdiff_t dst_pitch, const float* h, std::ptrdiff_t src_stride,
+               int t, int s, cudaStream_t st) {
+  DeviceScratch::check(cudaMemcpy2DAsync(d, dst_pitch * sizeof(float), h,
+                                         src_stride * sizeof(float), s * sizeof(float), t,
+                                         cudaMemcpyHostToDevice, st));
+}
+
+void get_table(float* h, std::ptrdiff_t dst_stride, const float* d, std::ptrdiff_t src_pitch,
+               int t, int s, cudaStream_t st) {
+  DeviceScratch::check(cudaMemcpy2DAsync(h, dst_stride * sizeof(float), d,
+                                         src_pitch * sizeof(float), s * sizeof(float), t,
+                                         cudaMemcpyDeviceToHost, st));
+}
+
+// The shared backtrack walk (backtrack.hpp:21-32) over a host score table:
+// the table goes to the device, the walk runs there (mas_backtrack_scores).
+PathVector walk_scores(const float* scores, std::ptrdiff_t row_stride, int t, int s) {
+  if (t < 1 || s < 1) return PathVector(static_cast<std::size_t>(s > 0 ? s : 0), 0);
+  const std::size_t table = static_cast<std::size_t>(t) * s * sizeof(float);
+  DeviceScratch d(table + static_cast<std::size_t>(s) * sizeof(int32_t));
+  float* dq = d.as<float>();
+  int32_t* dpath = d.as<int32_t>(table);
+  put_table(dq, s, scores, row_stride, t, s, d.stream());
+  mas_error_t err;
+  const int rc = mas_backtrack_scores(dq, s, 1, t, s, nullptr, dpath, d.stream(), &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+  PathVector path(static_cast<std::size_t>(s));
+  DeviceScratch::check(cudaMemcpyAsync(path.data(), dpath, s * sizeof(int32_t),
+                                       cudaMemcpyDeviceToHost, d.stream()));
+  d.sync();
+  return path;
+}
+
 }  // namespace
 
 const char* errc_name(Errc code) { return mas_errc_name(static_cast<int32_t>(code)); }
@@ -210,28 +276,34 @@ void forward_parallel(MutableLikelihoodView q, const MasConfig& cfg) {
   // The item round-trips through device memory; forward_scores_kernel
   // computes the table (mas_forward_scores), nothing is computed here.
   if (q.text < 1 || q.speech < 1) return;
-  const size_t row_bytes = static_cast<size_t>(q.speech) * sizeof(float);
-  const size_t bytes = row_bytes * q.text;
-  float* d = nullptr;
-  auto check = [&](cudaError_t e) {
-    if (e != cudaSuccess) {
-      if (d) cudaFree(d);
-      throw DeviceError(std::string("monoalign device path failed: ") + cudaGetErrorString(e));
-    }
-  };
-  check(cudaMalloc(reinterpret_cast<void**>(&d), bytes));
-  check(cudaMemcpy2D(d, row_bytes, q.data, q.row_stride * sizeof(float), row_bytes, q.text,
-                     cudaMemcpyHostToDevice));
+  DeviceScratch d(static_cast<std::size_t>(q.text) * q.speech * sizeof(float));
+  float* dq = d.as<float>();
+  put_table(dq, q.speech, q.data, q.row_stride, q.text, q.speech, d.stream());
   mas_error_t err;
-  const int rc = mas_forward_scores(d, q.speech, 1, q.text, q.speech, nullptr, cfg.max_neg_val,
-                                    nullptr, &err);
-  if (rc != MAS_OK) {
-    cudaFree(d);
-    throw_for(rc, err);
-  }
-  check(cudaMemcpy2D(q.data, q.row_stride * sizeof(float), d, row_bytes, row_bytes, q.text,
-                     cudaMemcpyDeviceToHost));
-  cudaFree(d);
+  const int rc = mas_forward_scores(dq, q.speech, 1, q.text, q.speech, nullptr, cfg.max_neg_val,
+                                    d.stream(), &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+  get_table(q.data, q.row_stride, dq, q.speech, q.text, q.speech, d.stream());
+  d.sync();
+}
+
+PathVector backward_parallel(const LikelihoodView& scores) {
+  return walk_scores(scores.data, scores.row_stride, scores.text, scores.speech);
+}
+
+void detail::relax_column(const float* prev, float* cur, int lanes, float sentinel) {
+  if (lanes < 1) return;
+  const std::size_t col = static_cast<std::size_t>(lanes) * sizeof(float);
+  DeviceScratch d(2 * col);
+  float* dprev = d.as<float>();
+  float* dcur = d.as<float>(col);
+  DeviceScratch::check(cudaMemcpyAsync(dprev, prev, col, cudaMemcpyHostToDevice, d.stream()));
+  DeviceScratch::check(cudaMemcpyAsync(dcur, cur, col, cudaMemcpyHostToDevice, d.stream()));
+  mas_error_t err;
+  const int rc = mas_relax_column(dprev, dcur, lanes, sentinel, d.stream(), &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+  DeviceScratch::check(cudaMemcpyAsync(cur, dcur, col, cudaMemcpyDeviceToHost, d.stream()));
+  d.sync();
 }
 
 AlignmentMatrix align_parallel(const LikelihoodBatch& batch, const MasConfig& cfg) {
@@ -249,6 +321,32 @@ AlignmentMatrix detail::align_unchecked(const LikelihoodBatch& batch, const MasC
 }  // namespace parallel
 
 namespace reference {
+
+QCache forward_reference(const LikelihoodView& q, const MasConfig& cfg) {
+  const int t = q.text;
+  const int s = q.speech;
+  // reference.cpp:12-15: an odd multiple of 16 floats
+  int stride = (s + 15) & ~15;
+  if ((stride / 16) % 2 == 0) stride += 16;
+  QCache cache{t, s, stride,
+               std::vector<float>(static_cast<std::size_t>(t > 0 ? t : 0) * stride,
+                                  cfg.max_neg_val)};
+  if (t < 1 || s < 1) return cache;
+  DeviceScratch d(static_cast<std::size_t>(t) * stride * sizeof(float));
+  float* dq = d.as<float>();
+  put_table(dq, stride, q.data, q.row_stride, t, s, d.stream());
+  mas_error_t err;
+  const int rc = mas_forward_scores_ex(dq, stride, 1, t, s, nullptr, MAS_ENGINE_REFERENCE,
+                                       cfg.max_neg_val, d.stream(), &err);
+  if (rc != MAS_OK) throw_for(rc, err);
+  get_table(cache.values.data(), stride, dq, stride, t, s, d.stream());
+  d.sync();
+  return cache;
+}
+
+PathVector backward_reference(const QCache& cache) {
+  return walk_scores(cache.values.data(), cache.stride, cache.text, cache.speech);
+}
 
 AlignmentMatrix align_reference(const LikelihoodBatch& batch, const MasConfig& cfg) {
   MasConfig c = cfg;
