@@ -22,7 +22,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 HOST_CXX = "/usr/bin/g++"  # dynamic libstdc++ 
 
 SOURCES = ["mas_abi.cu", "mas_fwd.cu", "mas_fwd4.cu", "mas_bt.cu", "monoalign_api.cpp",
-           "mas_io.cpp", "mas_scores.cu"]
+           "mas_io.cpp", "mas_scores.cu", "mas_bench.cpp"]
+CLI = os.path.join(LIBDIR, "monoalign")  # the `monoalign` command line (tools/main.cpp surface)
 HEADERS = ["mas_kernels.h", "mas_ptx.cuh"]
 
 
@@ -41,6 +42,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     """Compiles the library (``out``; ``defines`` are extra -D macros for
     experiment variants built next to the product library)."""
     if out == LIB and not defines and not force and not _stale():
+        build_cli()
         return out
     os.makedirs(os.path.dirname(out), exist_ok=True)
     cmd = [
@@ -56,7 +58,24 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
         raise RuntimeError("nvcc build of libmonoalign_b200.so failed")
     if verbose:
         sys.stderr.write(res.stderr)
+    if out == LIB:
+        build_cli(force=True)
     return out
+
+
+def build_cli(force: bool = False) -> str:
+    """The `monoalign` command line (csrc/mas_cli.cpp), linked to the library."""
+    src = os.path.join(CSRC, "mas_cli.cpp")
+    if not force and os.path.exists(CLI) and os.path.getmtime(CLI) >= max(
+            os.path.getmtime(src), os.path.getmtime(LIB)):
+        return CLI
+    cmd = [HOST_CXX, "-std=c++20", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+           src, "-L", LIBDIR, "-lmonoalign_b200", "-Wl,-rpath,$ORIGIN", "-o", CLI]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("build of the monoalign CLI failed")
+    return CLI
 
 
 if __name__ == "__main__":

@@ -31,7 +31,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 DROP = os.path.join(ROOT, "oracle", "_ref", "dropin")
 UNIT = os.path.join(DROP, "unit")
 SMOKE = os.path.join(DROP, "tests", "test_smoke.py")
-SUITES = ["test_types", "test_reference", "test_parallel", "test_io", "test_oracle"]
+SUITES = ["test_types", "test_reference", "test_parallel", "test_io", "test_oracle", "test_bench"]
+ACCEPT = os.path.join(DROP, "acceptance")
+CLI_TESTS = os.path.join(DROP, "cli_tests")
+CLI = os.path.join(ROOT, "paper_2409_07704_b200", "_lib", "monoalign")
 
 
 def _binding():
@@ -45,7 +48,7 @@ def _binding():
 
 
 def _need_dropin():
-    if not (os.path.exists(UNIT) and _binding() and os.path.exists(SMOKE)):
+    if not all(os.path.exists(p) for p in (UNIT, SMOKE, ACCEPT, CLI_TESTS)) or not _binding():
         pytest.skip("drop-in programs not built (oracle/Makefile dropin needs /root/reference "
                     "at build time)")
 
@@ -57,7 +60,7 @@ def _needed(path):
 
 def test_dropin_programs_link_our_library_only():
     _need_dropin()
-    for path in (UNIT, _binding()):
+    for path in (UNIT, ACCEPT, CLI_TESTS, _binding()):
         needed = _needed(path)
         assert "libmonoalign_b200.so" in needed, (path, needed)
         assert not any("monoalign_ref" in n or "monoalign_core" in n for n in needed), needed
@@ -117,3 +120,45 @@ def test_reference_unit_suite(cuda, suite):
     assert res.returncode == 0, res.stdout + res.stderr
     assert "failed checks: 0" in res.stdout, res.stdout + res.stderr
     assert "test cases: 0," not in res.stdout
+
+
+@pytest.mark.gpu
+def test_reference_acceptance(cuda):
+    """proj/tests/acceptance.cpp (8 criteria: exhaustive oracle over 1000
+    instances, engine equivalence over 1000 + 100 + 50 batches, invariants,
+    sentinel adversarial, scaling law, speedup (soft), IO, trivia)."""
+    _need_dropin()
+    res = subprocess.run([ACCEPT], capture_output=True, text=True, timeout=1800)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "acceptance: all gated criteria passed" in res.stdout, res.stdout
+
+
+@pytest.mark.gpu
+def test_reference_cli_driver(cuda):
+    """proj/tests/cli_driver.cpp against this repo's `monoalign` CLI."""
+    _need_dropin()
+    res = subprocess.run([CLI_TESTS], capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "failed checks: 0" in res.stdout
+
+
+def _cli(*args):
+    return subprocess.run([CLI, *args], capture_output=True, text=True, timeout=60)
+
+
+@pytest.mark.parametrize("args,code", [
+    ((), 2), (("frobnicate",), 2), (("--help",), 0), (("align", "--help"), 0),
+    (("verify", "--t-max", "7"), 2), (("verify", "--s-max", "11"), 2), (("verify", "--t-max", "0"), 2),
+    (("align", "--input", "a", "--output", "b", "--engine", "turbo"), 2),
+    (("align", "--input", "a"), 2),
+    (("bench", "--engines", "turbo", "--t-values", "8"), 2),
+    (("bench", "--t-values", "8", "--repeats", "0"), 2),
+    (("bench", "--format", "xml"), 2),
+    (("align", "--input", "/no/such/file.bin", "--output", "/tmp/x.bin"), 1),
+])
+def test_cli_usage_and_exit_codes(args, code):
+    """tools/main.cpp exit codes that need no device (usage 2, IO 1)."""
+    from paper_2409_07704_b200 import build as b
+
+    b.build()
+    assert _cli(*args).returncode == code, args
