@@ -246,9 +246,13 @@ MAS_API int mas_relax_column(const float* d_prev, float* d_cur, int32_t lanes, f
 MAS_API int mas_io_read_header(const char* path, uint64_t byte_budget, int32_t* dtype,
                                int64_t dims[3], int32_t* lengths_present, mas_error_t* err);
 /* Payload into `values` (dims product x dtype size bytes) and the lengths
- * table into `lengths` [B][2] (full lengths when the file has none). */
-MAS_API int mas_io_read(const char* path, uint64_t byte_budget, void* values, uint32_t* lengths,
-                        mas_error_t* err);
+ * table into `lengths` [B][2] (full lengths when the file has none).
+ * `dtype` / `dims` are what mas_io_read_header returned and what the buffers
+ * were sized for; a file whose header no longer matches them (replaced
+ * between the two calls) is rejected with IoFailure before anything is
+ * written (ABI 3). */
+MAS_API int mas_io_read(const char* path, uint64_t byte_budget, int32_t dtype, const int64_t dims[3],
+                        void* values, uint32_t* lengths, mas_error_t* err);
 /* write_tensor: header, payload, lengths table ([B][2] or NULL = full). */
 MAS_API int mas_io_write(const char* path, int32_t dtype, int64_t batch, int64_t text_cap,
                          int64_t speech_cap, const void* values, const uint32_t* lengths,

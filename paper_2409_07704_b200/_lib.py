@@ -96,7 +96,8 @@ _SIGS = {
                                           ctypes.POINTER(ctypes.c_int32),
                                           ctypes.POINTER(ctypes.c_int64 * 3),
                                           ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(MasError)]),
-    "mas_io_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint64, _VP, _VP,
+    "mas_io_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int32,
+                                   ctypes.POINTER(ctypes.c_int64 * 3), _VP, _VP,
                                    ctypes.POINTER(MasError)]),
     "mas_io_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int64,
                                     ctypes.c_int64, ctypes.c_int64, _VP, _VP,
@@ -104,6 +105,14 @@ _SIGS = {
     "mas_forward_scores": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int32, _VP, ctypes.c_float, _VP,
                                           ctypes.POINTER(MasError)]),
+    "mas_forward_scores_ex": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                             ctypes.c_int32, _VP, ctypes.c_int32, ctypes.c_float,
+                                             _VP, ctypes.POINTER(MasError)]),
+    "mas_backtrack_scores": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                            ctypes.c_int32, _VP, _VP, _VP,
+                                            ctypes.POINTER(MasError)]),
+    "mas_relax_column": (ctypes.c_int, [_VP, _VP, ctypes.c_int32, ctypes.c_float, _VP,
+                                        ctypes.POINTER(MasError)]),
     "mas_errc_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "mas_abi_version": (ctypes.c_int, []),
 }

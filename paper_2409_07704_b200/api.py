@@ -226,8 +226,8 @@ def read_tensor(path):
     shape = (dims[0], dims[1], dims[2])
     values = np.empty(shape, np.float32 if dtype.value == 0 else np.uint8)
     lengths = np.empty((dims[0], 2), np.uint32)
-    rc = lib.mas_io_read(p, _lib.MAS_IO_DEFAULT_BYTE_BUDGET, values.ctypes.data,
-                         lengths.ctypes.data, ctypes.byref(err))
+    rc = lib.mas_io_read(p, _lib.MAS_IO_DEFAULT_BYTE_BUDGET, dtype.value, ctypes.byref(dims),
+                         values.ctypes.data, lengths.ctypes.data, ctypes.byref(err))
     _lib.raise_for(rc, err)
     return values, lengths
 

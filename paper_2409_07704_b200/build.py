@@ -1,6 +1,6 @@
 """Builds the in-tree CUDA library ``_lib/libmonoalign_b200.so`` for sm_100a.
 
-One shared object holds the kernels (csrc/mas_fwd.cu, csrc/mas_bt.cu), the
+One shared object holds the kernels (csrc/mas_fwd4.cu, csrc/mas_bt.cu, csrc/mas_scores.cu), the
 extern "C" boundary (csrc/mas_abi.cu, include/monoalign_b200.h) and the C++
 mirror of the reference API (csrc/monoalign_api.cpp, include/monoalign/).
 The CUDA runtime is linked statically so the library does not clash with
@@ -21,7 +21,7 @@ LIB = os.path.join(LIBDIR, "libmonoalign_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 HOST_CXX = "/usr/bin/g++"  # dynamic libstdc++ 
 
-SOURCES = ["mas_abi.cu", "mas_fwd.cu", "mas_fwd4.cu", "mas_bt.cu", "monoalign_api.cpp",
+SOURCES = ["mas_abi.cu", "mas_fwd4.cu", "mas_bt.cu", "monoalign_api.cpp",
            "mas_io.cpp", "mas_scores.cu", "mas_bench.cpp"]
 CLI = os.path.join(LIBDIR, "monoalign")  # the `monoalign` command line (tools/main.cpp surface)
 HEADERS = ["mas_kernels.h", "mas_ptx.cuh"]

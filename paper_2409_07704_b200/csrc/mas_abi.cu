@@ -157,63 +157,13 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// Map r (r = 0, 1) views rows {2k + r} of the whole [B*T_pad][pitch] input
-// as a 2-D tensor [B*T_pad/2][S_cap] with row stride 2*pitch, 32x32 boxes,
-// 128-byte swizzle.
-bool encode_maps(const float* q, int64_t pitch, int64_t rows_total, int64_t S, CUtensorMap* m0,
-                 CUtensorMap* m1) {
-  EncodeTiledFn enc = get_encode_fn();
-  if (!enc) return false;
-  for (int r = 0; r < 2; ++r) {
-    CUtensorMap* m = r == 0 ? m0 : m1;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(rows_total / 2)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * pitch * 4)};
-    const cuuint32_t box[2] = {32, 32};
-    const cuuint32_t estr[2] = {1, 1};
-    void* addr = const_cast<float*>(q + r * pitch);
-    const CUresult res = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, addr, dims, strides, box, estr,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (res != CUDA_SUCCESS) return false;
-  }
-  return true;
-}
-
-// The uint8 output [B*T_cap][S_cap] as a 2-D tensor with 32 x 64 boxes: the
-// forward kernel TMA-stores zero tiles through it.
-bool encode_out_map(uint8_t* out, int64_t rows, int64_t S, CUtensorMap* m) {
-  EncodeTiledFn enc = get_encode_fn();
-  if (!enc) return false;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(rows)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(S)};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(mas::kStageCols),
-                             static_cast<cuuint32_t>(mas::kRowsPerWarp)};
-  const cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, out, dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 
 struct Geometry {
-  int R = 4;            // text rows per lane of mas_fwd4.cu: 4 (default) or 2
-  bool legacy = false;  // mas_fwd.cu (two rows per lane, MAS_FWD=old)
+  int R = 4;            // text rows per lane of mas_fwd4.cu
   int W = 1, K = 1, N = 2, L = 256, Kseg = 1, T_alloc = 128, M = 1;
   int bands = 1;       // mas_fwd4: launches of K*W*128 rows each (text longer than a cluster)
   int band_rows = 128;
 };
-
-// K1 selection (A/B switch): MAS_FWD=4 / 2 picks the rows per lane of
-// mas_fwd4.cu, MAS_FWD=old the legacy mas_fwd.cu; default 4.
-int forward_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("MAS_FWD");
-    if (e && std::strcmp(e, "old") == 0) return 0;
-    return e && e[0] == '2' ? 2 : 4;
-  }();
-  return v;
-}
 
 bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
   int sms = 148;
@@ -223,13 +173,11 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const size_t budget = 220 * 1024;
-  const int variant = forward_variant();
-  g->legacy = variant == 0;
-  g->R = g->legacy ? 2 : variant;
+  g->R = 4;
   g->M = (S_cap + 31) / 32;
   g->L = 256;
   g->Kseg = (S_cap + g->L - 1) / g->L;
-  if (!g->legacy) {
+  {
     // 32 R rows per warp; an item's warps form `bands` clusters of K CTAs of
     // W compute warps, all in one launch (mas_fwd4.cu, bands).  Candidates
     // (W, stages) in order of preference (few warps per CTA spread an item
@@ -246,8 +194,7 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
     const int rows = 32 * g->R;
     const int warps_total = std::max(1, (t_max + rows - 1) / rows);
     static const int cand4[][2] = {{2, 4}, {4, 3}, {2, 3}, {1, 4}, {2, 2}, {4, 2}, {1, 2}};
-    static const int cand2[][2] = {{4, 4}, {4, 3}, {2, 4}, {2, 3}, {4, 2}, {1, 4}, {1, 2}};
-    const int(*cand)[2] = g->R == 4 ? cand4 : cand2;
+    const int(*cand)[2] = cand4;
     const int ncand = 7;
     int best = -1;
     int64_t best_waves = 0;
@@ -283,26 +230,6 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
     g->T_alloc = g->bands * g->band_rows;
     return true;
   }
-  const int warps = std::max(1, (t_max + mas::kRowsPerWarp - 1) / mas::kRowsPerWarp);
-  // One warp per SM sub-partition (4 per CTA), clusters of up to 16 CTAs;
-  // 6 warps x 2 stages for the longest texts.
-  if (warps <= 4) {
-    g->K = 1;
-    g->W = warps;
-  } else if (warps <= 4 * mas::kMaxClusterCtas) {
-    g->W = 4;
-    g->K = (warps + 3) / 4;
-  } else if (warps <= 6 * mas::kMaxClusterCtas) {
-    g->W = 6;
-    g->K = (warps + 5) / 6;
-  } else {
-    return false;
-  }
-  int N = 8;
-  while (N > 2 && mas::fwd_smem_bytes(g->W, N) > budget) --N;
-  g->N = N;
-  g->T_alloc = g->K * g->W * mas::kRowsPerWarp;
-  return true;
 }
 
 // choose_geometry queries the occupancy API for every candidate (tens of
@@ -368,23 +295,45 @@ bool encode_out_map4(uint8_t* out, int64_t rows, int64_t S, int R, CUtensorMap* 
 
 }  // namespace
 
-// Device memory comes from the device's default stream-ordered pool, with
-// the release threshold raised once so repeated calls reuse it instead of
-// re-mapping pages (and cudaFree's device-wide synchronisation is avoided).
-cudaError_t pool_setup(int dev) {
+// Device memory comes from a stream-ordered pool owned by this library (one
+// per device) whose release threshold is raised, so repeated calls reuse it
+// instead of re-mapping pages (and cudaFree's device-wide synchronisation is
+// avoided).  A private pool leaves the device's default pool -- which torch
+// (cudaMallocAsync backend), CuPy or the caller may use -- untouched.
+namespace {
+cudaError_t device_pool(int dev, cudaMemPool_t* out) {
   constexpr int kMaxDevices = 64;
   static std::once_flag once[kMaxDevices];
   static cudaError_t status[kMaxDevices];
+  static cudaMemPool_t pools[kMaxDevices];
   if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
   std::call_once(once[dev], [dev] {
-    cudaMemPool_t pool;
-    cudaError_t r = cudaDeviceGetDefaultMemPool(&pool, dev);
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaError_t r = cudaMemPoolCreate(&pools[dev], &props);
     uint64_t keep = ~0ull;
-    if (r == cudaSuccess) r = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (r == cudaSuccess)
+      r = cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
     status[dev] = r;
   });
+  *out = pools[dev];
   return status[dev];
 }
+}  // namespace
+
+namespace mas {
+cudaError_t pool_alloc(void** ptr, size_t bytes, cudaStream_t stream) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (e == cudaSuccess) e = device_pool(dev, &pool);
+  if (e == cudaSuccess) e = cudaMallocFromPoolAsync(ptr, bytes, pool, stream);
+  return e;
+}
+}  // namespace mas
 
 struct mas_plan {
   int32_t B = 0, T = 0, S = 0;
@@ -417,6 +366,10 @@ struct mas_plan {
   int bnd_pitch = 0;
   bool internal = false;  // created by mas_align_host / _device, which order the frees
   int item_base = 0;      // added to item indices in messages (validate_item of one item)
+  // caller-held plans: per stream, an event recorded after the last enqueue
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> done;
+  bool captured = false;  // enqueued while a stream was capturing
+  bool nan_parallel = false;  // parallel engine, NaN sentinel (unchecked): score-table forward
 };
 
 extern "C" {
@@ -443,8 +396,14 @@ void mas_plan_destroy(mas_plan_t* p) {
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
   // A caller-held plan may still have kernels in flight on the caller's
-  // stream: finish them before the workspace goes back to the pool.
-  if (!p->internal) cudaDeviceSynchronize();
+  // streams: wait for the last enqueue on each before the workspace goes back
+  // to the pool (enqueues made under stream capture are only known to the
+  // graph, so then the whole device is synchronised).
+  if (!p->internal) {
+    if (p->captured) cudaDeviceSynchronize();
+    for (auto& se : p->done) cudaEventSynchronize(se.second);
+  }
+  for (auto& se : p->done) cudaEventDestroy(se.second);
   cudaStream_t st = cudaStreamPerThread;
   cudaFreeAsync(p->d_lengths, st);
   cudaFreeAsync(p->d_dirs, st);
@@ -508,6 +467,7 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
   p->T_pad = text_cap;
   p->mode = cfg.engine == MAS_ENGINE_REFERENCE ? 1 : 0;
   p->mnv = cfg.max_neg_val;
+  p->nan_parallel = p->mode == 0 && std::isnan(cfg.max_neg_val);
   p->lengths.resize(static_cast<size_t>(batch) * 2);
   int t_max = 0;
   for (int b = 0; b < batch; ++b) {
@@ -527,14 +487,14 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
       t_max = std::max<int>(t_max, static_cast<int>(t));
     }
   }
-  if (forward_variant() != 0 && mas::fwd4_configure() != cudaSuccess) {
+  if (mas::fwd4_configure() != cudaSuccess) {
     delete p;
     return set_error(err, MAS_E_CUDA, -1, -1, "forward kernel configuration failed");
   }
   if (!cached_geometry(batch, std::max(t_max, 1), speech_cap, &p->geo)) {
     delete p;
     return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
-                     "text length above 8192 rows is not supported by the device path");
+                     "no launch geometry fits this shape on the device");
   }
   const Geometry& g = p->geo;
   auto fail = [&](cudaError_t e, const char* what) {
@@ -542,23 +502,22 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
     return cuda_error(err, e, what);
   };
   cudaError_t e;
-  if ((e = !g.legacy ? mas::fwd4_configure() : mas::fwd_configure(g.W, g.N, g.K)) != cudaSuccess)
+  if ((e = mas::fwd4_configure()) != cudaSuccess)
     return fail(e, "fwd_configure");
   if ((e = mas::bt_configure(g.T_alloc, g.L)) != cudaSuccess) return fail(e, "bt_configure");
-  if ((e = pool_setup(p->device)) != cudaSuccess) return fail(e, "memory pool setup");
   // Workspace from the stream-ordered pool on this thread's default stream;
   // synchronised below, so it is valid on any stream afterwards.
   cudaStream_t st = cudaStreamPerThread;
   const size_t nB = static_cast<size_t>(batch);
-  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_lengths), nB * 2 * sizeof(uint32_t),
+  if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_lengths), nB * 2 * sizeof(uint32_t),
                            st)) != cudaSuccess)
-    return fail(e, "cudaMallocAsync(lengths)");
+    return fail(e, "mas::pool_alloc(lengths)");
   if ((e = cudaMemcpyAsync(p->d_lengths, p->lengths.data(), nB * 2 * sizeof(uint32_t),
                            cudaMemcpyHostToDevice, st)) != cudaSuccess)
     return fail(e, "cudaMemcpyAsync(lengths)");
-  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_dirs),
+  if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_dirs),
                            nB * g.M * g.T_alloc * sizeof(uint32_t), st)) != cudaSuccess)
-    return fail(e, "cudaMallocAsync(dirs)");
+    return fail(e, "mas::pool_alloc(dirs)");
   static const int bt_rows_cap = [] {
     const char* e = std::getenv("MAS_BT_ROWS");  // experiment override
     return e ? std::max(16, std::min(256, std::atoi(e))) & ~15 : 256;
@@ -566,20 +525,20 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
   p->bt_rows = std::min(bt_rows_cap, g.T_alloc);
   if (g.bands > 1) {
     p->bnd_pitch = (speech_cap + 31) & ~31;
-    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_bnd),
+    if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_bnd),
                              nB * (g.bands - 1) * p->bnd_pitch * sizeof(float), st)) !=
         cudaSuccess)
-      return fail(e, "cudaMallocAsync(boundary rows)");
-    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_sync),
+      return fail(e, "mas::pool_alloc(boundary rows)");
+    if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_sync),
                              nB * g.bands * sizeof(int), st)) != cudaSuccess)
-      return fail(e, "cudaMallocAsync(band progress)");
+      return fail(e, "mas::pool_alloc(band progress)");
   }
-  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_flags), nB * sizeof(int), st)) !=
+  if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_flags), nB * sizeof(int), st)) !=
       cudaSuccess)
-    return fail(e, "cudaMallocAsync(flags)");
-  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_locate), sizeof(unsigned long long),
+    return fail(e, "mas::pool_alloc(flags)");
+  if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_locate), sizeof(unsigned long long),
                            st)) != cudaSuccess)
-    return fail(e, "cudaMallocAsync(locate)");
+    return fail(e, "mas::pool_alloc(locate)");
   if (deferred) {
     if ((e = cudaEventCreateWithFlags(&p->ws_ready, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventRecord(p->ws_ready, st)) != cudaSuccess)
@@ -598,9 +557,7 @@ extern "C" {
 int mas_plan_launches(const mas_plan_t* p) { return p ? p->launches : 0; }
 
 void mas_plan_geometry(const mas_plan_t* p, int32_t geom[6]) {
-  geom[5] = !p->geo.legacy
-                ? mas::fwd4_max_active_clusters(p->geo.R, p->geo.W, p->geo.N, p->geo.K)
-                : mas::fwd_max_active_clusters(p->geo.W, p->geo.N, p->geo.K, 0);
+  geom[5] = mas::fwd4_max_active_clusters(p->geo.R, p->geo.W, p->geo.N, p->geo.K);
   geom[0] = 32 * p->geo.R;
   geom[1] = p->geo.W;
   geom[2] = p->geo.K;
@@ -623,29 +580,56 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
   const Geometry& g = p->geo;
   if (p->ws_ready) MAS_CUDA(cudaStreamWaitEvent(stream, p->ws_ready, 0), "workspace wait");
   int nfwd = 0, nbt = 0;
-  if (parts & MAS_PART_FORWARD) {
-    CUtensorMap tm0, tm1;
-    const bool r4 = !g.legacy;
+  if ((parts & MAS_PART_FORWARD) && p->nan_parallel) {
+    // parallel::detail::align_unchecked with a NaN sentinel: std::max's rule
+    // ((a < b) ? b : a, a NaN first operand wins) shapes the score table,
+    // which K1's FMNMX does not follow.  The table is computed with that rule
+    // (forward_scores_kernel, bit-exact with forward_parallel) in a scratch
+    // copy and its decisions are packed into the plan's direction words, so
+    // K2 runs unchanged.  Unchecked (test-only) sentinels only.
+    const size_t item_floats = static_cast<size_t>(p->T_pad) * p->pitch;
+    float* scratch = nullptr;
+    MAS_CUDA(mas::pool_alloc(reinterpret_cast<void**>(&scratch), nb * item_floats * 4, stream),
+             "pool_alloc(nan scratch)");
+    const float* src = d_values + b0 * item_floats;
+    cudaError_t e = cudaMemcpyAsync(scratch, src, nb * item_floats * 4, cudaMemcpyDeviceToDevice, stream);
+    mas_error_t sub;
+    int rc = MAS_OK;
+    if (e == cudaSuccess)
+      rc = mas::forward_scores_host_lengths(scratch, p->pitch, nb, p->T_pad, p->S,
+                                            p->lengths.data() + 2 * static_cast<size_t>(b0), p->mnv,
+                                            stream, &sub);
+    if (e == cudaSuccess && rc == MAS_OK)
+      e = mas::launch_scores_to_dirs(scratch, p->pitch, p->T_pad, p->S, p->d_lengths + 2 * b0, g.M,
+                                     g.T_alloc, nb, p->d_dirs + static_cast<size_t>(b0) * g.M * g.T_alloc,
+                                     stream);
+    if (e == cudaSuccess && rc == MAS_OK)
+      e = mas::launch_flag_nonfinite(src, p->pitch, p->T_pad, p->S, p->d_lengths + 2 * b0, nb,
+                                     p->d_flags + b0, stream);
+    if (e == cudaSuccess && rc == MAS_OK && d_out)
+      e = cudaMemsetAsync(d_out + b0 * static_cast<size_t>(p->T) * p->S, 0,
+                          nb * static_cast<size_t>(p->T) * p->S, stream);
+    cudaFreeAsync(scratch, stream);
+    if (rc != MAS_OK) return set_error(err, rc, -1, -1, sub.message);
+    MAS_CUDA(e, "NaN-sentinel forward");
+    nfwd = 4;
+  } else if (parts & MAS_PART_FORWARD) {
+    CUtensorMap tm0;
     // Tensor maps depend only on the buffers and the plan's layout: encoded
     // once per input pointer and reused by later enqueues (host cost).
-    const bool reuse_in = r4 && p->tm_in_ptr == d_values && p->tm_in_pitch == p->pitch &&
+    const bool reuse_in = p->tm_in_ptr == d_values && p->tm_in_pitch == p->pitch &&
                           p->tm_in_tpad == p->T_pad;
     if (reuse_in) {
       tm0 = p->tm_in;
-    } else if (r4 ? !encode_map4(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S,
-                                 g.R, &tm0)
-                  : !encode_maps(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S,
-                                 &tm0, &tm1)) {
+    } else if (!encode_map4(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, g.R,
+                            &tm0)) {
       return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled failed");
-    } else if (r4) {
+    } else {
       p->tm_in = tm0;
       p->tm_in_ptr = d_values;
       p->tm_in_pitch = p->pitch;
       p->tm_in_tpad = p->T_pad;
     }
-    if (!r4)  // mas_fwd4 zeroes each item's flag itself
-      MAS_CUDA(cudaMemsetAsync(p->d_flags + b0, 0, sizeof(int) * nb, stream),
-               "cudaMemsetAsync(flags)");
     mas::FwdArgs fa;
     fa.b0 = b0;
     fa.lengths = p->d_lengths;
@@ -672,18 +656,20 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
       const char* e = std::getenv("MAS_FUSED_ZERO");
       return e ? std::atoi(e) : -1;
     }();
-    static const int sms = [] {
-      int dev = 0, n = 148;
-      if (cudaGetDevice(&dev) == cudaSuccess)
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-      return n;
-    }();
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
     const double warps = static_cast<double>(nb) * g.bands * g.K * g.W;
     const double chain_s = p->S * 50.0 / 1.9e9 * std::max(1.0, warps / (4.0 * sms));
     const double stream_s = static_cast<double>(nb) * p->T * p->S * 4.125 / 5.9e12;
     const bool chain_bound = stream_s <= 1.1 * chain_s;
+    // The zero boxes are 32R rows tall on a flat [B*T] row map: with
+    // T % 32R != 0 an item's last box spills into the next item's first rows,
+    // harmless only when this launch owns the next item too (the whole batch;
+    // TMA clips past the end).  Chunked host calls run other chunks
+    // concurrently, so they fuse only row-aligned items.
+    const bool rows_own = (p->T % (32 * g.R)) == 0 || (b0 == 0 && nb == p->B);
     const bool fused_zero = d_out && (fuse_env >= 0 ? fuse_env == 1 : chain_bound) &&
-                            p->all_full && (p->S % 16) == 0 &&
+                            p->all_full && rows_own && (p->S % 16) == 0 &&
                             (reinterpret_cast<uintptr_t>(d_out) & 15u) == 0;
     const size_t item_bytes = static_cast<size_t>(p->T) * p->S;
     if (d_out && !fused_zero) {
@@ -692,14 +678,12 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     }
     CUtensorMap tm_out;
     std::memset(&tm_out, 0, sizeof(tm_out));
-    if (fused_zero && r4 && p->tm_out_ptr == d_out) {
+    if (fused_zero && p->tm_out_ptr == d_out) {
       tm_out = p->tm_out;
-    } else if (fused_zero && !(r4 ? encode_out_map4(d_out, static_cast<int64_t>(p->B) * p->T, p->S, g.R,
-                                             &tm_out)
-                           : encode_out_map(d_out, static_cast<int64_t>(p->B) * p->T, p->S,
-                                            &tm_out)))
+    } else if (fused_zero &&
+               !encode_out_map4(d_out, static_cast<int64_t>(p->B) * p->T, p->S, g.R, &tm_out)) {
       return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled(out) failed");
-    else if (fused_zero && r4 && p->tm_out_ptr != d_out) {
+    } else if (fused_zero) {
       p->tm_out = tm_out;
       p->tm_out_ptr = d_out;
     }
@@ -721,22 +705,16 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     fa.bnd_pitch = p->bnd_pitch;
     fa.ticket = p->d_sync ? p->d_sync + b0 : nullptr;
     fa.progress = p->d_sync ? p->d_sync + p->B : nullptr;
-    if (r4) {
-      // All bands of all items in one launch (clusters ordered by ticket).
-      if (g.bands > 1) {
-        MAS_CUDA(cudaMemsetAsync(fa.ticket, 0, sizeof(int), stream), "cudaMemsetAsync(ticket)");
-        MAS_CUDA(cudaMemsetAsync(fa.progress + static_cast<size_t>(b0) * (g.bands - 1), 0,
-                                 sizeof(int) * nb * (g.bands - 1), stream),
-                 "cudaMemsetAsync(progress)");
-      }
-      MAS_CUDA(mas::launch_fwd4(g.R, p->mode, tm0, tm_out, fa, nb * g.bands, stream),
-               "launch mas_fwd4");
-      nfwd = 1;
-    } else
-    {
-      MAS_CUDA(mas::launch_fwd(p->mode, tm0, tm1, tm_out, fa, nb, stream), "launch mas_fwd");
-      nfwd = 1;
+    // All bands of all items in one launch (clusters ordered by ticket).
+    if (g.bands > 1) {
+      MAS_CUDA(cudaMemsetAsync(fa.ticket, 0, sizeof(int), stream), "cudaMemsetAsync(ticket)");
+      MAS_CUDA(cudaMemsetAsync(fa.progress + static_cast<size_t>(b0) * (g.bands - 1), 0,
+                               sizeof(int) * nb * (g.bands - 1), stream),
+               "cudaMemsetAsync(progress)");
     }
+    MAS_CUDA(mas::launch_fwd4(g.R, p->mode, tm0, tm_out, fa, nb * g.bands, stream),
+             "launch mas_fwd4");
+    nfwd = 1;
   }
   if ((parts & MAS_PART_BACKTRACK) && (d_out || d_paths || d_dur)) {
     mas::BtArgs ba;
@@ -776,8 +754,25 @@ int mas_plan_enqueue_ex(mas_plan_t* p, uint32_t parts, const float* d_values, ui
                         int32_t* d_paths, int32_t* d_durations, void* stream_v,
                         mas_error_t* err) {
   clear_error(err);
-  return enqueue_items(p, parts, 0, p->B, d_values, d_out, d_paths, d_durations,
-                       static_cast<cudaStream_t>(stream_v), err);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  const int rc = enqueue_items(p, parts, 0, p->B, d_values, d_out, d_paths, d_durations, stream, err);
+  if (rc != MAS_OK || p->internal) return rc;
+  // remember the enqueue so mas_plan_destroy can wait for it
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  MAS_CUDA(cudaStreamIsCapturing(stream, &cap), "cudaStreamIsCapturing");
+  if (cap != cudaStreamCaptureStatusNone) {
+    p->captured = true;
+    return MAS_OK;
+  }
+  cudaEvent_t ev = nullptr;
+  for (auto& se : p->done)
+    if (se.first == stream) ev = se.second;
+  if (!ev) {
+    MAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+    p->done.emplace_back(stream, ev);
+  }
+  MAS_CUDA(cudaEventRecord(ev, stream), "cudaEventRecord");
+  return MAS_OK;
 }
 
 int mas_plan_finish(mas_plan_t* p, const float* d_values, void* stream_v, mas_error_t* err) {
@@ -790,7 +785,11 @@ int mas_plan_finish(mas_plan_t* p, const float* d_values, void* stream_v, mas_er
                            stream),
            "cudaMemcpyAsync(flags)");
   MAS_CUDA(cudaStreamSynchronize(stream), "flags readback");
-  const int limit = p->first_host_error.item >= 0 ? p->first_host_error.item : p->B;
+  // first_host_error.item carries item_base (message numbering); flags are
+  // indexed from 0 within this plan.
+  const int limit = p->first_host_error.item >= 0
+                        ? std::max(0, std::min(p->B, p->first_host_error.item - p->item_base))
+                        : p->B;
   for (int b = 0; b < limit; ++b) {
     if (!flags[b]) continue;
     // Conservative device flag: confirm and locate exactly (row-major first).
@@ -811,8 +810,10 @@ int mas_plan_finish(mas_plan_t* p, const float* d_values, void* stream_v, mas_er
       const int64_t i = static_cast<int64_t>(hit / s), j = static_cast<int64_t>(hit % s);
       set_error(err, MAS_E_VALIDATION, MAS_ERRC_NON_FINITE, b + p->item_base,
                 nonfinite_message(b + p->item_base, i, j));
-      err->i = i;
-      err->j = j;
+      if (err) {
+        err->i = i;
+        err->j = j;
+      }
       return MAS_E_VALIDATION;
     }
   }
@@ -846,11 +847,11 @@ int mas_align_device_ex(const float* d_values, int64_t row_pitch, int32_t batch,
     // Re-pitch into an aligned [B][T_pad][pitch'] copy the TMA path accepts.
     const int T_pad = (text_cap + 3) & ~3;
     const int64_t pitch2 = (static_cast<int64_t>(speech_cap) + 3) & ~int64_t(3);
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+    cudaError_t e = mas::pool_alloc(reinterpret_cast<void**>(&scratch),
                                     static_cast<size_t>(batch) * T_pad * pitch2 * 4, stream);
     if (e != cudaSuccess) {
       mas_plan_destroy(plan);
-      return cuda_error(err, e, "cudaMallocAsync(repitch)");
+      return cuda_error(err, e, "mas::pool_alloc(repitch)");
     }
     for (int b = 0; b < batch && e == cudaSuccess; ++b) {
       e = cudaMemcpy2DAsync(scratch + static_cast<size_t>(b) * T_pad * pitch2, pitch2 * 4,
@@ -976,26 +977,40 @@ class CopyPool {
   pid_t owner_;
 };
 
-// Pinned buffers kept for reuse across calls (pinning costs milliseconds).
+// Pinned buffers kept for reuse across calls (pinning costs milliseconds),
+// bounded: at most kKeepBytes stay page-locked while idle; beyond that idle
+// buffers are released (largest first) before new ones are pinned, and
+// returned buffers are released instead of kept.
 class PinnedPool {
  public:
+  static constexpr size_t kKeepBytes = size_t(2) << 30;
   static PinnedPool& get() {
     static PinnedPool pool;
     return pool;
   }
   void* take(size_t bytes) {
     std::lock_guard<std::mutex> lk(mu_);
+    size_t best = free_.size();
     for (size_t i = 0; i < free_.size(); ++i)
-      if (free_[i].second >= bytes) {
-        void* p = free_[i].first;
-        free_.erase(free_.begin() + static_cast<long>(i));
-        return p;
-      }
+      if (free_[i].second >= bytes && (best == free_.size() || free_[i].second < free_[best].second))
+        best = i;
+    if (best < free_.size()) {
+      void* p = free_[best].first;
+      free_.erase(free_.begin() + static_cast<long>(best));
+      return p;
+    }
+    while (!free_.empty() && pinned_ + bytes > kKeepBytes) {
+      auto largest = std::max_element(free_.begin(), free_.end(),
+                                      [](const auto& a, const auto& b) { return a.second < b.second; });
+      release(*largest);
+      free_.erase(largest);
+    }
     void* p = nullptr;
     if (cudaMallocHost(&p, bytes) != cudaSuccess) {
       cudaGetLastError();
       return nullptr;
     }
+    pinned_ += bytes;
     sizes_.push_back({p, bytes});
     return p;
   }
@@ -1003,12 +1018,29 @@ class PinnedPool {
     if (!p) return;
     std::lock_guard<std::mutex> lk(mu_);
     for (const auto& e : sizes_)
-      if (e.first == p) free_.push_back(e);
+      if (e.first == p) {
+        if (pinned_ > kKeepBytes)
+          release(e);
+        else
+          free_.push_back(e);
+        return;
+      }
   }
 
  private:
+  // caller holds mu_
+  void release(std::pair<void*, size_t> e) {
+    cudaFreeHost(e.first);
+    pinned_ -= e.second;
+    for (size_t i = 0; i < sizes_.size(); ++i)
+      if (sizes_[i].first == e.first) {
+        sizes_.erase(sizes_.begin() + static_cast<long>(i));
+        break;
+      }
+  }
   std::mutex mu_;
   std::vector<std::pair<void*, size_t>> free_, sizes_;
+  size_t pinned_ = 0;
 };
 
 // Two non-blocking streams and a join event per (host thread, device),
@@ -1107,14 +1139,14 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
     st[1] = hs->st[1];
   }
   if (e == cudaSuccess)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&d_q), batch * q_item * sizeof(float), st[0]);
+    e = mas::pool_alloc(reinterpret_cast<void**>(&d_q), batch * q_item * sizeof(float), st[0]);
   if (e == cudaSuccess && out)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&d_out), batch * o_item, st[0]);
+    e = mas::pool_alloc(reinterpret_cast<void**>(&d_out), batch * o_item, st[0]);
   if (e == cudaSuccess && paths)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&d_paths),
+    e = mas::pool_alloc(reinterpret_cast<void**>(&d_paths),
                         static_cast<size_t>(batch) * speech_cap * sizeof(int32_t), st[0]);
   if (e == cudaSuccess && durations)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&d_dur),
+    e = mas::pool_alloc(reinterpret_cast<void**>(&d_dur),
                         static_cast<size_t>(batch) * text_cap * sizeof(int32_t), st[0]);
   cudaEvent_t ready = hs ? hs->ready : nullptr;
   if (e == cudaSuccess) e = cudaEventRecord(ready, st[0]);

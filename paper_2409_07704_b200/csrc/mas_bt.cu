@@ -425,44 +425,6 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
   if (dur) finish_durations();
 }
 
-// Reference-order serial walk, one thread per item -- kept as a
-// cross-check (MAS_BT_SERIAL=1) for the windowed walker.
-__global__ void bt_serial_kernel(const BtArgs a) {
-  const int bi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (bi >= a.B) return;
-  const int b = a.b0 + bi;
-  const int t = static_cast<int>(a.lengths[2 * b]);
-  const int s = static_cast<int>(a.lengths[2 * b + 1]);
-  int32_t* dur = a.dur ? a.dur + static_cast<size_t>(b) * a.T_cap : nullptr;
-  if (dur)
-    for (int i = 0; i < a.T_cap; ++i) dur[i] = 0;
-  if (t <= 0 || s <= 0) return;
-  const uint32_t* src = a.dirs + static_cast<size_t>(b) * a.M * a.T_alloc;
-  uint8_t* out = a.out ? a.out + static_cast<size_t>(b) * a.T_cap * a.S_cap : nullptr;
-  int32_t* prow = a.path ? a.path + static_cast<size_t>(b) * a.S_cap : nullptr;
-  int cur = t - 1;
-  if (out) out[static_cast<size_t>(cur) * a.S_cap + s - 1] = 1;
-  if (prow) prow[s - 1] = cur;
-  if (dur) ++dur[cur];
-  for (int j = s - 2; j >= 0; --j) {
-    if (cur > 0) {
-      const int p = j + 1;
-      const uint32_t w = src[static_cast<size_t>(p >> 5) * a.T_alloc + cur];
-      if ((w >> (31 - (p & 31))) & 1u) --cur;
-    }
-    if (out) out[static_cast<size_t>(cur) * a.S_cap + j] = 1;
-    if (prow) prow[j] = cur;
-    if (dur) ++dur[cur];
-  }
-}
-
-__global__ void fill_paths_kernel(int32_t* paths, size_t n) {
-  if (!paths) return;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x)
-    paths[i] = -1;
-}
-
 // Exact NonFinite locator (error path only): lowest row-major (i, j) in the
 // valid region of item b (types.cpp:107-115), as i * s + j via atomicMin.
 __global__ void locate_nonfinite_kernel(const float* q, int64_t row_pitch, int T_pad, int b, int t,
@@ -512,18 +474,6 @@ int grid_for(size_t n, int threads) {
 }  // namespace
 
 cudaError_t launch_backtrack(const BtArgs& a, cudaStream_t stream, int* launches) {
-  static const bool serial = [] {
-    const char* e = std::getenv("MAS_BT_SERIAL");
-    return e && e[0] == '1';
-  }();
-  if (serial) {
-    fill_paths_kernel<<<grid_for(static_cast<size_t>(a.B) * a.S_cap, 256), 256, 0, stream>>>(
-        a.path ? a.path + static_cast<size_t>(a.b0) * a.S_cap : nullptr,
-        static_cast<size_t>(a.B) * a.S_cap);
-    bt_serial_kernel<<<(a.B + 63) / 64, 64, 0, stream>>>(a);
-    if (launches) *launches = 2;
-    return cudaGetLastError();
-  }
   // Programmatic dependent launch: the walkers' prologue overlaps the tail
   // of the forward kernel; griddepcontrol.wait orders every data access.
   cudaLaunchConfig_t cfg = {};

@@ -739,7 +739,7 @@ const void* fwd4_fn() {
   return reinterpret_cast<const void*>(&mas_fwd4_kernel<R, MODE>);
 }
 const void* fwd4_fn(int R, int mode) {
-  if (R == 2) return mode == 0 ? fwd4_fn<2, 0>() : fwd4_fn<2, 1>();
+  (void)R;  // four rows per lane
   return mode == 0 ? fwd4_fn<4, 0>() : fwd4_fn<4, 1>();
 }
 }  // namespace
@@ -755,8 +755,8 @@ cudaError_t fwd4_configure() {
   std::call_once(once[dev], [dev] {
     int smem_max = 0;
     cudaError_t r = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    for (int v = 0; v < 4 && r == cudaSuccess; ++v) {
-      const void* fn = fwd4_fn(v < 2 ? 4 : 2, v & 1);
+    for (int v = 0; v < 2 && r == cudaSuccess; ++v) {
+      const void* fn = fwd4_fn(4, v);
       r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
       if (r == cudaSuccess)
         r = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -800,9 +800,7 @@ cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorM
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (R == 2)
-    return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<2, 0>, tmq, tm_out, a)
-                     : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<2, 1>, tmq, tm_out, a);
+  if (R != 4) return cudaErrorInvalidValue;
   return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0>, tmq, tm_out, a)
                    : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 1>, tmq, tm_out, a);
 }

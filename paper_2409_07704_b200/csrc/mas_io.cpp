@@ -163,14 +163,20 @@ int mas_io_read_header(const char* path, uint64_t byte_budget, int32_t* dtype, i
   return MAS_OK;
 }
 
-int mas_io_read(const char* path, uint64_t byte_budget, void* values, uint32_t* lengths,
-                mas_error_t* err) {
+int mas_io_read(const char* path, uint64_t byte_budget, int32_t dtype, const int64_t dims[3],
+                void* values, uint32_t* lengths, mas_error_t* err) {
   clear(err);
   File f;
   Header h;
   int rc = open_and_check(path, byte_budget, &f, &h, err);
   if (rc) return rc;
   const std::string p = path;
+  // The caller sized `values` / `lengths` from an earlier header read; the
+  // file must still describe exactly that tensor.
+  if (!dims || h.dtype != dtype || static_cast<int64_t>(h.dims[0]) != dims[0] ||
+      static_cast<int64_t>(h.dims[1]) != dims[1] || static_cast<int64_t>(h.dims[2]) != dims[2])
+    return io_error(err, MAS_ERRC_IO_FAILURE,
+                    "tensor header differs from the expected dtype and dimensions: " + p);
   const size_t bytes = h.count * (h.dtype == 0 ? 4 : 1);
   rc = read_exact(f.get(), values, bytes, p, "payload", err);
   if (rc) return rc;

@@ -6,26 +6,24 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "monoalign_b200.h"
+
 namespace mas {
 
-// Forward kernel geometry: every lane owns kRowsPerLane consecutive text
-// rows, every warp 32 * kRowsPerLane rows, and stages hold kStageCols speech
-// columns.
-constexpr int kRowsPerLane = 2;
-constexpr int kRowsPerWarp = 32 * kRowsPerLane;  // 64
-constexpr int kStageCols = 64;                              // columns per iteration / TMA stage
-constexpr int kStageBytes = kRowsPerWarp * kStageCols * 4;  // 16 KiB
-constexpr int kQuadCols = 16;  // columns per boundary-row FIFO hand-off
 #ifndef MAS_FIFO_SLOTS
 #define MAS_FIFO_SLOTS 32
 #endif
-constexpr int kFifoSlots = MAS_FIFO_SLOTS;  // boundary-row FIFO depth, in 16-column quads
+constexpr int kFifoSlots = MAS_FIFO_SLOTS;  // boundary-row FIFO depth, in quads
 constexpr int kMaxWarpsPerCta = 8;
 #ifndef MAS_ZCOLS
 #define MAS_ZCOLS 128
 #endif
 constexpr int kZeroCols = MAS_ZCOLS;  // mas_fwd4: columns per fused zero-fill TMA store
 constexpr int kMaxClusterCtas = 16;
+
+// Stream-ordered device allocation from the library's own pool on the
+// current device (mas_abi.cu); free with cudaFreeAsync.
+cudaError_t pool_alloc(void** ptr, size_t bytes, cudaStream_t stream);
 
 struct FwdArgs {
   int b0;                   // first item of this launch (items b0 .. b0 + grid/K - 1)
@@ -70,21 +68,29 @@ struct BtArgs {
   int R;                    // rows per backtrack window (<= 256, <= T_alloc)
 };
 
-size_t fwd_smem_bytes(int W, int N);
-cudaError_t launch_fwd(int mode, const CUtensorMap& tm0, const CUtensorMap& tm1,
-                       const CUtensorMap& tm_out, const FwdArgs& a, int B, cudaStream_t stream);
 cudaError_t launch_backtrack(const BtArgs& a, cudaStream_t stream, int* launches);
 cudaError_t launch_locate_nonfinite(const float* q, int64_t row_pitch, int T_pad, int b, int t,
                                     int s, unsigned long long* d_result, cudaStream_t stream);
 cudaError_t launch_generate(uint64_t s0, int64_t first_elem, int B, int T, int S, int64_t pitch,
                             float* out, cudaStream_t stream);
-cudaError_t fwd_configure(int W, int N, int K);
 // mas_fwd4.cu: R (4 or 2) rows per lane, 32 R rows per warp, 32-column stages.
+// mas_scores.cu: score tables (std::max arithmetic, bit-exact with the
+// reference's forward_parallel) and their direction words in the backtrack
+// kernel's [B][M][T_alloc] layout; used for NaN sentinels (mas_abi.cu).
+cudaError_t launch_scores_to_dirs(const float* q, int64_t pitch, int rows_per_item, int S_cap,
+                                  const uint32_t* d_lengths, int M, int T_alloc, int B,
+                                  uint32_t* dirs, cudaStream_t stream);
+cudaError_t launch_flag_nonfinite(const float* q, int64_t pitch, int rows_per_item, int S_cap,
+                                  const uint32_t* d_lengths, int B, int* flags,
+                                  cudaStream_t stream);
+// mas_forward_scores over items `rows_per_item` rows apart, host lengths.
+int forward_scores_host_lengths(float* d_values, int64_t row_pitch, int32_t batch,
+                                int32_t rows_per_item, int32_t speech_cap, const uint32_t* lengths,
+                                float max_neg_val, cudaStream_t stream, mas_error_t* err);
 size_t fwd4_smem_bytes(int R, int W, int N);
 cudaError_t fwd4_configure();
 int fwd4_max_active_clusters(int R, int W, int N, int K);
 cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorMap& tm_out,
                         const FwdArgs& a, int B, cudaStream_t stream);
-int fwd_max_active_clusters(int W, int N, int K, int mode);
 
 }  // namespace mas

@@ -371,6 +371,24 @@ __global__ void relax_column_kernel(const float* __restrict__ prev, float* __res
     cur[i] += ref_max(i == 0 ? sentinel : prev[i - 1], prev[i]);
 }
 
+// NonFinite flags of a batch (types.cpp:107-115 scan, flag only; the exact
+// location comes from the locator on the error path).
+__global__ void flag_nonfinite_kernel(const float* __restrict__ q, int64_t pitch, int rows_per_item,
+                                      int S_cap, const uint32_t* __restrict__ lengths, int B,
+                                      int* __restrict__ flags) {
+  const int64_t per_item = static_cast<int64_t>(rows_per_item) * S_cap;
+  const int64_t total = per_item * B;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int b = static_cast<int>(k / per_item);
+    const int64_t r = k - b * per_item;
+    const int i = static_cast<int>(r / S_cap), j = static_cast<int>(r % S_cap);
+    if (i < static_cast<int>(lengths[2 * b]) && j < static_cast<int>(lengths[2 * b + 1]) &&
+        !isfinite(q[(static_cast<int64_t>(b) * rows_per_item + i) * pitch + j]))
+      flags[b] = 1;
+  }
+}
+
 int forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_t text_cap,
                    int32_t speech_cap, const uint32_t* lengths, int mode, float max_neg_val,
                    void* stream_v, mas_error_t* err) {
@@ -395,7 +413,7 @@ int forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_t te
   const size_t len_bytes = lengths ? static_cast<size_t>(batch) * 2 * sizeof(uint32_t) : 0;
   const size_t sync_bytes = (1 + static_cast<size_t>(nprogress)) * sizeof(int);
   char* ws = nullptr;
-  e = cudaMallocAsync(reinterpret_cast<void**>(&ws), len_bytes + sync_bytes, stream);
+  e = mas::pool_alloc(reinterpret_cast<void**>(&ws), len_bytes + sync_bytes, stream);
   uint32_t* d_len = lengths ? reinterpret_cast<uint32_t*>(ws) : nullptr;
   int* sync = reinterpret_cast<int*>(ws + len_bytes);
   if (e == cudaSuccess && lengths)
@@ -430,6 +448,39 @@ int forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_t te
 }
 
 }  // namespace
+
+namespace mas {
+
+cudaError_t launch_scores_to_dirs(const float* q, int64_t pitch, int rows_per_item, int S_cap,
+                                  const uint32_t* d_lengths, int M, int T_alloc, int B,
+                                  uint32_t* dirs, cudaStream_t stream) {
+  const int64_t warps = static_cast<int64_t>(B) * M * T_alloc;
+  const int64_t blocks = std::min<int64_t>((warps + 7) / 8, static_cast<int64_t>(sm_count()) * 16);
+  scores_to_dirs_kernel<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0, stream>>>(
+      q, pitch, rows_per_item, S_cap, d_lengths, M, T_alloc, B, dirs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flag_nonfinite(const float* q, int64_t pitch, int rows_per_item, int S_cap,
+                                  const uint32_t* d_lengths, int B, int* flags,
+                                  cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * B, stream);
+  if (e != cudaSuccess) return e;
+  const int64_t total = static_cast<int64_t>(B) * rows_per_item * S_cap;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, static_cast<int64_t>(sm_count()) * 16);
+  flag_nonfinite_kernel<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0, stream>>>(
+      q, pitch, rows_per_item, S_cap, d_lengths, B, flags);
+  return cudaGetLastError();
+}
+
+int forward_scores_host_lengths(float* d_values, int64_t row_pitch, int32_t batch,
+                                int32_t rows_per_item, int32_t speech_cap, const uint32_t* lengths,
+                                float max_neg_val, cudaStream_t stream, mas_error_t* err) {
+  return forward_scores(d_values, row_pitch, batch, rows_per_item, speech_cap, lengths, 0,
+                        max_neg_val, stream, err);
+}
+
+}  // namespace mas
 
 extern "C" {
 
@@ -475,18 +526,14 @@ int mas_backtrack_scores(const float* d_scores, int64_t row_pitch, int32_t batch
     lengths = full.data();
   }
   char* ws = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), dir_bytes + len_bytes, stream);
+  cudaError_t e = mas::pool_alloc(reinterpret_cast<void**>(&ws), dir_bytes + len_bytes, stream);
   uint32_t* d_dirs = reinterpret_cast<uint32_t*>(ws);
   uint32_t* d_len = reinterpret_cast<uint32_t*>(ws + dir_bytes);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(d_len, lengths, len_bytes, cudaMemcpyHostToDevice, stream);
-  if (e == cudaSuccess) {
-    const int64_t warps = static_cast<int64_t>(batch) * M * T_alloc;
-    const int64_t blocks = std::min<int64_t>((warps + 7) / 8, static_cast<int64_t>(sm_count()) * 16);
-    scores_to_dirs_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
-        d_scores, row_pitch, text_cap, speech_cap, d_len, M, T_alloc, batch, d_dirs);
-    e = cudaGetLastError();
-  }
+  if (e == cudaSuccess)
+    e = mas::launch_scores_to_dirs(d_scores, row_pitch, text_cap, speech_cap, d_len, M, T_alloc,
+                                   batch, d_dirs, stream);
   if (e == cudaSuccess) {
     mas::BtArgs ba = {};
     ba.b0 = 0;

@@ -17,6 +17,7 @@
 
 #include <cuda_runtime.h>
 #include "../../include/monoalign_b200.h"
+#include "mas_kernels.h"
 
 namespace monoalign {
 
@@ -83,7 +84,7 @@ AlignmentMatrix run(const LikelihoodBatch& batch, const MasConfig& cfg, bool unc
 class DeviceScratch {
  public:
   explicit DeviceScratch(std::size_t bytes) : stream_(cudaStreamPerThread) {
-    if (bytes) check(cudaMallocAsync(&p_, bytes, stream_));
+    if (bytes) check(mas::pool_alloc(&p_, bytes, stream_));
   }
   ~DeviceScratch() {
     if (p_) cudaFreeAsync(p_, stream_);
@@ -372,7 +373,7 @@ LikelihoodBatch generate_random_batch(int b, int t, int s, std::uint64_t seed) {
   const size_t bytes = batch.values.size() * sizeof(float);
   float* d = nullptr;
   cudaStream_t st = cudaStreamPerThread;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), bytes, st);
+  cudaError_t e = mas::pool_alloc(reinterpret_cast<void**>(&d), bytes, st);
   if (e == cudaSuccess &&
       mas_generate_device(seed, b, t, s, 0, s, d, st) != MAS_OK)
     e = cudaErrorLaunchFailure;
@@ -435,13 +436,13 @@ Tensor read_tensor(const std::filesystem::path& path, std::size_t byte_budget) {
   };
   if (dtype == 0) {
     LikelihoodBatch batch(b, t, s);
-    rc = mas_io_read(p.c_str(), byte_budget, batch.values.data(), lens.data(), &err);
+    rc = mas_io_read(p.c_str(), byte_budget, dtype, dims, batch.values.data(), lens.data(), &err);
     if (rc != MAS_OK) throw_for(rc, err);
     unflat(batch.lengths);
     return batch;
   }
   AlignmentMatrix m(b, t, s);
-  rc = mas_io_read(p.c_str(), byte_budget, m.values.data(), lens.data(), &err);
+  rc = mas_io_read(p.c_str(), byte_budget, dtype, dims, m.values.data(), lens.data(), &err);
   if (rc != MAS_OK) throw_for(rc, err);
   unflat(m.lengths);
   return m;

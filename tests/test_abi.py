@@ -69,7 +69,7 @@ def test_config_default_and_names(mas):
     assert cfg.engine == mas._lib.MAS_ENGINE_PARALLEL
     assert cfg.max_neg_val == np.float32(-1e32)
     assert cfg.threads == 0 and cfg.flags == 0
-    assert lib.mas_abi_version() == 2
+    assert lib.mas_abi_version() == 3
     for code, name in enumerate(mas._lib.ERRC_NAMES):
         assert lib.mas_errc_name(code).decode() == name
     assert lib.mas_errc_name(99).decode() == "Unknown"

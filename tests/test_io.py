@@ -39,7 +39,8 @@ def _read_c(mas, path, budget=1 << 30):
     lens = np.empty(1 << 12, np.uint32)
     return _errc(mas, lambda err: lib.mas_io_read_header(
         os.fsencode(path), budget, ctypes.byref(dtype), ctypes.byref(dims), ctypes.byref(has),
-        ctypes.byref(err)) or lib.mas_io_read(os.fsencode(path), budget, vals.ctypes.data,
+        ctypes.byref(err)) or lib.mas_io_read(os.fsencode(path), budget, dtype.value,
+                                              ctypes.byref(dims), vals.ctypes.data,
                                               lens.ctypes.data, ctypes.byref(err)))
 
 
@@ -193,3 +194,33 @@ def test_python_surface_checks(mas, tmp_path):
         mas.write_tensor(p, np.zeros((1, 2, 2), np.float32), lengths=[[3, 2]])
     with pytest.raises(ValueError):
         mas.write_tensor(p, np.zeros((0, 2, 2), np.float32))
+
+
+def test_read_rejects_a_file_replaced_after_the_header(mas, tmp_path):
+    """mas_io_read checks the header against the dims the buffers were sized
+    for (a file swapped between the two reads must not overflow them)."""
+    import ctypes
+
+    from paper_2409_07704_b200 import _lib
+
+    lib = mas._lib.load()
+    p = tmp_path / "swap.bin"
+    mas.write_tensor(str(p), np.zeros((1, 2, 3), np.float32))
+    dtype = ctypes.c_int32()
+    dims = (ctypes.c_int64 * 3)()
+    has = ctypes.c_int32()
+    err = _lib.MasError()
+    assert lib.mas_io_read_header(os.fsencode(str(p)), 1 << 30, ctypes.byref(dtype),
+                                  ctypes.byref(dims), ctypes.byref(has), ctypes.byref(err)) == 0
+    vals = np.full(6, 7.0, np.float32)
+    lens = np.zeros((1, 2), np.uint32)
+    mas.write_tensor(str(p), np.zeros((4, 8, 9), np.float32))  # bigger file, same path
+    rc = lib.mas_io_read(os.fsencode(str(p)), 1 << 30, dtype.value, ctypes.byref(dims),
+                         vals.ctypes.data, lens.ctypes.data, ctypes.byref(err))
+    assert rc == _lib.MAS_E_IO and err.errc == 12  # IoFailure
+    assert b"differs from the expected" in err.message
+    assert (vals == 7.0).all()
+    mas.write_tensor(str(p), np.zeros((1, 2, 3), np.uint8))  # same dims, other dtype
+    rc = lib.mas_io_read(os.fsencode(str(p)), 1 << 30, dtype.value, ctypes.byref(dims),
+                         vals.ctypes.data, lens.ctypes.data, ctypes.byref(err))
+    assert rc == _lib.MAS_E_IO
