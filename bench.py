@@ -2,6 +2,7 @@
 (B*T*S / time) and ms/batch at B32 T1024 S8192 vs the CPU reference).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3|c5]
 
 One step = the whole maximum-path call on one batch of config 3
 (B=32 items per GPU, T=1024, S=8192, fp32 log-likelihoods from the
@@ -14,7 +15,11 @@ GPU) are larger than L2 (126 MB), so no flush is needed between steps.
 Under torchrun each rank aligns its own 32-item shard (items [32r, 32r+32)
 of generate_random_batch(32 N, ...)): weak scaling, no collective on the data
 path; NCCL is used only for the start/stop barrier and the max-over-ranks
-timing.
+timing.  `--config c5` is BASELINE's batch-sharded sweep instead: the fixed
+batch generate_random_batch(256, 512, 4096, 0) split over the N ranks by
+shard.shard_ranges (strong scaling).  `--gpus N` without torchrun's
+environment re-launches this script under torch.distributed.run with N ranks
+(127.0.0.1 rendezvous).
 
 `--impl reference` times the reference's own CPU engine (oracle/_ref, the
 unmodified /root/reference/proj/src compiled in place) on this box's host
@@ -34,10 +39,37 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-T_TEXT, S_SPEECH, B_PER_GPU = 1024, 8192, 32
 BYTES_PER_CELL = 4 + 1 / 8 + 1  # q read + direction bit + uint8 output
 METRIC = "MAS Gcells/s (B*T*S/time) and ms/batch at B32 T1024 S8192 vs CPU ref"
-WORKLOAD = "c3: B32 T1024 S8192 fp32 maximum-path (align -> uint8 [B,T,S]), per GPU"
+# BASELINE.json configs: c3 (the metric's config, 32 items per GPU, weak
+# scaling) and c5 (256 items split over the GPUs, strong scaling).
+CONFIGS = {
+    "c3": {"B": 32, "T": 1024, "S": 8192, "scaling": "weak",
+           "workload": "c3: B32 T1024 S8192 fp32 maximum-path (align -> uint8 [B,T,S]), per GPU"},
+    "c5": {"B": 256, "T": 512, "S": 4096, "scaling": "strong",
+           "workload": "c5: B256 T512 S4096 fp32 maximum-path (align -> uint8 [B,T,S]), "
+                       "batch-sharded over the GPUs"},
+}
+L2_NOTE = "inputs larger than L2 (q per GPU >= 134 MB vs 126 MB L2), no flush"
+
+
+def workload_config(name, world):
+    """The `config` object both arms print (workload keys only, so the
+    driver's same_config check compares like with like)."""
+    c = CONFIGS[name]
+    B = c["B"] * world if c["scaling"] == "weak" else c["B"]
+    return {"workload": c["workload"], "B": c["B"], "T": c["T"], "S": c["S"],
+            "global_batch": B, "l2": L2_NOTE}
+
+
+def rank_items(name, rank, world):
+    """[b0, b1) of the batch this rank aligns."""
+    c = CONFIGS[name]
+    if c["scaling"] == "weak":
+        return rank * c["B"], (rank + 1) * c["B"]
+    from paper_2409_07704_b200.shard import shard_ranges
+
+    return shard_ranges(c["B"], world)[rank]
 
 
 def _peaks():
@@ -131,16 +163,18 @@ def _dist():
     return rank, world, local
 
 
-def cpu_reference_leg(steps, warmup, budget_s=None):
+def cpu_reference_leg(steps, warmup, budget_s=None, config="c3"):
     """Times monoalign::align (parallel engine, threads=0 = all host threads,
-    capped at B by the engine, parallel.cpp:86-91) on a pre-built config-3
-    batch.  Returns (ms list, cores, sample description)."""
+    capped at B by the engine, parallel.cpp:86-91) on a pre-built batch of
+    the config (c3: 32 items; c5: the 256-item batch).  Returns (ms list,
+    cores, sample description, cells per call)."""
     from oracle.oracle import Reference, build
 
+    c = CONFIGS[config]
     build()
     ref = Reference()
     hw = ref.hardware_threads()
-    batch = ref.timed_batch(B_PER_GPU, T_TEXT, S_SPEECH, 0)
+    batch = ref.timed_batch(c["B"], c["T"], c["S"], 0)
     try:
         for _ in range(warmup):
             batch.time("parallel", 0)
@@ -154,28 +188,27 @@ def cpu_reference_leg(steps, warmup, budget_s=None):
                 break
     finally:
         batch.close()
-    cores = min(hw, B_PER_GPU)
-    sample = (f"full config-3 batch (32x1024x8192) per align call, {len(ms)} call(s), "
-              f"monoalign::align parallel engine, threads=0 -> {cores} workers of {hw} "
+    cores = min(hw, c["B"])
+    sample = (f"full {config} batch ({c['B']}x{c['T']}x{c['S']}) per align call, {len(ms)} "
+              f"call(s), monoalign::align parallel engine, threads=0 -> {cores} workers of {hw} "
               f"hardware threads, timed with steady_clock around align only")
-    return ms, cores, sample
+    return ms, cores, sample, c["B"] * c["T"] * c["S"]
 
 
 def run_reference(args):
     rank, world, _ = _dist()
     if rank != 0:
         return 0
-    ms, cores, sample = cpu_reference_leg(args.steps, args.warmup)
-    cells = B_PER_GPU * T_TEXT * S_SPEECH
+    ms, cores, sample, cells = cpu_reference_leg(args.steps, args.warmup, config=args.config)
     tot = sum(ms) / 1e3
     value = cells * len(ms) / tot / 1e9
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "Gcells/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": len(ms), "warmup": args.warmup,
         "ms_per_step": round(statistics.mean(ms), 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "B": B_PER_GPU, "T": T_TEXT, "S": S_SPEECH,
-                   "global_batch": B_PER_GPU, "parallelism": "host threads"},
+        "scaling": CONFIGS[args.config]["scaling"], "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": workload_config(args.config, world),
+        "parallelism": "host threads",
         "cpu_baseline": {"value": round(value, 4), "unit": "Gcells/s", "cores": cores,
                          "kind": "reference", "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "Gcells/s", "h2d_bytes_per_step": 0,
@@ -196,17 +229,22 @@ def run_ours(args):
     from paper_2409_07704_b200 import _lib
 
     rank, world, local = _dist()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    B, T, S = B_PER_GPU, T_TEXT, S_SPEECH
+    c = CONFIGS[args.config]
+    b0, b1 = rank_items(args.config, rank, world)
+    B, T, S = b1 - b0, c["T"], c["S"]
     cells = B * T * S
+    total_cells = (c["B"] * world if c["scaling"] == "weak" else c["B"]) * T * S
 
-    # Inputs: this rank's shard of generate_random_batch(B * world, T, S, 0).
+    # Inputs: this rank's shard [b0, b1) of generate_random_batch(., T, S, 0).
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
-        q = mas.generate_device(B, T, S, 0, first_item=rank * B, device=dev)
+        q = mas.generate_device(B, T, S, 0, first_item=b0, device=dev)
         out = torch.empty((B, T, S), dtype=torch.uint8, device=dev)
     plan = mas.Plan(B, T, S)
     geom = plan.geometry
@@ -251,7 +289,7 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     elapsed_ms = float(tmax.item())
-    value = world * cells * K / (elapsed_ms / 1e3) / 1e9
+    value = total_cells * K / (elapsed_ms / 1e3) / 1e9
 
     # ---- e2e: the C-ABI host entry point with pinned HOST buffers ----------
     lib = _lib.load()
@@ -279,7 +317,7 @@ def run_ours(args):
     e2e_s = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    e2e_value = world * cells * e2e_steps / float(e2e_s.item()) / 1e9
+    e2e_value = total_cells * e2e_steps / float(e2e_s.item()) / 1e9
     assert torch.equal(hout, out.cpu()), "host entry point differs from the device path"
     h2d = B * T * S * 4
     d2h = B * T * S + 4 * B  # alignment bytes + NonFinite flags
@@ -325,7 +363,7 @@ def run_ours(args):
     np_s = (time.perf_counter() - t0) / np_steps
     assert np.array_equal(out_np, hout.numpy()), "numpy path differs from the device path"
     del q_np, out_np
-    numpy_line = {"value": round(world * cells / np_s / 1e9, 3), "unit": "Gcells/s",
+    numpy_line = {"value": round(total_cells / np_s / 1e9, 3), "unit": "Gcells/s",
                   "ms_per_step": round(np_s * 1e3, 2),
                   "path": "paper_2409_07704_b200.align(numpy float32 [B,T,S]) -> numpy uint8, "
                           "pageable host memory (the reference binding's call)"}
@@ -345,15 +383,15 @@ def run_ours(args):
         sc_ms.append(s0.elapsed_time(s1))
     del qs
     sc_best = statistics.median(sc_ms)
-    scores_line = {"value": round(world * cells / (sc_best / 1e3) / 1e9, 2), "unit": "Gcells/s",
+    scores_line = {"value": round(total_cells / (sc_best / 1e3) / 1e9, 2), "unit": "Gcells/s",
                    "ms_per_step": round(sc_best, 4), "bytes_per_cell": 8,
                    "path": "forward_parallel(torch CUDA tensor): the parallel engine's score "
                            "table written in place (forward_scores_kernel)"}
     durations_line = {
-        "value": round(world * cells / (dur_ms / 1e3) / 1e9, 2), "unit": "Gcells/s",
+        "value": round(total_cells / (dur_ms / 1e3) / 1e9, 2), "unit": "Gcells/s",
         "ms_per_step": round(dur_ms, 4), "bytes_per_cell": 4.125,
         "frac": None,  # filled below once the peak is known
-        "e2e": {"value": round(world * cells * e2e_steps / e2e_dur_s / 1e9, 3),
+        "e2e": {"value": round(total_cells * e2e_steps / e2e_dur_s / 1e9, 3),
                 "unit": "Gcells/s", "h2d_bytes_per_step": B * T * S * 4,
                 "d2h_bytes_per_step": B * T * 4 + 4 * B,
                 "path": "mas_align_host_ex (C-ABI), pinned host in, durations out"},
@@ -363,8 +401,9 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            ms, cores, sample = cpu_reference_leg(20, 1, budget_s=12.0)
-            cpu = {"value": round(cells * len(ms) / (sum(ms) / 1e3) / 1e9, 4),
+            ms, cores, sample, ref_cells = cpu_reference_leg(20, 1, budget_s=12.0,
+                                                             config=args.config)
+            cpu = {"value": round(ref_cells * len(ms) / (sum(ms) / 1e3) / 1e9, 4),
                    "unit": "Gcells/s", "cores": cores, "kind": "reference", "sample": sample}
         except Exception as e:  # the reference build did not travel
             cpu = {"value": None, "unit": "Gcells/s", "cores": None, "kind": "reference",
@@ -386,13 +425,12 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "Gcells/s", "n_gpus": world,
         "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": round(step_ms, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": c["scaling"], "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (bench::generate_random_batch seed 0, generated bit-identically on "
                 "the device)",
-        "config": {"workload": WORKLOAD, "B": B, "T": T, "S": S, "global_batch": B * world,
-                   "parallelism": f"batch-shard dp{world}, no collective",
-                   "l2": "inputs larger than L2 (1.07 GB q per GPU vs 126 MB L2), no flush",
-                   "geometry": geom},
+        "config": workload_config(args.config, world),
+        "parallelism": f"batch-shard dp{world}, no collective; rank 0 items [{b0}, {b1})",
+        "geometry": geom,
         "roofline": {"bound": "hbm", "kernel": "mas_fwd4_kernel", "achieved": round(achieved, 1),
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -412,14 +450,59 @@ def run_ours(args):
     return 0
 
 
+def relaunch_under_torchrun(argv, nproc):
+    """`--gpus N` without torchrun's environment: run this script again as N
+    ranks (one per GPU) through torch.distributed.run on 127.0.0.1."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + list(argv)
+    return subprocess.run(cmd).returncode
+
+
+def spawn_selftest(args):
+    """CPU check of the launch path (tests/test_bench_launch.py): every rank
+    joins a gloo group, the max-over-ranks reduction runs, rank 0 prints the
+    world it saw."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, _ = _dist()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.destroy_process_group()
+    b0, b1 = rank_items(args.config, rank, world)
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "max_over_ranks": float(t.item()),
+                          "rank0_items": [b0, b1],
+                          "config": workload_config(args.config, world)}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--spawn-selftest", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(sys.argv[1:], args.gpus)
+    if args.spawn_selftest:
+        return spawn_selftest(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
