@@ -263,6 +263,11 @@ bool cached_geometry(int B, int t_max, int S_cap, Geometry* g) {
 // The input [B*T_pad][pitch] as a 3-D tensor {columns, row groups of R,
 // row residue mod R}: one {32, 32, R} box is a 32R-row x 32-column stage of
 // mas_fwd4.cu laid out [residue][group][column] (128-byte swizzle).
+#ifndef MAS_Q_L2PROMO
+#define MAS_Q_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+constexpr CUtensorMapL2promotion kQPromotion = MAS_Q_L2PROMO;
+
 bool encode_map4(const float* q, int64_t pitch, int64_t rows_total, int64_t S, int R,
                  CUtensorMap* m) {
   EncodeTiledFn enc = get_encode_fn();
@@ -274,8 +279,8 @@ bool encode_map4(const float* q, int64_t pitch, int64_t rows_total, int64_t S, i
   const cuuint32_t box[3] = {32, 32, static_cast<cuuint32_t>(R)};
   const cuuint32_t estr[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(q), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, kQPromotion,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // The uint8 output as {columns, rows} with kZeroCols x 32R boxes

@@ -8,7 +8,7 @@ mkdir -p $O
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $O/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:mas_fwd -s 2 -c 1 \
-  -o $O/prof_fwd_$TAG -f python scratch/prof_run.py 32 1024 8192 4 > $O/ncu_fwd_$TAG.log 2>&1
+  -o $O/prof_fwd_$TAG -f python tools/prof_run.py 32 1024 8192 4 > $O/ncu_fwd_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:bt_walk -s 2 -c 1 \
-  -o $O/prof_bt_$TAG -f python scratch/prof_run.py 32 1024 8192 4 > $O/ncu_bt_$TAG.log 2>&1
+  -o $O/prof_bt_$TAG -f python tools/prof_run.py 32 1024 8192 4 > $O/ncu_bt_$TAG.log 2>&1
 ls -la $O | grep $TAG
