@@ -236,6 +236,18 @@ MAS_API int mas_backtrack_scores(const float* d_scores, int64_t row_pitch, int32
 MAS_API int mas_relax_column(const float* d_prev, float* d_cur, int32_t lanes, float sentinel,
                              void* stream, mas_error_t* err);
 
+/* ---- fused log-likelihood -----
+ * The Glow-TTS / VITS prior's log-likelihood matrix
+ *   q[b][i][j] = sum_c log N(z[b][c][j]; mean[b][c][i], exp(logstd[b][c][i]))
+ * computed on the tensor cores (bf16 operands of the expanded form, fp32
+ * accumulation).  z [batch][channels][speech_cap], mean / logstd
+ * [batch][channels][text_cap], fp32, device.  channels <= 192.  (ABI 3)
+ * mas_gaussian_loglik_device writes q [batch][text_cap][q_pitch] fp32. */
+MAS_API int mas_gaussian_loglik_device(const float* d_z, const float* d_mean,
+                                       const float* d_logstd, int32_t batch, int32_t channels,
+                                       int32_t text_cap, int32_t speech_cap, float* d_q,
+                                       int64_t q_pitch, void* stream, mas_error_t* err);
+
 /* ---- MASTENS v1 tensor files (tensor_io.hpp:11-23, tensor_io.cpp) --------
  * Host-only.  Errors are MAS_E_IO with the reference's IoError code and text
  * (IoFailure, BadMagic, UnsupportedVersion, TruncatedFile, DimensionOverflow).

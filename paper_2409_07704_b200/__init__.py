@@ -15,6 +15,7 @@ from .api import (
     align_durations,
     align_paths,
     forward_parallel,
+    gaussian_loglik,
     generate_device,
     generate_random_batch,
     read_tensor,
@@ -29,6 +30,7 @@ __all__ = [
     "generate_random_batch",
     "generate_device",
     "forward_parallel",
+    "gaussian_loglik",
     "Plan",
     "read_tensor",
     "write_tensor",

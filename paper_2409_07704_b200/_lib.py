@@ -113,6 +113,9 @@ _SIGS = {
                                             ctypes.POINTER(MasError)]),
     "mas_relax_column": (ctypes.c_int, [_VP, _VP, ctypes.c_int32, ctypes.c_float, _VP,
                                         ctypes.POINTER(MasError)]),
+    "mas_gaussian_loglik_device": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int32, ctypes.c_int32,
+                                                  ctypes.c_int32, ctypes.c_int32, _VP,
+                                                  ctypes.c_int64, _VP, ctypes.POINTER(MasError)]),
     "mas_errc_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "mas_abi_version": (ctypes.c_int, []),
 }

@@ -331,6 +331,46 @@ def forward_parallel(values, lengths=None, max_neg_val=_DEFAULT_MAX_NEG_VAL):
     return values
 
 
+# ---- fused log-likelihood ---------------------------
+def _gauss_inputs(z, mean, logstd):
+    import torch
+
+    for name, x in (("z", z), ("mean", mean), ("logstd", logstd)):
+        if not _is_torch(x) or not x.is_cuda or x.dtype != torch.float32 or x.dim() != 3:
+            raise ValueError(f"{name} must be a float32 CUDA tensor of rank 3")
+    if mean.shape != logstd.shape:
+        raise ValueError("mean and logstd must have the same shape [B, C, T]")
+    if z.shape[0] != mean.shape[0] or z.shape[1] != mean.shape[1]:
+        raise ValueError("z must be [B, C, S] with the B and C of mean / logstd")
+    if not (z.device == mean.device == logstd.device):
+        raise ValueError("z, mean and logstd must be on one device")
+    B, C, S = (int(v) for v in z.shape)
+    T = int(mean.shape[2])
+    return z.contiguous(), mean.contiguous(), logstd.contiguous(), B, C, T, S
+
+
+def gaussian_loglik(z, mean, logstd):
+    """The prior log-likelihood matrix MAS aligns:
+    q[b, i, j] = sum_c log N(z[b, c, j]; mean[b, c, i], exp(logstd[b, c, i])),
+    float32 [B, T, S] on z's device, from z [B, C, S] and mean / logstd
+    [B, C, T] (Glow-TTS / VITS layouts).  Computed on the tensor cores
+    (tcgen05, bf16 operands of the expanded square, fp32 accumulation:
+    csrc/mas_gauss.cu); the same values the fused align_gaussian uses."""
+    import torch
+
+    z, mean, logstd, B, C, T, S = _gauss_inputs(z, mean, logstd)
+    lib = _lib.load()
+    q = torch.empty((B, T, S), dtype=torch.float32, device=z.device)
+    err = _lib.MasError()
+    with torch.cuda.device(z.device):
+        st = torch.cuda.current_stream(z.device)
+        rc = lib.mas_gaussian_loglik_device(z.data_ptr(), mean.data_ptr(), logstd.data_ptr(), B, C,
+                                            T, S, q.data_ptr(), S, ctypes.c_void_p(st.cuda_stream),
+                                            ctypes.byref(err))
+    _lib.raise_for(rc, err)
+    return q
+
+
 class Plan:
     """Enqueue-only execution of the maximum-path call on device buffers
     (mas_plan_* in include/monoalign_b200.h): validation and workspace once,

@@ -22,9 +22,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 HOST_CXX = "/usr/bin/g++"  # dynamic libstdc++ 
 
 SOURCES = ["mas_abi.cu", "mas_fwd4.cu", "mas_bt.cu", "monoalign_api.cpp",
-           "mas_io.cpp", "mas_scores.cu", "mas_bench.cpp"]
+           "mas_io.cpp", "mas_scores.cu", "mas_bench.cpp", "mas_gauss.cu"]
 CLI = os.path.join(LIBDIR, "monoalign")  # the `monoalign` command line (tools/main.cpp surface)
-HEADERS = ["mas_kernels.h", "mas_ptx.cuh"]
+HEADERS = ["mas_kernels.h", "mas_ptx.cuh", "mas_umma.cuh"]
 
 
 def _stale() -> bool:

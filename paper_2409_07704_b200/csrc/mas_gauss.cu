@@ -1,0 +1,370 @@
+// mas_gauss.cu -- the log-likelihood q of the Glow-TTS / VITS prior
+// (SURVEY.md 8(f) rank 2), on the tensor cores:
+//
+//   q[b][i][j] = sum_c log N(z[b][c][j]; mean[b][c][i], exp(logstd[b][c][i]))
+//              = sum_k A[b][i][k] * B[b][k][j] + bias[b][i]
+//
+//   A[i][c]     = -0.5 exp(-2 logstd[c][i])           B[c][j]     = z[c][j]^2
+//   A[i][C + c] = mean[c][i] exp(-2 logstd[c][i])     B[C + c][j] = z[c][j]
+//   bias[i]     = sum_c (-0.5 log(2 pi) - logstd[c][i] - 0.5 mean[c][i]^2 exp(-2 logstd[c][i]))
+//
+// (the expanded form Glow-TTS computes with two matmuls), A and B in bf16,
+// accumulated in fp32 by tcgen05.mma: D[128 rows x 32 frames] per MMA group,
+// A resident in TMEM, B streamed through shared memory by TMA.
+//
+//   K4a gauss_prep_kernel  A, B (bf16, K padded to Kp = 64 * ceil(2C / 64))
+//                          and bias (fp32) from z, mean, logstd
+//   K4b gauss_q_kernel     q itself, written to HBM (the unfused path, and
+//                          the reference the fused K1 is checked against)
+//   K1g (mas_fwd4.cu)      the same MMAs feeding the DP's shared-memory
+//                          ring directly: q never reaches HBM
+//
+// K4b and K1g issue the same MMA sequence (M = 128, N = 32, K in steps of 16,
+// same descriptors) and the same bias addition, so their q values are
+// identical bit for bit.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "mas_kernels.h"
+#include "mas_ptx.cuh"
+#include "mas_umma.cuh"
+#include "monoalign_b200.h"
+
+namespace mas {
+
+namespace {
+
+// ---- K4a: operands -----------------------------------------------------------
+// One thread per (item, row) for A / bias (the C channels of a text row are
+// strided by T in mean / logstd: consecutive threads read consecutive rows),
+// one thread per (item, frame) for B (likewise for z).
+__global__ void gauss_prep_rows_kernel(const float* __restrict__ mean,
+                                       const float* __restrict__ logstd, int B, int C, int T,
+                                       int Tp, int Kp, __nv_bfloat16* __restrict__ A,
+                                       float* __restrict__ bias) {
+  const int64_t n = static_cast<int64_t>(B) * Tp;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int b = static_cast<int>(k / Tp), i = static_cast<int>(k % Tp);
+    __nv_bfloat16* a = A + k * Kp;
+    float acc = 0.f;
+    for (int c = 0; c < C; ++c) {
+      float lo = 0.f, hi = 0.f;
+      if (i < T) {
+        const int64_t x = (static_cast<int64_t>(b) * C + c) * T + i;
+        const float ls = logstd[x], m = mean[x];
+        const float inv_var = expf(-2.f * ls);
+        lo = -0.5f * inv_var;
+        hi = m * inv_var;
+        acc += -0.91893853320467274f - ls - 0.5f * m * m * inv_var;  // -0.5 log(2 pi)
+      }
+      a[c] = __float2bfloat16_rn(lo);
+      a[C + c] = __float2bfloat16_rn(hi);
+    }
+    for (int c = 2 * C; c < Kp; ++c) a[c] = __float2bfloat16_rn(0.f);
+    bias[k] = acc;
+  }
+}
+
+__global__ void gauss_prep_frames_kernel(const float* __restrict__ z, int B, int C, int S, int Sp,
+                                         int Kp, __nv_bfloat16* __restrict__ Bm) {
+  const int64_t n = static_cast<int64_t>(B) * Sp;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int b = static_cast<int>(k / Sp), j = static_cast<int>(k % Sp);
+    __nv_bfloat16* o = Bm + k * Kp;
+    for (int c = 0; c < C; ++c) {
+      const float v = j < S ? z[(static_cast<int64_t>(b) * C + c) * S + j] : 0.f;
+      o[c] = __float2bfloat16_rn(v * v);
+      o[C + c] = __float2bfloat16_rn(v);
+    }
+    for (int c = 2 * C; c < Kp; ++c) o[c] = __float2bfloat16_rn(0.f);
+  }
+}
+
+// ---- K4b: q to HBM -----------------------------------------------------------
+constexpr int kQStages = 4;       // B stages in flight
+constexpr int kQColsPerCta = 1024;
+constexpr int kQThreads = 6 * 32;  // TMA warp, MMA warp, 4 epilogue warps
+
+struct QArgs {
+  const __nv_bfloat16* A;  // [B][Tp][Kp]
+  const float* bias;       // [B][Tp]
+  float* q;                // [B][T][pitch]
+  int64_t pitch;
+  int B, T, S, Tp, Sp, Kp;
+  int tmem_cols;
+};
+
+__global__ void __launch_bounds__(kQThreads, 1)
+    gauss_q_kernel(const __grid_constant__ CUtensorMap tmb, const QArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-byte alignment for the swizzled B atoms
+  const uint32_t raw = smem_addr(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* const sbase = smem_raw + (base - raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Kp = a.Kp;
+  const uint32_t stage_bytes = static_cast<uint32_t>((Kp / umma::kAtomK) * umma::kAtomBytes);
+  const uint32_t bars = base + kQStages * stage_bytes;  // zfull[S] zfree[S] dfull[2] dempty[2]
+  const uint32_t zfull = bars, zfree = bars + 8u * kQStages;
+  const uint32_t dfull = zfree + 8u * kQStages, dempty = dfull + 16u;
+  volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(sbase + kQStages * stage_bytes + 8 * (2 * kQStages + 4));
+
+  const int tiles_t = a.Tp / umma::kM;
+  const int cblocks = (a.Sp + kQColsPerCta - 1) / kQColsPerCta;
+  const int b = blockIdx.x / (tiles_t * cblocks);
+  const int tr = (blockIdx.x / cblocks) % tiles_t;
+  const int cb = blockIdx.x % cblocks;
+  const int c0 = cb * kQColsPerCta;
+  const int nst = min(kQColsPerCta, a.Sp - c0) / umma::kN;
+  const uint32_t colA = 0, colD = static_cast<uint32_t>(Kp / 2);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kQStages; ++s) {
+      mbar_init(zfull + 8u * s, 1u);
+      mbar_init(zfree + 8u * s, 1u);
+    }
+    for (int d = 0; d < 2; ++d) {
+      mbar_init(dfull + 8u * d, 1u);
+      mbar_init(dempty + 8u * d, 4u);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) umma::tmem_alloc(smem_addr(const_cast<uint32_t*>(tmem_slot)), a.tmem_cols);
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp >= 2) {
+    // A rows of this tile into TMEM: the warp of sub-partition qd owns TMEM
+    // lanes 32 qd .. 32 qd + 31 = rows 32 qd + lane.
+    const int qd = warp & 3;
+    const int row = tr * umma::kM + 32 * qd + lane;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.A + (static_cast<int64_t>(b) * a.Tp + row) * Kp);
+    for (int c = 0; c < Kp / 2; c += 8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = src[c + e];
+      umma::tmem_st8(tmem + (static_cast<uint32_t>(32 * qd) << 16) + colA + static_cast<uint32_t>(c), v);
+    }
+    umma::tmem_wait_st();
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA: B stages
+      prefetch_tensormap(&tmb);
+      for (int m = 0; m < nst; ++m) {
+        const int s = m % kQStages;
+        if (m >= kQStages) mbar_wait(zfree + 8u * s, ((m / kQStages) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(zfull + 8u * s, stage_bytes);
+        for (int at = 0; at < Kp / umma::kAtomK; ++at)
+          tma_load_2d(base + s * stage_bytes + at * umma::kAtomBytes, &tmb, at * umma::kAtomK,
+                      b * a.Sp + c0 + m * umma::kN, zfull + 8u * s, policy_evict_first());
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issue
+      const uint32_t idesc = umma::idesc_bf16_f32(umma::kM, umma::kN);
+      for (int m = 0; m < nst; ++m) {
+        const int s = m % kQStages, d = m & 1;
+        mbar_wait(zfull + 8u * s, (m / kQStages) & 1u);
+        if (m >= 2) mbar_wait(dempty + 8u * d, ((m / 2) & 1u) ^ 1u);
+        umma::fence_after_sync();
+        umma::mma_tile(tmem + colD + static_cast<uint32_t>(d * umma::kN), tmem + colA,
+                       base + s * stage_bytes, Kp, idesc);
+        umma::mma_commit(zfree + 8u * s);
+        umma::mma_commit(dfull + 8u * d);
+      }
+    }
+  } else {  // ---- epilogue: TMEM -> +bias -> q
+    const int qd = warp & 3;
+    const int i = tr * umma::kM + 32 * qd + lane;
+    const float bi = a.bias[static_cast<int64_t>(b) * a.Tp + i];
+    float* qrow = a.q + (static_cast<int64_t>(b) * a.T + i) * a.pitch;
+    for (int m = 0; m < nst; ++m) {
+      const int d = m & 1;
+      mbar_wait(dfull + 8u * d, (m / 2) & 1u);
+      umma::fence_after_sync();
+      float v[32];
+      umma::tmem_ld32(tmem + (static_cast<uint32_t>(32 * qd) << 16) + colD + static_cast<uint32_t>(d * umma::kN), v);
+      umma::tmem_wait_ld();
+      umma::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(dempty + 8u * d) : "memory");
+      const int j0 = c0 + m * umma::kN;
+      if (i < a.T) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (j0 + e < a.S) qrow[j0 + e] = v[e] + bi;
+      }
+    }
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 2) umma::tmem_dealloc(tmem, a.tmem_cols);
+}
+
+size_t q_smem_bytes(int Kp) {
+  return 1024 + static_cast<size_t>(kQStages) * (Kp / umma::kAtomK) * umma::kAtomBytes +
+         8 * (2 * kQStages + 4) + 16;
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+}  // namespace
+
+cudaError_t gauss_alloc(int B, int C, int T, int S, cudaStream_t stream, GaussOperands* g,
+                        void** ws) {
+  g->Kp = gauss_kp(C);
+  g->Tp = (T + umma::kM - 1) / umma::kM * umma::kM;
+  g->Sp = (S + umma::kN - 1) / umma::kN * umma::kN;
+  const size_t a_bytes = static_cast<size_t>(B) * g->Tp * g->Kp * 2;
+  const size_t b_bytes = static_cast<size_t>(B) * g->Sp * g->Kp * 2;
+  const size_t bias_bytes = static_cast<size_t>(B) * g->Tp * 4;
+  char* p = nullptr;
+  const cudaError_t e = pool_alloc(reinterpret_cast<void**>(&p), a_bytes + b_bytes + bias_bytes, stream);
+  if (e != cudaSuccess) return e;
+  *ws = p;
+  g->A = reinterpret_cast<__nv_bfloat16*>(p);
+  g->B = reinterpret_cast<__nv_bfloat16*>(p + a_bytes);
+  g->bias = reinterpret_cast<float*>(p + a_bytes + b_bytes);
+  return cudaSuccess;
+}
+
+int gauss_kp(int C) { return ((2 * C + umma::kAtomK - 1) / umma::kAtomK) * umma::kAtomK; }
+
+bool encode_gauss_b_map(const void* Bm, int64_t rows, int Kp, CUtensorMap* m) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(Kp) * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(umma::kAtomK), static_cast<cuuint32_t>(umma::kN)};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(Bm), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t gauss_prep(const float* z, const float* mean, const float* logstd, int B, int C, int T,
+                       int S, const GaussOperands& g, cudaStream_t stream) {
+  const int sms = sm_count();
+  const int64_t nr = static_cast<int64_t>(B) * g.Tp, nf = static_cast<int64_t>(B) * g.Sp;
+  gauss_prep_rows_kernel<<<static_cast<unsigned>(std::min<int64_t>((nr + 127) / 128, sms * 8)), 128, 0,
+                           stream>>>(mean, logstd, B, C, T, g.Tp, g.Kp, g.A, g.bias);
+  gauss_prep_frames_kernel<<<static_cast<unsigned>(std::min<int64_t>((nf + 127) / 128, sms * 8)), 128, 0,
+                             stream>>>(z, B, C, S, g.Sp, g.Kp, g.B);
+  return cudaGetLastError();
+}
+
+cudaError_t gauss_q(const GaussOperands& g, int B, int T, int S, float* q, int64_t pitch,
+                    cudaStream_t stream) {
+  CUtensorMap tmb;
+  if (!encode_gauss_b_map(g.B, static_cast<int64_t>(B) * g.Sp, g.Kp, &tmb)) return cudaErrorInvalidValue;
+  const size_t smem = q_smem_bytes(g.Kp);
+  constexpr int kMaxDevices = 64;
+  static std::once_flag once[kMaxDevices];
+  static cudaError_t status[kMaxDevices];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || dev >= kMaxDevices) return e != cudaSuccess ? e : cudaErrorInvalidDevice;
+  std::call_once(once[dev], [dev] {
+    status[dev] = cudaFuncSetAttribute(gauss_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       q_smem_bytes(gauss_kp(kGaussMaxChannels)));
+  });
+  if (status[dev] != cudaSuccess) return status[dev];
+  QArgs qa;
+  qa.A = g.A;
+  qa.bias = g.bias;
+  qa.q = q;
+  qa.pitch = pitch;
+  qa.B = B;
+  qa.T = T;
+  qa.S = S;
+  qa.Tp = g.Tp;
+  qa.Sp = g.Sp;
+  qa.Kp = g.Kp;
+  qa.tmem_cols = static_cast<int>(umma::tmem_cols_pow2(static_cast<uint32_t>(g.Kp / 2 + 2 * umma::kN)));
+  const int tiles = g.Tp / umma::kM, cblocks = (g.Sp + kQColsPerCta - 1) / kQColsPerCta;
+  gauss_q_kernel<<<static_cast<unsigned>(B * tiles * cblocks), kQThreads, smem, stream>>>(tmb, qa);
+  return cudaGetLastError();
+}
+
+}  // namespace mas
+
+extern "C" {
+
+int mas_gaussian_loglik_device(const float* d_z, const float* d_mean, const float* d_logstd,
+                               int32_t batch, int32_t channels, int32_t text_cap,
+                               int32_t speech_cap, float* d_q, int64_t q_pitch, void* stream_v,
+                               mas_error_t* err) {
+  if (err) {
+    std::memset(err, 0, sizeof(*err));
+    err->item = -1;
+    err->i = err->j = -1;
+  }
+  auto fail = [&](int status, int errc, const std::string& msg) {
+    if (err) {
+      err->status = status;
+      err->errc = errc;
+      std::snprintf(err->message, sizeof(err->message), "%s", msg.c_str());
+    }
+    return status;
+  };
+  if (batch < 1 || channels < 1 || text_cap < 1 || speech_cap < 1)
+    return fail(MAS_E_VALIDATION, MAS_ERRC_ZERO_DIM, "every dimension must be at least 1");
+  if (channels > mas::kGaussMaxChannels)
+    return fail(MAS_E_UNSUPPORTED, -1,
+                "gaussian log-likelihood: at most " + std::to_string(mas::kGaussMaxChannels) +
+                    " channels");
+  if (q_pitch < speech_cap)
+    return fail(MAS_E_VALIDATION, MAS_ERRC_SHAPE_MISMATCH, "row pitch is smaller than the speech capacity");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  mas::GaussOperands g;
+  void* ws = nullptr;
+  cudaError_t e = mas::gauss_alloc(batch, channels, text_cap, speech_cap, stream, &g, &ws);
+  if (e == cudaSuccess)
+    e = mas::gauss_prep(d_z, d_mean, d_logstd, batch, channels, text_cap, speech_cap, g, stream);
+  if (e == cudaSuccess) e = mas::gauss_q(g, batch, text_cap, speech_cap, d_q, q_pitch, stream);
+  if (ws) {
+    const cudaError_t f = cudaFreeAsync(ws, stream);
+    if (e == cudaSuccess) e = f;
+  }
+  if (e != cudaSuccess)
+    return fail(MAS_E_CUDA, -1, std::string("gaussian log-likelihood: ") + cudaGetErrorString(e));
+  return MAS_OK;
+}
+
+}  // extern "C"

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -24,6 +25,24 @@ constexpr int kMaxClusterCtas = 16;
 // Stream-ordered device allocation from the library's own pool on the
 // current device (mas_abi.cu); free with cudaFreeAsync.
 cudaError_t pool_alloc(void** ptr, size_t bytes, cudaStream_t stream);
+
+// mas_gauss.cu: the Gaussian log-likelihood operands (bf16, K-major, K
+// padded to Kp = 64 * ceil(2C / 64); rows padded to Tp = 128 * ceil(T / 128),
+// frames to Sp = 32 * ceil(S / 32)).
+constexpr int kGaussMaxChannels = 192;  // Kp <= 384: A (Kp/2) + D fit TMEM's 512 columns at W = 2
+struct GaussOperands {
+  __nv_bfloat16* A;  // [B][Tp][Kp]  row coefficients
+  __nv_bfloat16* B;  // [B][Sp][Kp]  z^2, z per frame
+  float* bias;       // [B][Tp]
+  int Tp, Sp, Kp;
+};
+int gauss_kp(int C);
+cudaError_t gauss_alloc(int B, int C, int T, int S, cudaStream_t stream, GaussOperands* g, void** ws);
+cudaError_t gauss_prep(const float* z, const float* mean, const float* logstd, int B, int C, int T,
+                       int S, const GaussOperands& g, cudaStream_t stream);
+cudaError_t gauss_q(const GaussOperands& g, int B, int T, int S, float* q, int64_t pitch,
+                    cudaStream_t stream);
+bool encode_gauss_b_map(const void* Bm, int64_t rows, int Kp, CUtensorMap* m);
 
 struct FwdArgs {
   int b0;                   // first item of this launch (items b0 .. b0 + grid/K - 1)
