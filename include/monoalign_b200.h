@@ -247,6 +247,20 @@ MAS_API int mas_gaussian_loglik_device(const float* d_z, const float* d_mean,
                                        const float* d_logstd, int32_t batch, int32_t channels,
                                        int32_t text_cap, int32_t speech_cap, float* d_q,
                                        int64_t q_pitch, void* stream, mas_error_t* err);
+/* The maximum-path call on that q without materialising it: the forward
+ * kernel computes each 32-frame tile of q on the tensor cores (A in TMEM, B
+ * by TMA) and feeds it straight to the DP, so q never reaches HBM.  Same
+ * outputs, validation, errors and engines as mas_align_device_ex (lengths a
+ * HOST [batch][2] array or NULL; a non-finite q is reported at its exact
+ * (i, j)); the alignment equals mas_align_device_ex on the q
+ * mas_gaussian_loglik_device writes, bit for bit.  Texts up to one cluster of
+ * rows (4096 at 192 channels).  Synchronises `stream`.  (ABI 3) */
+MAS_API int mas_align_gaussian_device(const float* d_z, const float* d_mean,
+                                      const float* d_logstd, int32_t batch, int32_t channels,
+                                      int32_t text_cap, int32_t speech_cap,
+                                      const uint32_t* lengths, const mas_config_t* cfg,
+                                      uint8_t* d_out, int32_t* d_paths, int32_t* d_durations,
+                                      void* stream, mas_error_t* err);
 
 /* ---- MASTENS v1 tensor files (tensor_io.hpp:11-23, tensor_io.cpp) --------
  * Host-only.  Errors are MAS_E_IO with the reference's IoError code and text

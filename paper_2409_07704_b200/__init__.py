@@ -13,6 +13,7 @@ from .api import (
     _align_unchecked,
     align,
     align_durations,
+    align_gaussian,
     align_paths,
     forward_parallel,
     gaussian_loglik,
@@ -27,6 +28,7 @@ __all__ = [
     "align",
     "align_paths",
     "align_durations",
+    "align_gaussian",
     "generate_random_batch",
     "generate_device",
     "forward_parallel",

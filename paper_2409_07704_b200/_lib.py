@@ -116,6 +116,10 @@ _SIGS = {
     "mas_gaussian_loglik_device": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int32, ctypes.c_int32,
                                                   ctypes.c_int32, ctypes.c_int32, _VP,
                                                   ctypes.c_int64, _VP, ctypes.POINTER(MasError)]),
+    "mas_align_gaussian_device": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int32, ctypes.c_int32,
+                                                 ctypes.c_int32, ctypes.c_int32, _VP,
+                                                 ctypes.POINTER(MasConfig), _VP, _VP, _VP, _VP,
+                                                 ctypes.POINTER(MasError)]),
     "mas_errc_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "mas_abi_version": (ctypes.c_int, []),
 }

@@ -371,6 +371,47 @@ def gaussian_loglik(z, mean, logstd):
     return q
 
 
+def align_gaussian(z, mean, logstd, lengths=None, engine="parallel",
+                   max_neg_val=_DEFAULT_MAX_NEG_VAL, outputs=("alignment",), unchecked=False):
+    """The maximum-path call on q = gaussian_loglik(z, mean, logstd) without
+    materialising q: the forward kernel
+    computes each 32-frame tile of q on the tensor cores and feeds it to the
+    DP directly.  z [B, C, S], mean / logstd [B, C, T] float32 CUDA tensors;
+    lengths [B, 2] of (t, s) as in align.  Returns a dict with the requested
+    `outputs` among "alignment" (uint8 [B, T, S]), "paths" (int32 [B, S], -1
+    past s_b) and "durations" (int32 [B, T]).  Equal, bit for bit, to
+    align(gaussian_loglik(z, mean, logstd), ...) for the same arguments."""
+    import torch
+
+    z, mean, logstd, B, C, T, S = _gauss_inputs(z, mean, logstd)
+    lens = None if lengths is None else _parse_lengths(lengths, B, T, S)
+    cfg = _make_config(engine, max_neg_val, 0, unchecked)
+    bad = set(outputs) - {"alignment", "paths", "durations"}
+    if bad:
+        raise ValueError(f"unknown outputs: {sorted(bad)}")
+    dev = z.device
+    res = {}
+    if "alignment" in outputs:
+        res["alignment"] = torch.empty((B, T, S), dtype=torch.uint8, device=dev)
+    if "paths" in outputs:
+        res["paths"] = torch.empty((B, S), dtype=torch.int32, device=dev)
+    if "durations" in outputs:
+        res["durations"] = torch.empty((B, T), dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    err = _lib.MasError()
+    with torch.cuda.device(dev):
+        st = torch.cuda.current_stream(dev)
+        rc = lib.mas_align_gaussian_device(
+            z.data_ptr(), mean.data_ptr(), logstd.data_ptr(), B, C, T, S,
+            None if lens is None else lens.ctypes.data, ctypes.byref(cfg),
+            res["alignment"].data_ptr() if "alignment" in res else None,
+            res["paths"].data_ptr() if "paths" in res else None,
+            res["durations"].data_ptr() if "durations" in res else None,
+            ctypes.c_void_p(st.cuda_stream), ctypes.byref(err))
+    _lib.raise_for(rc, err)
+    return res
+
+
 class Plan:
     """Enqueue-only execution of the maximum-path call on device buffers
     (mas_plan_* in include/monoalign_b200.h): validation and workspace once,

@@ -165,7 +165,7 @@ struct Geometry {
   int band_rows = 128;
 };
 
-bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
+bool choose_geometry(int B, int t_max, int S_cap, Geometry* g, int kp) {
   int sms = 148;
   {
     int dev = 0;
@@ -201,16 +201,19 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
     int best_bands = 0;
     for (int c = 0; c < ncand && !(best >= 0 && best_waves == 1); ++c) {
       const int W = std::min(cand[c][0], warps_total), N = cand[c][1];
-      if (mas::fwd4_smem_bytes(g->R, W, N) > budget) continue;
+      if (mas::fwd4_smem_bytes(g->R, W, N, kp) > budget) continue;
+      // Gaussian source: A (Kp/2 columns per warp) and two 32-column
+      // accumulators per warp in TMEM's 512 columns; one band only
+      if (kp > 0 && W * kp / 2 + 2 * W * 32 > 512) continue;
       int last_K = -1;
-      for (int nb = 1; nb <= warps_total; ++nb) {
+      for (int nb = 1; nb <= (kp > 0 ? 1 : warps_total); ++nb) {
         const int per_band = (warps_total + nb - 1) / nb;
-        if (per_band > band_warps_cap) continue;
+        if (per_band > band_warps_cap && kp == 0) continue;
         const int K = (per_band + W - 1) / W;
         if (K > mas::kMaxClusterCtas || K == last_K) continue;
         last_K = K;
         const int bands = (warps_total + K * W - 1) / (K * W);
-        const int act = mas::fwd4_max_active_clusters(g->R, W, N, K);
+        const int act = mas::fwd4_max_active_clusters(g->R, W, N, K, kp);
         if (act <= 0) continue;
         const int64_t waves = (static_cast<int64_t>(B) * bands + act - 1) / act;
         if (best < 0 || waves < best_waves || (waves == best_waves && bands < best_bands)) {
@@ -235,9 +238,9 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g) {
 // choose_geometry queries the occupancy API for every candidate (tens of
 // microseconds per call); plans of the same shape on the same device reuse
 // the answer.
-bool cached_geometry(int B, int t_max, int S_cap, Geometry* g) {
+bool cached_geometry(int B, int t_max, int S_cap, Geometry* g, int kp = 0) {
   struct Entry {
-    int dev, B, t, S;
+    int dev, B, t, S, kp;
     Geometry g;
     bool ok;
   };
@@ -248,15 +251,15 @@ bool cached_geometry(int B, int t_max, int S_cap, Geometry* g) {
   {
     std::lock_guard<std::mutex> lk(mu);
     for (const Entry& e : cache)
-      if (e.dev == dev && e.B == B && e.t == t_max && e.S == S_cap) {
+      if (e.dev == dev && e.B == B && e.t == t_max && e.S == S_cap && e.kp == kp) {
         *g = e.g;
         return e.ok;
       }
   }
-  const bool ok = choose_geometry(B, t_max, S_cap, g);
+  const bool ok = choose_geometry(B, t_max, S_cap, g, kp);
   std::lock_guard<std::mutex> lk(mu);
   if (cache.size() >= 256) cache.erase(cache.begin());
-  cache.push_back({dev, B, t_max, S_cap, *g, ok});
+  cache.push_back({dev, B, t_max, S_cap, kp, *g, ok});
   return ok;
 }
 
@@ -375,6 +378,10 @@ struct mas_plan {
   std::vector<std::pair<cudaStream_t, cudaEvent_t>> done;
   bool captured = false;  // enqueued while a stream was capturing
   bool nan_parallel = false;  // parallel engine, NaN sentinel (unchecked): score-table forward
+  // Gaussian source (mas_align_gaussian_device): K1 computes q from these
+  int gauss_kp = 0;
+  const mas::GaussOperands* gauss = nullptr;
+  const CUtensorMap* gauss_map = nullptr;
 };
 
 extern "C" {
@@ -426,7 +433,7 @@ void mas_plan_destroy(mas_plan_t* p) {
 namespace {
 int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row_pitch,
                 const uint32_t* lengths, const mas_config_t* cfg_in, int item_base,
-                mas_plan_t** plan_out, mas_error_t* err, bool deferred = false);
+                mas_plan_t** plan_out, mas_error_t* err, bool deferred = false, int gauss_kp = 0);
 }  // namespace
 
 extern "C" {
@@ -446,7 +453,7 @@ namespace {
 // mas_align_host / _device, whose enqueues are never captured).
 int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row_pitch,
                 const uint32_t* lengths, const mas_config_t* cfg_in, int item_base,
-                mas_plan_t** plan_out, mas_error_t* err, bool deferred) {
+                mas_plan_t** plan_out, mas_error_t* err, bool deferred, int gauss_kp) {
   clear_error(err);
   *plan_out = nullptr;
   mas_config_t cfg;
@@ -472,7 +479,8 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
   p->T_pad = text_cap;
   p->mode = cfg.engine == MAS_ENGINE_REFERENCE ? 1 : 0;
   p->mnv = cfg.max_neg_val;
-  p->nan_parallel = p->mode == 0 && std::isnan(cfg.max_neg_val);
+  p->nan_parallel = p->mode == 0 && std::isnan(cfg.max_neg_val) && gauss_kp == 0;
+  p->gauss_kp = gauss_kp;
   p->lengths.resize(static_cast<size_t>(batch) * 2);
   int t_max = 0;
   for (int b = 0; b < batch; ++b) {
@@ -496,7 +504,7 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
     delete p;
     return set_error(err, MAS_E_CUDA, -1, -1, "forward kernel configuration failed");
   }
-  if (!cached_geometry(batch, std::max(t_max, 1), speech_cap, &p->geo)) {
+  if (!cached_geometry(batch, std::max(t_max, 1), speech_cap, &p->geo, gauss_kp)) {
     delete p;
     return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
                      "no launch geometry fits this shape on the device");
@@ -562,7 +570,7 @@ extern "C" {
 int mas_plan_launches(const mas_plan_t* p) { return p ? p->launches : 0; }
 
 void mas_plan_geometry(const mas_plan_t* p, int32_t geom[6]) {
-  geom[5] = mas::fwd4_max_active_clusters(p->geo.R, p->geo.W, p->geo.N, p->geo.K);
+  geom[5] = mas::fwd4_max_active_clusters(p->geo.R, p->geo.W, p->geo.N, p->geo.K, p->gauss_kp);
   geom[0] = 32 * p->geo.R;
   geom[1] = p->geo.W;
   geom[2] = p->geo.K;
@@ -579,7 +587,8 @@ namespace {
 int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_values,
                   uint8_t* d_out, int32_t* d_paths, int32_t* d_dur, cudaStream_t stream,
                   mas_error_t* err) {
-  if ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (p->pitch & 3) != 0 || (p->T_pad & 3))
+  if (!p->gauss &&
+      ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (p->pitch & 3) != 0 || (p->T_pad & 3)))
     return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
                      "device layout needs a 16-byte base, pitch % 4 == 0 and text_cap % 4 == 0");
   const Geometry& g = p->geo;
@@ -624,7 +633,9 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     // once per input pointer and reused by later enqueues (host cost).
     const bool reuse_in = p->tm_in_ptr == d_values && p->tm_in_pitch == p->pitch &&
                           p->tm_in_tpad == p->T_pad;
-    if (reuse_in) {
+    if (p->gauss) {
+      tm0 = *p->gauss_map;
+    } else if (reuse_in) {
       tm0 = p->tm_in;
     } else if (!encode_map4(d_values, p->pitch, static_cast<int64_t>(p->B) * p->T_pad, p->S, g.R,
                             &tm0)) {
@@ -635,7 +646,7 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
       p->tm_in_pitch = p->pitch;
       p->tm_in_tpad = p->T_pad;
     }
-    mas::FwdArgs fa;
+    mas::FwdArgs fa = {};
     fa.b0 = b0;
     fa.lengths = p->d_lengths;
     fa.dirs = p->d_dirs;
@@ -708,6 +719,13 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     fa.nb = nb;
     fa.bnd = p->d_bnd;
     fa.bnd_pitch = p->bnd_pitch;
+    if (p->gauss) {
+      fa.Kp = p->gauss->Kp;
+      fa.Tp = p->gauss->Tp;
+      fa.Sp = p->gauss->Sp;
+      fa.gA = p->gauss->A;
+      fa.gbias = p->gauss->bias;
+    }
     fa.ticket = p->d_sync ? p->d_sync + b0 : nullptr;
     fa.progress = p->d_sync ? p->d_sync + p->B : nullptr;
     // All bands of all items in one launch (clusters ordered by ticket).
@@ -1296,6 +1314,70 @@ int mas_generate_device(uint64_t seed, int32_t batch, int32_t text_cap, int32_t 
   const cudaError_t e = mas::launch_generate(s0, first_elem, batch, text_cap, speech_cap, row_pitch,
                                              d_out, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? MAS_OK : MAS_E_CUDA;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int mas_align_gaussian_device(const float* d_z, const float* d_mean, const float* d_logstd,
+                              int32_t batch, int32_t channels, int32_t text_cap,
+                              int32_t speech_cap, const uint32_t* lengths, const mas_config_t* cfg,
+                              uint8_t* d_out, int32_t* d_paths, int32_t* d_durations,
+                              void* stream_v, mas_error_t* err) {
+  clear_error(err);
+  if (channels < 1)
+    return set_error(err, MAS_E_VALIDATION, MAS_ERRC_ZERO_DIM, -1,
+                     "every dimension must be at least 1");
+  if (channels > mas::kGaussMaxChannels)
+    return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
+                     "gaussian log-likelihood: at most " + std::to_string(mas::kGaussMaxChannels) +
+                         " channels");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  mas_plan_t* plan = nullptr;
+  int rc = plan_create(batch, text_cap, speech_cap, speech_cap, lengths, cfg, 0, &plan, err, true,
+                       mas::gauss_kp(channels));
+  if (rc) return rc;
+  plan->internal = true;
+  mas::GaussOperands g;
+  void* ws = nullptr;
+  CUtensorMap tmb;
+  cudaError_t e = mas::gauss_alloc(batch, channels, text_cap, speech_cap, stream, &g, &ws);
+  if (e == cudaSuccess)
+    e = mas::gauss_prep(d_z, d_mean, d_logstd, batch, channels, text_cap, speech_cap, g, stream);
+  if (e == cudaSuccess && !mas::encode_gauss_b_map(g.B, static_cast<int64_t>(batch) * g.Sp, g.Kp, &tmb))
+    e = cudaErrorInvalidValue;
+  if (e == cudaSuccess) {
+    plan->gauss = &g;
+    plan->gauss_map = &tmb;
+    rc = enqueue_items(plan, MAS_PART_ALL, 0, batch, nullptr, d_out, d_paths, d_durations, stream,
+                       err);
+    // NonFinite: the compute warps flag items whose q is not finite; only
+    // then is q materialised (error path) for the exact row-major location.
+    std::vector<int> flags(static_cast<size_t>(batch));
+    if (rc == MAS_OK &&
+        (e = cudaMemcpyAsync(flags.data(), plan->d_flags, sizeof(int) * batch,
+                             cudaMemcpyDeviceToHost, stream)) == cudaSuccess &&
+        (e = cudaStreamSynchronize(stream)) == cudaSuccess) {
+      float* q = nullptr;
+      bool any = false;
+      for (int f : flags) any = any || f != 0;
+      if (any) {
+        e = mas::pool_alloc(reinterpret_cast<void**>(&q),
+                            static_cast<size_t>(batch) * text_cap * speech_cap * sizeof(float), stream);
+        if (e == cudaSuccess) e = mas::gauss_q(g, batch, text_cap, speech_cap, q, speech_cap, stream);
+      }
+      if (e == cudaSuccess) rc = mas_plan_finish(plan, q, stream, err);
+      if (q) cudaFreeAsync(q, stream);
+    }
+  }
+  if (ws) cudaFreeAsync(ws, stream);
+  cudaStreamSynchronize(stream);
+  plan->gauss = nullptr;
+  plan->gauss_map = nullptr;
+  mas_plan_destroy(plan);
+  if (e != cudaSuccess) return cuda_error(err, e, "gaussian alignment");
+  return rc;
 }
 
 }  // extern "C"

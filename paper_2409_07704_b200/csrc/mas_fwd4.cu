@@ -36,6 +36,7 @@
 
 #include "mas_kernels.h"
 #include "mas_ptx.cuh"
+#include "mas_umma.cuh"
 
 namespace mas {
 
@@ -71,9 +72,15 @@ constexpr int kFifoIt4 = kFifoSlots / kQuadsPerStage;  // FIFO depth in stages
 
 struct Smem4 {
   uint32_t ring, bars, ebars, full, empty, sink, fifo, zero, ticket, total;
+  // Gaussian source (SRC 1): B operand stages, their barriers, TMEM slot
+  uint32_t zst, zbars, tslot;
 };
 
-__host__ __device__ inline Smem4 smem4_layout(int R, int W, int N) {
+// Gaussian source: B stages in flight, TMEM accumulator buffers.
+constexpr int kGStages = 3;
+constexpr int kGAcc = 2;
+
+__host__ __device__ inline Smem4 smem4_layout(int R, int W, int N, int Kp = 0) {
   Smem4 L;
   L.ring = 0;
   L.bars = static_cast<uint32_t>(W * N * stage_bytes(R));
@@ -89,6 +96,14 @@ __host__ __device__ inline Smem4 smem4_layout(int R, int W, int N) {
   L.zero = L.fifo + static_cast<uint32_t>((W + 1) * kFifoSlots * kSlot4);
   L.ticket = L.zero + static_cast<uint32_t>(rows_of(R) * kZCols);  // after the uint8 zero tile
   L.total = L.ticket + 16u;
+  L.zst = L.zbars = L.tslot = L.total;
+  if (Kp > 0) {
+    // zfull[kGStages] zfree[kGStages] dfull[kGAcc] dempty[kGAcc] aready, then the slot
+    L.zst = (L.total + 1023u) & ~1023u;
+    L.zbars = L.zst + static_cast<uint32_t>(kGStages * (Kp / umma::kAtomK) * umma::kAtomBytes);
+    L.tslot = (L.zbars + static_cast<uint32_t>((2 * kGStages + 2 * kGAcc + 1) * 8) + 15u) & ~15u;
+    L.total = L.tslot + 16u;
+  }
   return L;
 }
 
@@ -332,7 +347,14 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
                : "memory");
 }
 
-template <int R, int MODE>
+// SRC 0: q streamed from HBM by TMA.  SRC 1: q computed in the CTA from the
+// Gaussian prior (mas_gauss.cu operands): tmq is then the map of the B
+// operand; the producer warp's lane 0 loads B stages, warp W+1 issues the
+// tcgen05 MMAs (A resident in TMEM; the whole warp waits, one lane issues),
+// and four epilogue warps (warps W+2..W+5, one per TMEM sub-partition) add
+// the row bias and write each 32-column tile into the compute warps' ring in
+// the layout TMA would have used.  The compute warps run unchanged.
+template <int R, int MODE, int SRC>
 __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     mas_fwd4_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tm_out,
                     const FwdArgs a) {
@@ -344,7 +366,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   const int N = a.N;
   constexpr int kRows4 = rows_of(R);
   constexpr int kStage4 = stage_bytes(R);
-  const Smem4 SL = smem4_layout(R, W, N);
+  const Smem4 SL = smem4_layout(R, W, N, SRC ? a.Kp : 0);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -388,7 +410,9 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     uint8_t* const my_fifo = sbase + SL.fifo + warp * kFifoSlots * kSlot4;
     if (lane == 0) {
       for (int s = 0; s < N; ++s) {
-        mbar_init(bar0 + 8u * s, 1u);   // stage loaded (producer's expect_tx + TMA bytes)
+        // stage loaded: the producer's expect_tx + TMA bytes, or the four
+        // epilogue warps of the Gaussian source
+        mbar_init(bar0 + 8u * s, SRC ? 4u : 1u);
         mbar_init(ebar0 + 8u * s, 1u);  // stage consumed (this warp's lane 0)
       }
       for (int s = 0; s < kFifoSlots; ++s) mbar_init(my_full + 8u * s, 1u);
@@ -401,7 +425,7 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
       for (int k = lane; k < kFifoSlots * kQuad; k += 32)
         reinterpret_cast<float*>(my_fifo)[k] = a.row0_up;
     }
-  } else {
+  } else if (warp == W) {
     for (int k = lane; k < kRows4 * kZCols / 16; k += 32)
       reinterpret_cast<uint4*>(sbase + SL.zero)[k] = make_uint4(0u, 0u, 0u, 0u);
     if (lane == 0) {
@@ -411,6 +435,21 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
         mbar_init(base + SL.full + static_cast<uint32_t>((W * kFifoSlots + s) * 8), 1u);
     }
   }
+  uint32_t tmem = 0, tmem_cols = 0;
+  if constexpr (SRC == 1) {
+    tmem_cols = umma::tmem_cols_pow2(static_cast<uint32_t>(W * a.Kp / 2 + kGAcc * W * umma::kN));
+    if (warp == W + 2) {
+      if (lane == 0) {
+        for (int k = 0; k < 2 * kGStages + 2 * kGAcc + 1; ++k) {
+          const bool dempty = k >= 2 * kGStages + kGAcc && k < 2 * kGStages + 2 * kGAcc;
+          const bool aready = k == 2 * kGStages + 2 * kGAcc;
+          mbar_init(base + SL.zbars + 8u * k, dempty || aready ? 4u : 1u);
+        }
+      }
+      umma::tmem_alloc(base + SL.tslot, tmem_cols);
+    }
+    umma::fence_before_sync();
+  }
   // the item's NonFinite flag starts at 0 (set by atomicOr only after the
   // cluster barrier below, and in the bands below after this band's
   // progress releases)
@@ -419,6 +458,121 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   fence_mbar_init();
   cluster_sync_all();  // every CTA's FIFO / stage barriers exist before any use
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if constexpr (SRC == 1) {
+    umma::fence_after_sync();
+    tmem = *reinterpret_cast<volatile uint32_t*>(sbase + SL.tslot);
+  }
+
+  if (SRC == 1 && warp == W + 1) {
+    // ---- Gaussian source, MMA warp: waits converged, lane 0 issues --------
+    const uint32_t zb = base + SL.zbars;
+    const uint32_t zfull = zb, zfree = zb + 8u * kGStages;
+    const uint32_t dfull = zb + 8u * (2 * kGStages), dempty = dfull + 8u * kGAcc;
+    const uint32_t aready = dempty + 8u * kGAcc;
+    const uint32_t stage_bytes = static_cast<uint32_t>((a.Kp / umma::kAtomK) * umma::kAtomBytes);
+    int wl = 0;
+    for (int v = 0; v < W; ++v)
+      if (s_b > 0 && band + (crank * W + v) * kRows4 < t_b) wl = v + 1;
+    if (wl > 0) {
+      const uint32_t idesc = umma::idesc_bf16_f32(umma::kM, umma::kN);
+      mbar_wait(aready, 0u);
+      umma::fence_after_sync();
+      for (int m = 0; m < nit; ++m) {
+        const int zs = m % kGStages, d = m % kGAcc;
+        mbar_wait(zfull + 8u * zs, static_cast<uint32_t>(m / kGStages) & 1u);
+        if (m >= kGAcc) mbar_wait(dempty + 8u * d, (static_cast<uint32_t>(m / kGAcc) & 1u) ^ 1u);
+        umma::fence_after_sync();
+        __syncwarp();
+        if (lane == 0) {
+          for (int v = 0; v < wl; ++v)
+            umma::mma_tile(tmem + static_cast<uint32_t>(W * a.Kp / 2 + (d * W + v) * umma::kN),
+                           tmem + static_cast<uint32_t>(v * a.Kp / 2),
+                           base + SL.zst + zs * stage_bytes, a.Kp, idesc);
+          umma::mma_commit(zfree + 8u * zs);
+          umma::mma_commit(dfull + 8u * d);
+        }
+        __syncwarp();
+      }
+    }
+    __syncwarp();
+    cluster_sync_all();
+    return;
+  }
+
+  if (SRC == 1 && warp > W + 1) {
+    // ---- Gaussian source, epilogue warp of TMEM sub-partition qd ----------
+    const int qd = warp & 3;
+    const uint32_t zb = base + SL.zbars;
+    const uint32_t dfull = zb + 8u * (2 * kGStages), dempty = dfull + 8u * kGAcc;
+    const uint32_t aready = dempty + 8u * kGAcc;
+    const uint32_t lane_base = static_cast<uint32_t>(32 * qd) << 16;
+#ifdef MAS_GAUSS_DEBUG
+    if (lane == 0)
+      printf("cta %d warp %d tmem %08x cols %u W %d N %d Kp %d Tp %d tslot %u base %u\n", blockIdx.x,
+             warp, tmem, tmem_cols, W, N, a.Kp, a.Tp, SL.tslot, base);
+#endif
+    int wl = 0;  // compute warps of this CTA with rows to align
+    for (int w = 0; w < W; ++w)
+      if (s_b > 0 && band + (crank * W + w) * kRows4 < t_b) wl = w + 1;
+    float bias[4];
+    for (int w = 0; w < W && w < 4; ++w) {
+      // rows i0w + 32 qd + lane: their A rows into TMEM, their bias into registers
+      const int row = band + (crank * W + w) * kRows4 + 32 * qd + lane;
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(a.gA) +
+                            (static_cast<int64_t>(b) * a.Tp + row) * (a.Kp / 2);
+      if (w < wl) {
+        for (int c = 0; c < a.Kp / 2; c += 8) {
+          uint32_t v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = __ldg(src + c + e);
+          umma::tmem_st8(tmem + lane_base + static_cast<uint32_t>(w * a.Kp / 2 + c), v);
+        }
+        bias[w] = __ldg(a.gbias + static_cast<int64_t>(b) * a.Tp + row);
+      }
+    }
+    umma::tmem_wait_st();
+    umma::fence_before_sync();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_local(aready);
+    const int grp = 32 * qd + lane;  // row within each warp's 128-row tile
+    const uint32_t rbase = static_cast<uint32_t>((grp & 3) * 4096 + (grp >> 2) * 128);
+    const uint32_t sw = static_cast<uint32_t>((grp >> 2) & 7);
+    for (int m = 0; m < (wl > 0 ? nit : 0); ++m) {
+      const int d = m % kGAcc;
+      mbar_wait(dfull + 8u * d, static_cast<uint32_t>(m / kGAcc) & 1u);
+      umma::fence_after_sync();
+      float v[4][32];
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        if (w < wl)
+          umma::tmem_ld32(tmem + lane_base + static_cast<uint32_t>(W * a.Kp / 2 + (d * W + w) * umma::kN), v[w]);
+      umma::tmem_wait_ld();
+      umma::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(dempty + 8u * d);
+      const int st = m % N;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        if (w >= wl) continue;
+        if (m >= N)  // ring slot st of warp w consumed in iteration m - N
+          mbar_wait(base + SL.ebars + static_cast<uint32_t>((w * N + st) * 8),
+                    (static_cast<uint32_t>(m / N) & 1u) ^ 1u);
+        uint8_t* dst = sbase + SL.ring + (w * N + st) * kStage4 + rbase;
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4)
+          *reinterpret_cast<float4*>(dst + ((c4 ^ sw) << 4)) =
+              make_float4(v[w][4 * c4] + bias[w], v[w][4 * c4 + 1] + bias[w],
+                          v[w][4 * c4 + 2] + bias[w], v[w][4 * c4 + 3] + bias[w]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_local(base + SL.bars + static_cast<uint32_t>((w * N + st) * 8));
+      }
+    }
+    umma::fence_before_sync();
+    __syncwarp();
+    cluster_sync_all();
+    if (warp == W + 2) umma::tmem_dealloc(tmem, tmem_cols);
+    return;
+  }
 
   if (warp == W) {
     // ---- TMA producer warp: loads every compute warp's stages and issues
@@ -500,7 +654,43 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
         }
       }
     }
-    if (w < W && s_b > 0 && i0w < t_b) {
+    if (SRC == 1 && s_b > 0) {
+      const uint32_t zb = base + SL.zbars;
+      const uint32_t zfull = zb, zfree = zb + 8u * kGStages;
+      const uint32_t stage_bytes = static_cast<uint32_t>((a.Kp / umma::kAtomK) * umma::kAtomBytes);
+      int wl = 0;
+      for (int v = 0; v < W; ++v)
+        if (band + (crank * W + v) * kRows4 < t_b) wl = v + 1;
+      if (lane == 0 && wl > 0) {  // B stages of this item's frames
+        prefetch_tensormap(&tmq);
+        const uint64_t pol_b = policy_evict_last();  // the cluster's CTAs share them
+        for (int m = 0; m < nit; ++m) {
+          const int zs = m % kGStages;
+          if (m >= kGStages) mbar_wait(zfree + 8u * zs, (static_cast<uint32_t>(m / kGStages) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(zfull + 8u * zs, stage_bytes);
+          for (int at = 0; at < a.Kp / umma::kAtomK; ++at)
+            tma_load_2d(base + SL.zst + zs * stage_bytes + at * umma::kAtomBytes, &tmq,
+                        at * umma::kAtomK, b * a.Sp + m * umma::kN, zfull + 8u * zs, pol_b);
+        }
+      } else if (lane >= 2 && lane < 2 + W && a.zero_fill != 0) {  // zero fill of warp lane-2's rows
+        const int v = lane - 2;
+        const int i0v = band + (crank * W + v) * kRows4;
+        if (i0v < t_b) {
+          const int orow = b * a.T_cap + i0v;
+          for (int m = 0; m < nit; ++m) {
+            if (m % kZStages != 0) continue;
+            if (m >= N) {
+              const int st = m % N;
+              mbar_wait(base + SL.ebars + static_cast<uint32_t>((v * N + st) * 8),
+                        (static_cast<uint32_t>(m / N) & 1u) ^ 1u);
+            }
+            tma_store_2d(&tm_out, base + SL.zero, m * kSC, orow);
+          }
+          bulk_store_drain();
+        }
+      }
+    }
+    if (SRC == 0 && w < W && s_b > 0 && i0w < t_b) {
       prefetch_tensormap(&tmq);
 #ifndef MAS_Q_POLICY
 #define MAS_Q_POLICY policy_evict_unchanged  // measured: evict_first re-reads 8 % of q (r12)
@@ -734,16 +924,19 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
 
 }  // namespace
 
-size_t fwd4_smem_bytes(int R, int W, int N) { return smem4_layout(R, W, N).total + 1024u; }
+size_t fwd4_smem_bytes(int R, int W, int N, int Kp) {
+  return smem4_layout(R, W, N, Kp).total + 1024u;
+}
 
 namespace {
-template <int R, int MODE>
+template <int R, int MODE, int SRC>
 const void* fwd4_fn() {
-  return reinterpret_cast<const void*>(&mas_fwd4_kernel<R, MODE>);
+  return reinterpret_cast<const void*>(&mas_fwd4_kernel<R, MODE, SRC>);
 }
-const void* fwd4_fn(int R, int mode) {
+const void* fwd4_fn(int R, int mode, int src = 0) {
   (void)R;  // four rows per lane
-  return mode == 0 ? fwd4_fn<4, 0>() : fwd4_fn<4, 1>();
+  if (src) return mode == 0 ? fwd4_fn<4, 0, 1>() : fwd4_fn<4, 1, 1>();
+  return mode == 0 ? fwd4_fn<4, 0, 0>() : fwd4_fn<4, 1, 0>();
 }
 }  // namespace
 
@@ -758,8 +951,8 @@ cudaError_t fwd4_configure() {
   std::call_once(once[dev], [dev] {
     int smem_max = 0;
     cudaError_t r = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    for (int v = 0; v < 2 && r == cudaSuccess; ++v) {
-      const void* fn = fwd4_fn(4, v);
+    for (int v = 0; v < 4 && r == cudaSuccess; ++v) {
+      const void* fn = fwd4_fn(4, v & 1, v >> 1);
       r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
       if (r == cudaSuccess)
         r = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -769,11 +962,11 @@ cudaError_t fwd4_configure() {
   return status[dev];
 }
 
-int fwd4_max_active_clusters(int R, int W, int N, int K) {
+int fwd4_max_active_clusters(int R, int W, int N, int K, int Kp) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(K), 1, 1);
-  cfg.blockDim = dim3(static_cast<unsigned>((W + 1) * 32), 1, 1);
-  cfg.dynamicSmemBytes = fwd4_smem_bytes(R, W, N);
+  cfg.blockDim = dim3(static_cast<unsigned>((W + 1 + (Kp > 0 ? 5 : 0)) * 32), 1, 1);
+  cfg.dynamicSmemBytes = fwd4_smem_bytes(R, W, N, Kp);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(K);
@@ -782,7 +975,7 @@ int fwd4_max_active_clusters(int R, int W, int N, int K) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, fwd4_fn(R, 0), &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, fwd4_fn(R, 0, Kp > 0 ? 1 : 0), &cfg) != cudaSuccess) {
     cudaGetLastError();
     return -1;
   }
@@ -791,10 +984,12 @@ int fwd4_max_active_clusters(int R, int W, int N, int K) {
 
 cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorMap& tm_out,
                         const FwdArgs& a, int B, cudaStream_t stream) {
+  const bool gauss = a.Kp > 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(B * a.K), 1, 1);
-  cfg.blockDim = dim3(static_cast<unsigned>((a.W + 1) * 32), 1, 1);  // + the TMA producer warp
-  cfg.dynamicSmemBytes = fwd4_smem_bytes(R, a.W, a.N);
+  // + the producer warp (+ the MMA warp and four epilogue warps for the Gaussian source)
+  cfg.blockDim = dim3(static_cast<unsigned>((a.W + 1 + (gauss ? 5 : 0)) * 32), 1, 1);
+  cfg.dynamicSmemBytes = fwd4_smem_bytes(R, a.W, a.N, a.Kp);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -804,8 +999,11 @@ cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorM
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (R != 4) return cudaErrorInvalidValue;
-  return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0>, tmq, tm_out, a)
-                   : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 1>, tmq, tm_out, a);
+  if (gauss)
+    return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0, 1>, tmq, tm_out, a)
+                     : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 1, 1>, tmq, tm_out, a);
+  return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0, 0>, tmq, tm_out, a)
+                   : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 1, 0>, tmq, tm_out, a);
 }
 
 }  // namespace mas

@@ -72,6 +72,11 @@ struct FwdArgs {
   int* progress;
   int* ticket;
   int bnd_pitch;
+  // Gaussian source (Kp > 0): q computed in-kernel from mas_gauss.cu's operands
+  int Kp;                   // padded K (0: q read from HBM)
+  int Tp, Sp;               // padded rows / frames per item of the operands
+  const __nv_bfloat16* gA;  // [B][Tp][Kp]
+  const float* gbias;       // [B][Tp]
   uint32_t one;             // 1 and 0.0f passed at run time so ptxas keeps the
   float zero;               //   bit IMADs / NonFinite FFMAs on the FMA pipe
 };
@@ -106,9 +111,9 @@ cudaError_t launch_flag_nonfinite(const float* q, int64_t pitch, int rows_per_it
 int forward_scores_host_lengths(float* d_values, int64_t row_pitch, int32_t batch,
                                 int32_t rows_per_item, int32_t speech_cap, const uint32_t* lengths,
                                 float max_neg_val, cudaStream_t stream, mas_error_t* err);
-size_t fwd4_smem_bytes(int R, int W, int N);
+size_t fwd4_smem_bytes(int R, int W, int N, int Kp = 0);
 cudaError_t fwd4_configure();
-int fwd4_max_active_clusters(int R, int W, int N, int K);
+int fwd4_max_active_clusters(int R, int W, int N, int K, int Kp = 0);
 cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorMap& tm_out,
                         const FwdArgs& a, int B, cudaStream_t stream);
 

@@ -1,6 +1,7 @@
 // mas_ptx.cuh -- thin inline-PTX wrappers for sm_100a: mbarrier, TMA
 // (cp.async.bulk.tensor), cluster / DSMEM, release/acquire flags.
 #pragma once
+#include <cstdio>
 
 #include <cuda.h>
 #include <cstdint>
@@ -46,8 +47,24 @@ __device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifdef MAS_WATCHDOG
+// Debug builds: a wait that spins for seconds reports itself and traps.
+__device__ __forceinline__ void mbar_watchdog(uint32_t& n, uint32_t bar, uint32_t parity) {
+  if (++n == (1u << 22)) {
+    printf("WATCHDOG block %d thread %d bar %u parity %u\n", blockIdx.x, threadIdx.x, bar, parity);
+    __trap();
+  }
+}
+#define MAS_WD_DECL uint32_t wd_n = 0;
+#define MAS_WD(bar, parity) mbar_watchdog(wd_n, bar, parity);
+#else
+#define MAS_WD_DECL
+#define MAS_WD(bar, parity)
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  MAS_WD_DECL
   while (!mbar_try_wait(bar, parity)) {
+    MAS_WD(bar, parity)
   }
 }
 // Warp-uniform variants for warps that shuffle right after: every lane
@@ -59,7 +76,9 @@ __device__ __forceinline__ bool mbar_test_wait_all(uint32_t bar, uint32_t parity
   return __all_sync(0xffffffffu, mbar_test_wait(bar, parity));
 }
 __device__ __forceinline__ void mbar_wait_all(uint32_t bar, uint32_t parity) {
+  MAS_WD_DECL
   while (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
+    MAS_WD(bar, parity)
   }
 }
 #else

@@ -89,3 +89,81 @@ def test_gaussian_loglik_rejects_bad_inputs(mas, cuda):
     z2, m2, l2 = _inputs(1, 193, 6, 9, 0)
     with pytest.raises(RuntimeError):
         mas.gaussian_loglik(z2, m2, l2)
+
+
+def _unfused(mas, z, mean, logstd, lens, engine, want):
+    q = mas.gaussian_loglik(z, mean, logstd)
+    out = {}
+    if "alignment" in want:
+        out["alignment"] = mas.align(q, lengths=lens, engine=engine)
+    if "paths" in want:
+        ps = mas.align_paths(q, lengths=lens, engine=engine)
+        out["paths"] = ps
+    if "durations" in want:
+        out["durations"] = mas.align_durations(q, lengths=lens, engine=engine)
+    return q, out
+
+
+@pytest.mark.parametrize("engine", ["parallel", "reference"])
+@pytest.mark.parametrize("shape,ragged", [((2, 80, 200, 800), False), ((3, 80, 257, 1000), True),
+                                          ((1, 192, 1024, 2048), False), ((4, 16, 37, 111), True),
+                                          ((2, 80, 1024, 8192), False)])
+def test_fused_equals_unfused(mas, cuda, shape, ragged, engine):
+    """align_gaussian (q computed inside the forward kernel, never written)
+    == align(gaussian_loglik(...)) bit for bit: same MMAs, same bias add."""
+    import numpy as np
+    import torch
+
+    B, C, T, S = shape
+    z, mean, logstd = _inputs(B, C, T, S, seed=B * T + S)
+    lens = None
+    if ragged:
+        rng = np.random.default_rng(T)
+        t = rng.integers(1, T + 1, B)
+        t[0] = T
+        s = np.maximum(t, rng.integers(1, S + 1, B))
+        s[0] = S
+        lens = np.stack([t, s], 1)
+    want = ("alignment", "paths", "durations")
+    got = mas.align_gaussian(z, mean, logstd, lengths=lens, engine=engine, outputs=want)
+    q, exp = _unfused(mas, z, mean, logstd, lens, engine, want)
+    assert torch.equal(got["alignment"], exp["alignment"])
+    assert torch.equal(got["durations"], exp["durations"])
+    for b in range(B):
+        sb = S if lens is None else int(lens[b, 1])
+        gp = got["paths"][b, :sb].cpu()
+        ep = exp["paths"][b] if not hasattr(exp["paths"][b], "cpu") else exp["paths"][b].cpu()
+        assert torch.equal(gp, torch.as_tensor(ep)), b
+        assert bool((got["paths"][b, sb:] == -1).all())
+
+
+def test_fused_alignment_is_near_optimal_for_exact_q(mas, cuda):
+    """Against the exact (float64) log-likelihood the fused path -- optimal
+    for the bf16-operand q -- scores within the q error of the exact optimum
+    (the path sum of q errors bounds the loss), and mostly picks the same
+    frames."""
+    import numpy as np
+    import torch
+
+    B, C, T, S = 2, 80, 120, 500
+    z, mean, logstd = _inputs(B, C, T, S, seed=11)
+    got = mas.align_gaussian(z, mean, logstd, outputs=("paths",))["paths"].cpu().numpy()
+    qx = reference_q64(z, mean, logstd).cpu().numpy()             # exact q
+    qf = mas.gaussian_loglik(z, mean, logstd).double().cpu().numpy()
+    exact_paths = np.stack([np.asarray(p) for p in mas.align_paths(qx.astype(np.float32))])
+    cols = np.arange(S)
+    for b in range(B):
+        s_fused = qx[b, got[b], cols].sum()
+        s_exact = qx[b, exact_paths[b], cols].sum()
+        bound = np.abs(qf[b] - qx[b]).max() * 2 * S
+        assert s_exact - s_fused <= bound + 1e-6 * abs(s_exact), (b, s_exact - s_fused, bound)
+        assert (got[b] == exact_paths[b]).mean() > 0.5
+
+
+def test_fused_nonfinite_is_located(mas, cuda):
+    import torch
+
+    z, mean, logstd = _inputs(3, 8, 40, 90, 4)
+    z[1, 2, 17] = float("nan")  # column 17 of every row of item 1
+    with pytest.raises(ValueError, match=r"item 1: non-finite likelihood at \(0, 17\)"):
+        mas.align_gaussian(z, mean, logstd)
