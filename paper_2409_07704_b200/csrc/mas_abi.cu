@@ -204,7 +204,7 @@ bool choose_geometry(int B, int t_max, int S_cap, Geometry* g, int kp) {
       if (mas::fwd4_smem_bytes(g->R, W, N, kp) > budget) continue;
       // Gaussian source: A (Kp/2 columns per warp) and two 32-column
       // accumulators per warp in TMEM's 512 columns; one band only
-      if (kp > 0 && W * kp / 2 + 2 * W * 32 > 512) continue;
+      if (kp > 0 && (W > 2 || W * kp / 2 + W * 64 > 512)) continue;
       int last_K = -1;
       for (int nb = 1; nb <= (kp > 0 ? 1 : warps_total); ++nb) {
         const int per_band = (warps_total + nb - 1) / nb;
@@ -721,6 +721,10 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     fa.bnd_pitch = p->bnd_pitch;
     if (p->gauss) {
       fa.Kp = p->gauss->Kp;
+      const mas::GaussCfg gc = mas::gauss_cfg(g.W, fa.Kp);
+      fa.gstages = gc.gstages;
+      fa.gacc = gc.gacc;
+      fa.gN = gc.gN;
       fa.Tp = p->gauss->Tp;
       fa.Sp = p->gauss->Sp;
       fa.gA = p->gauss->A;
@@ -1345,7 +1349,9 @@ int mas_align_gaussian_device(const float* d_z, const float* d_mean, const float
   cudaError_t e = mas::gauss_alloc(batch, channels, text_cap, speech_cap, stream, &g, &ws);
   if (e == cudaSuccess)
     e = mas::gauss_prep(d_z, d_mean, d_logstd, batch, channels, text_cap, speech_cap, g, stream);
-  if (e == cudaSuccess && !mas::encode_gauss_b_map(g.B, static_cast<int64_t>(batch) * g.Sp, g.Kp, &tmb))
+  if (e == cudaSuccess &&
+      !mas::encode_gauss_b_map(g.B, static_cast<int64_t>(batch) * g.Sp, g.Kp, &tmb,
+                               mas::gauss_cfg(plan->geo.W, g.Kp).gN))
     e = cudaErrorInvalidValue;
   if (e == cudaSuccess) {
     plan->gauss = &g;

@@ -31,6 +31,7 @@
 // MAS_FWD_PROFILE prints per-warp clock64 breakdowns, MAS_FWD_TIMELINE per-CTA
 // globaltimer spans; MAS_ABL_{NOQLDS,NOSHFL,NOBITS,NOFOLD,NOPROBE} remove one
 // part of the per-column work (results are wrong) to price it.
+#include <algorithm>
 #include <cstdio>
 #include <mutex>
 
@@ -76,11 +77,13 @@ struct Smem4 {
   uint32_t zst, zbars, tslot;
 };
 
-// Gaussian source: B stages in flight, TMEM accumulator buffers.
-constexpr int kGStages = 3;
-constexpr int kGAcc = 2;
+// Gaussian source: at most this many B stages / TMEM accumulator buffers in
+// flight (the launch picks a.gstages / a.gacc within smem and TMEM).
+constexpr int kGStages = 4;
+constexpr int kGAcc = 4;
 
-__host__ __device__ inline Smem4 smem4_layout(int R, int W, int N, int Kp = 0) {
+__host__ __device__ inline Smem4 smem4_layout(int R, int W, int N, int Kp = 0, int gstages = 0,
+                                              int gN = 0) {
   Smem4 L;
   L.ring = 0;
   L.bars = static_cast<uint32_t>(W * N * stage_bytes(R));
@@ -100,7 +103,7 @@ __host__ __device__ inline Smem4 smem4_layout(int R, int W, int N, int Kp = 0) {
   if (Kp > 0) {
     // zfull[kGStages] zfree[kGStages] dfull[kGAcc] dempty[kGAcc] aready, then the slot
     L.zst = (L.total + 1023u) & ~1023u;
-    L.zbars = L.zst + static_cast<uint32_t>(kGStages * (Kp / umma::kAtomK) * umma::kAtomBytes);
+    L.zbars = L.zst + static_cast<uint32_t>(gstages * (Kp / umma::kAtomK) * gN * 128);
     L.tslot = (L.zbars + static_cast<uint32_t>((2 * kGStages + 2 * kGAcc + 1) * 8) + 15u) & ~15u;
     L.total = L.tslot + 16u;
   }
@@ -354,8 +357,22 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
 // and four epilogue warps (warps W+2..W+5, one per TMEM sub-partition) add
 // the row bias and write each 32-column tile into the compute warps' ring in
 // the layout TMA would have used.  The compute warps run unchanged.
+// Waits of the Gaussian source's helper warps, which share SM sub-partitions
+// with the compute warps: back off between probes instead of spinning.
+__device__ __forceinline__ void mbar_wait_idle(uint32_t bar, uint32_t parity) {
+#ifdef MAS_GAUSS_SLEEP
+  while (!mbar_try_wait(bar, parity)) __nanosleep(MAS_GAUSS_SLEEP);
+#else
+  mbar_wait(bar, parity);
+#endif
+}
+
 template <int R, int MODE, int SRC>
-__global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
+#ifdef MAS_DUMMY_WARPS
+__global__ void __launch_bounds__(12 * 32, 1)
+#else
+__global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
+#endif
     mas_fwd4_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tm_out,
                     const FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -366,7 +383,11 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   const int N = a.N;
   constexpr int kRows4 = rows_of(R);
   constexpr int kStage4 = stage_bytes(R);
-  const Smem4 SL = smem4_layout(R, W, N, SRC ? a.Kp : 0);
+  const Smem4 SL = smem4_layout(R, W, N, SRC ? a.Kp : 0, SRC ? a.gstages : 0, SRC ? a.gN : 0);
+  const int NB = a.gstages, NA = a.gacc;  // Gaussian source pipeline depths
+  const int GN = a.gN;                    // frames per MMA (64 or 128)
+  const int kGS = GN / umma::kStageN;     // K1 stages per MMA group
+  const uint32_t atom_bytes = static_cast<uint32_t>(GN * 128);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -437,14 +458,14 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   }
   uint32_t tmem = 0, tmem_cols = 0;
   if constexpr (SRC == 1) {
-    tmem_cols = umma::tmem_cols_pow2(static_cast<uint32_t>(W * a.Kp / 2 + kGAcc * W * umma::kN));
+    tmem_cols = umma::tmem_cols_pow2(static_cast<uint32_t>(W * a.Kp / 2 + NA * W * GN));
     if (warp == W + 2) {
       if (lane == 0) {
-        for (int k = 0; k < 2 * kGStages + 2 * kGAcc + 1; ++k) {
-          const bool dempty = k >= 2 * kGStages + kGAcc && k < 2 * kGStages + 2 * kGAcc;
-          const bool aready = k == 2 * kGStages + 2 * kGAcc;
-          mbar_init(base + SL.zbars + 8u * k, dempty || aready ? 4u : 1u);
-        }
+        // zfull / zfree: TMA + commit; dfull: commit; dempty, aready: every
+        // epilogue warp (4 per compute warp)
+        for (int k = 0; k < 2 * kGStages + 2 * kGAcc + 1; ++k)
+          mbar_init(base + SL.zbars + 8u * k,
+                    k >= 2 * kGStages + kGAcc ? static_cast<uint32_t>(4 * W) : 1u);
       }
       umma::tmem_alloc(base + SL.tslot, tmem_cols);
     }
@@ -463,36 +484,70 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     tmem = *reinterpret_cast<volatile uint32_t*>(sbase + SL.tslot);
   }
 
+#ifdef MAS_DUMMY_WARPS  // experiment: SRC 0 with 8 extra warps waiting like the epilogue
+  if (SRC == 0 && warp > W) {
+    const int w = (warp - W - 1) & 1;
+    if (s_b > 0 && band + (crank * W + w) * kRows4 < t_b)
+      for (int m = N; m < nit; ++m)
+        mbar_wait(base + SL.ebars + static_cast<uint32_t>((w * N + m % N) * 8),
+                  (static_cast<uint32_t>(m / N) & 1u) ^ 1u);
+    __syncwarp();
+    cluster_sync_all();
+    return;
+  }
+#endif
   if (SRC == 1 && warp == W + 1) {
     // ---- Gaussian source, MMA warp: waits converged, lane 0 issues --------
     const uint32_t zb = base + SL.zbars;
     const uint32_t zfull = zb, zfree = zb + 8u * kGStages;
     const uint32_t dfull = zb + 8u * (2 * kGStages), dempty = dfull + 8u * kGAcc;
     const uint32_t aready = dempty + 8u * kGAcc;
-    const uint32_t stage_bytes = static_cast<uint32_t>((a.Kp / umma::kAtomK) * umma::kAtomBytes);
+    const uint32_t stage_bytes = static_cast<uint32_t>(a.Kp / umma::kAtomK) * atom_bytes;
     int wl = 0;
     for (int v = 0; v < W; ++v)
       if (s_b > 0 && band + (crank * W + v) * kRows4 < t_b) wl = v + 1;
+#ifdef MAS_GAUSS_BARE
+    wl = 0;
+#endif
     if (wl > 0) {
-      const uint32_t idesc = umma::idesc_bf16_f32(umma::kM, umma::kN);
-      mbar_wait(aready, 0u);
+      const uint32_t idesc = umma::idesc_bf16_f32(umma::kM, GN);
+      mbar_wait_idle(aready, 0u);
       umma::fence_after_sync();
-      for (int m = 0; m < nit; ++m) {
-        const int zs = m % kGStages, d = m % kGAcc;
-        mbar_wait(zfull + 8u * zs, static_cast<uint32_t>(m / kGStages) & 1u);
-        if (m >= kGAcc) mbar_wait(dempty + 8u * d, (static_cast<uint32_t>(m / kGAcc) & 1u) ^ 1u);
+#ifdef MAS_GAUSS_PROFILE
+      long long gp_t0 = clock64(), gp_z = 0, gp_d = 0, gp_i = 0;
+#endif
+      const int ngr = (nit + kGS - 1) / kGS;  // MMA groups of kGS stages
+      for (int m = 0; m < ngr; ++m) {
+        const int zs = m % NB, d = m % NA;
+#ifdef MAS_GAUSS_PROFILE
+        long long gp_a = clock64();
+#endif
+        mbar_wait_idle(zfull + 8u * zs, static_cast<uint32_t>(m / NB) & 1u);
+#ifdef MAS_GAUSS_PROFILE
+        long long gp_b = clock64();
+        gp_z += gp_b - gp_a;
+#endif
+        if (m >= NA) mbar_wait_idle(dempty + 8u * d, (static_cast<uint32_t>(m / NA) & 1u) ^ 1u);
+#ifdef MAS_GAUSS_PROFILE
+        gp_d += clock64() - gp_b;
+#endif
         umma::fence_after_sync();
         __syncwarp();
         if (lane == 0) {
-          for (int v = 0; v < wl; ++v)
-            umma::mma_tile(tmem + static_cast<uint32_t>(W * a.Kp / 2 + (d * W + v) * umma::kN),
-                           tmem + static_cast<uint32_t>(v * a.Kp / 2),
-                           base + SL.zst + zs * stage_bytes, a.Kp, idesc);
+#ifndef MAS_GAUSS_NOMMA  // experiment: pipeline without tensor work (wrong results)
+          umma::mma_tiles(tmem + static_cast<uint32_t>(W * a.Kp / 2 + d * W * GN),
+                          static_cast<uint32_t>(GN), tmem, static_cast<uint32_t>(a.Kp / 2), wl,
+                          base + SL.zst + zs * stage_bytes, a.Kp, idesc, atom_bytes);
+#endif
           umma::mma_commit(zfree + 8u * zs);
           umma::mma_commit(dfull + 8u * d);
         }
         __syncwarp();
       }
+#ifdef MAS_GAUSS_PROFILE
+      if (lane == 0 && b == 0)
+        printf("MMA cta %d: total %lld zfull-wait %lld dempty-wait %lld\n", crank, clock64() - gp_t0, gp_z, gp_d);
+#endif
     }
     __syncwarp();
     cluster_sync_all();
@@ -500,73 +555,111 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
   }
 
   if (SRC == 1 && warp > W + 1) {
-    // ---- Gaussian source, epilogue warp of TMEM sub-partition qd ----------
+    // ---- Gaussian source, epilogue warp (TMEM sub-partition qd, tile w) ---
+    // Warps W+2 .. W+1+4W: tile w = (warp - W - 2) / 4, so each compute
+    // warp's tiles are written by its own four warps and the two compute
+    // warps' rings fill independently.
     const int qd = warp & 3;
+    const int w = (warp - W - 2) >> 2;
     const uint32_t zb = base + SL.zbars;
     const uint32_t dfull = zb + 8u * (2 * kGStages), dempty = dfull + 8u * kGAcc;
     const uint32_t aready = dempty + 8u * kGAcc;
     const uint32_t lane_base = static_cast<uint32_t>(32 * qd) << 16;
-#ifdef MAS_GAUSS_DEBUG
-    if (lane == 0)
-      printf("cta %d warp %d tmem %08x cols %u W %d N %d Kp %d Tp %d tslot %u base %u\n", blockIdx.x,
-             warp, tmem, tmem_cols, W, N, a.Kp, a.Tp, SL.tslot, base);
-#endif
-    int wl = 0;  // compute warps of this CTA with rows to align
-    for (int w = 0; w < W; ++w)
-      if (s_b > 0 && band + (crank * W + w) * kRows4 < t_b) wl = w + 1;
-    float bias[4];
-    for (int w = 0; w < W && w < 4; ++w) {
-      // rows i0w + 32 qd + lane: their A rows into TMEM, their bias into registers
-      const int row = band + (crank * W + w) * kRows4 + 32 * qd + lane;
+    // TMEM lane 32 qd + lane holds tile row 32 qd + 4 (lane & 7) + (lane >> 3):
+    // each 8-lane phase of a ring store then covers eight row groups (eight
+    // distinct swizzled 16-byte chunks): STS.128 without bank conflicts
+    // (the natural order put four residues of one group in a phase: 16
+    // wavefronts per store instead of 4, r12 ncu).
+    const int grp = 32 * qd + 4 * (lane & 7) + (lane >> 3);  // row within the warp's 128-row tile
+    const int row = band + (crank * W + w) * kRows4 + grp;
+    const bool live_w = s_b > 0 && band + (crank * W + w) * kRows4 < t_b;
+    float bias = 0.f;
+    if (live_w) {
+      // rows i0w + 32 qd + lane: their A rows into TMEM, their bias into a register
       const uint32_t* src = reinterpret_cast<const uint32_t*>(a.gA) +
                             (static_cast<int64_t>(b) * a.Tp + row) * (a.Kp / 2);
-      if (w < wl) {
-        for (int c = 0; c < a.Kp / 2; c += 8) {
-          uint32_t v[8];
+      for (int c = 0; c < a.Kp / 2; c += 8) {
+        uint32_t v[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] = __ldg(src + c + e);
-          umma::tmem_st8(tmem + lane_base + static_cast<uint32_t>(w * a.Kp / 2 + c), v);
-        }
-        bias[w] = __ldg(a.gbias + static_cast<int64_t>(b) * a.Tp + row);
+        for (int e = 0; e < 8; ++e) v[e] = __ldg(src + c + e);
+        umma::tmem_st8(tmem + lane_base + static_cast<uint32_t>(w * a.Kp / 2 + c), v);
       }
+      bias = __ldg(a.gbias + static_cast<int64_t>(b) * a.Tp + row);
+      umma::tmem_wait_st();
     }
-    umma::tmem_wait_st();
     umma::fence_before_sync();
     __syncwarp();
     if (lane == 0) mbar_arrive_local(aready);
-    const int grp = 32 * qd + lane;  // row within each warp's 128-row tile
     const uint32_t rbase = static_cast<uint32_t>((grp & 3) * 4096 + (grp >> 2) * 128);
     const uint32_t sw = static_cast<uint32_t>((grp >> 2) & 7);
-    for (int m = 0; m < (wl > 0 ? nit : 0); ++m) {
-      const int d = m % kGAcc;
-      mbar_wait(dfull + 8u * d, static_cast<uint32_t>(m / kGAcc) & 1u);
+    uint8_t* const ring_w = sbase + SL.ring + w * N * kStage4 + rbase;
+    int wl = 0;
+    for (int v = 0; v < W; ++v)
+      if (s_b > 0 && band + (crank * W + v) * kRows4 < t_b) wl = v + 1;
+#ifdef MAS_GAUSS_PROFILE
+    long long ge_t0 = clock64(), ge_e = 0, ge_d = 0;
+#endif
+    const int ngr = wl > 0 ? (nit + kGS - 1) / kGS : 0;
+    for (int gi = 0; gi < ngr; ++gi) {
+      const int d = gi % NA;
+#ifdef MAS_GAUSS_PROFILE
+      long long ge_b = clock64();
+#endif
+#ifndef MAS_GAUSS_BARE  // experiment: ring fed without the MMA pipeline (wrong results)
+      mbar_wait_idle(dfull + 8u * d, static_cast<uint32_t>(gi / NA) & 1u);
+#endif
       umma::fence_after_sync();
-      float v[4][32];
-#pragma unroll
-      for (int w = 0; w < 4; ++w)
-        if (w < wl)
-          umma::tmem_ld32(tmem + lane_base + static_cast<uint32_t>(W * a.Kp / 2 + (d * W + w) * umma::kN), v[w]);
-      umma::tmem_wait_ld();
-      umma::fence_before_sync();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_local(dempty + 8u * d);
-      const int st = m % N;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        if (w >= wl) continue;
+#ifdef MAS_GAUSS_PROFILE
+      ge_d += clock64() - ge_b;
+#endif
+      // 32-frame chunks: TMEM -> registers; the accumulator is released
+      // after the last chunk is read, each chunk written to its ring stage
+      for (int h = 0; h < kGS; ++h) {
+        const int m = gi * kGS + h;
+        float v[32];
+#ifdef MAS_GAUSS_NOEPI  // experiment: no TMEM read (wrong results)
+        if (false) {
+#else
+        if (live_w) {
+#endif
+          umma::tmem_ld32(tmem + lane_base +
+                              static_cast<uint32_t>(W * a.Kp / 2 + (d * W + w) * GN + h * umma::kStageN),
+                          v);
+          umma::tmem_wait_ld();
+        }
+        if (h == kGS - 1) {
+          umma::fence_before_sync();
+          __syncwarp();
+#ifndef MAS_GAUSS_BARE
+          if (lane == 0) mbar_arrive_local(dempty + 8u * d);
+#endif
+        }
+        if (!live_w || m >= nit) continue;
+        const int st = m % N;
+#ifdef MAS_GAUSS_PROFILE
+        long long ge_a = clock64();
+#endif
         if (m >= N)  // ring slot st of warp w consumed in iteration m - N
-          mbar_wait(base + SL.ebars + static_cast<uint32_t>((w * N + st) * 8),
-                    (static_cast<uint32_t>(m / N) & 1u) ^ 1u);
-        uint8_t* dst = sbase + SL.ring + (w * N + st) * kStage4 + rbase;
+          mbar_wait_idle(base + SL.ebars + static_cast<uint32_t>((w * N + st) * 8),
+                         (static_cast<uint32_t>(m / N) & 1u) ^ 1u);
+#ifdef MAS_GAUSS_PROFILE
+        ge_e += clock64() - ge_a;
+#endif
+        uint8_t* dst = ring_w + st * kStage4;
 #pragma unroll
         for (int c4 = 0; c4 < 8; ++c4)
           *reinterpret_cast<float4*>(dst + ((c4 ^ sw) << 4)) =
-              make_float4(v[w][4 * c4] + bias[w], v[w][4 * c4 + 1] + bias[w],
-                          v[w][4 * c4 + 2] + bias[w], v[w][4 * c4 + 3] + bias[w]);
+              make_float4(v[4 * c4] + bias, v[4 * c4 + 1] + bias, v[4 * c4 + 2] + bias,
+                          v[4 * c4 + 3] + bias);
         __syncwarp();
         if (lane == 0) mbar_arrive_local(base + SL.bars + static_cast<uint32_t>((w * N + st) * 8));
       }
     }
+#ifdef MAS_GAUSS_PROFILE
+    if (lane == 0 && b == 0)
+      printf("EPI cta %d tile %d qd %d: total %lld ebar-wait %lld dfull-wait %lld\n", crank, w, qd,
+             clock64() - ge_t0, ge_e, ge_d);
+#endif
     umma::fence_before_sync();
     __syncwarp();
     cluster_sync_all();
@@ -657,20 +750,24 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
     if (SRC == 1 && s_b > 0) {
       const uint32_t zb = base + SL.zbars;
       const uint32_t zfull = zb, zfree = zb + 8u * kGStages;
-      const uint32_t stage_bytes = static_cast<uint32_t>((a.Kp / umma::kAtomK) * umma::kAtomBytes);
+      const uint32_t stage_bytes = static_cast<uint32_t>(a.Kp / umma::kAtomK) * atom_bytes;
       int wl = 0;
       for (int v = 0; v < W; ++v)
         if (band + (crank * W + v) * kRows4 < t_b) wl = v + 1;
+#ifdef MAS_GAUSS_BARE
+      wl = 0;
+#endif
       if (lane == 0 && wl > 0) {  // B stages of this item's frames
         prefetch_tensormap(&tmq);
         const uint64_t pol_b = policy_evict_last();  // the cluster's CTAs share them
-        for (int m = 0; m < nit; ++m) {
-          const int zs = m % kGStages;
-          if (m >= kGStages) mbar_wait(zfree + 8u * zs, (static_cast<uint32_t>(m / kGStages) & 1u) ^ 1u);
+        const int ngr = (nit + kGS - 1) / kGS;
+        for (int m = 0; m < ngr; ++m) {
+          const int zs = m % NB;
+          if (m >= NB) mbar_wait(zfree + 8u * zs, (static_cast<uint32_t>(m / NB) & 1u) ^ 1u);
           mbar_arrive_expect_tx(zfull + 8u * zs, stage_bytes);
           for (int at = 0; at < a.Kp / umma::kAtomK; ++at)
-            tma_load_2d(base + SL.zst + zs * stage_bytes + at * umma::kAtomBytes, &tmq,
-                        at * umma::kAtomK, b * a.Sp + m * umma::kN, zfull + 8u * zs, pol_b);
+            tma_load_2d(base + SL.zst + zs * stage_bytes + at * atom_bytes, &tmq,
+                        at * umma::kAtomK, b * a.Sp + m * GN, zfull + 8u * zs, pol_b);
         }
       } else if (lane >= 2 && lane < 2 + W && a.zero_fill != 0) {  // zero fill of warp lane-2's rows
         const int v = lane - 2;
@@ -924,8 +1021,28 @@ __global__ void __launch_bounds__((kMaxWarpsPerCta + 1) * 32, 1)
 
 }  // namespace
 
+// Gaussian source pipeline for W tiles of Kp: 128-frame MMAs (half the MMA
+// issues of 64-frame ones; r12) when A, one 128-column accumulator per tile
+// and one B stage fit TMEM / shared memory, else 64-frame MMAs with more
+// buffers.
+GaussCfg gauss_cfg(int W, int Kp) {
+  GaussCfg c{0, 0, 0};
+  if (Kp <= 0 || W < 1) return c;
+  const int a_cols = W * Kp / 2;
+  if (a_cols + W * 128 <= 512 && Kp <= 192) {
+    c.gN = 128;
+    c.gacc = std::min(2, (512 - a_cols) / (W * 128));
+    c.gstages = 1;
+  } else {
+    c.gN = 64;
+    c.gacc = std::min(kGAcc, (512 - a_cols) / (W * 64));
+    c.gstages = Kp <= 192 ? 2 : 1;
+  }
+  return c;
+}
 size_t fwd4_smem_bytes(int R, int W, int N, int Kp) {
-  return smem4_layout(R, W, N, Kp).total + 1024u;
+  const GaussCfg c = gauss_cfg(W, Kp);
+  return smem4_layout(R, W, N, Kp, c.gstages, c.gN).total + 1024u;
 }
 
 namespace {
@@ -965,7 +1082,7 @@ cudaError_t fwd4_configure() {
 int fwd4_max_active_clusters(int R, int W, int N, int K, int Kp) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(K), 1, 1);
-  cfg.blockDim = dim3(static_cast<unsigned>((W + 1 + (Kp > 0 ? 5 : 0)) * 32), 1, 1);
+  cfg.blockDim = dim3(static_cast<unsigned>((W + 1 + (Kp > 0 ? 1 + 4 * W : 0)) * 32), 1, 1);
   cfg.dynamicSmemBytes = fwd4_smem_bytes(R, W, N, Kp);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -988,7 +1105,11 @@ cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorM
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(B * a.K), 1, 1);
   // + the producer warp (+ the MMA warp and four epilogue warps for the Gaussian source)
-  cfg.blockDim = dim3(static_cast<unsigned>((a.W + 1 + (gauss ? 5 : 0)) * 32), 1, 1);
+#ifdef MAS_DUMMY_WARPS
+  cfg.blockDim = dim3(static_cast<unsigned>((a.W + 1 + (gauss ? 1 + 4 * a.W : 8)) * 32), 1, 1);
+#else
+  cfg.blockDim = dim3(static_cast<unsigned>((a.W + 1 + (gauss ? 1 + 4 * a.W : 0)) * 32), 1, 1);
+#endif
   cfg.dynamicSmemBytes = fwd4_smem_bytes(R, a.W, a.N, a.Kp);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

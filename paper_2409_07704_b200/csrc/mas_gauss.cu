@@ -42,50 +42,83 @@ namespace mas {
 namespace {
 
 // ---- K4a: operands -----------------------------------------------------------
-// One thread per (item, row) for A / bias (the C channels of a text row are
-// strided by T in mean / logstd: consecutive threads read consecutive rows),
-// one thread per (item, frame) for B (likewise for z).
-__global__ void gauss_prep_rows_kernel(const float* __restrict__ mean,
-                                       const float* __restrict__ logstd, int B, int C, int T,
-                                       int Tp, int Kp, __nv_bfloat16* __restrict__ A,
-                                       float* __restrict__ bias) {
-  const int64_t n = static_cast<int64_t>(B) * Tp;
-  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
-       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int b = static_cast<int>(k / Tp), i = static_cast<int>(k % Tp);
-    __nv_bfloat16* a = A + k * Kp;
-    float acc = 0.f;
-    for (int c = 0; c < C; ++c) {
-      float lo = 0.f, hi = 0.f;
-      if (i < T) {
-        const int64_t x = (static_cast<int64_t>(b) * C + c) * T + i;
-        const float ls = logstd[x], m = mean[x];
-        const float inv_var = expf(-2.f * ls);
-        lo = -0.5f * inv_var;
-        hi = m * inv_var;
-        acc += -0.91893853320467274f - ls - 0.5f * m * m * inv_var;  // -0.5 log(2 pi)
-      }
-      a[c] = __float2bfloat16_rn(lo);
-      a[C + c] = __float2bfloat16_rn(hi);
+// A block stages 32 text rows (or frames) of every channel in shared memory
+// (reads coalesced along the row / frame index of mean, logstd, z) and then
+// writes the 32 K-major rows of Kp bf16 as consecutive 32-bit pairs
+// (coalesced: the 32 rows are one contiguous 32 x Kp block).
+constexpr int kPrepRows = 32;
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&p);
+}
+
+__global__ void __launch_bounds__(256) gauss_prep_rows_kernel(
+    const float* __restrict__ mean, const float* __restrict__ logstd, int B, int C, int T, int Tp,
+    int Kp, __nv_bfloat16* __restrict__ A, float* __restrict__ bias) {
+  extern __shared__ float sm[];  // [kPrepRows][2C + 1]: -0.5 e^{-2ls}, m e^{-2ls}
+  __shared__ float sbias[8][kPrepRows];
+  const int ld = 2 * C + 1;  // odd row stride: conflict-free in both phases
+  const int blocks_per_item = Tp / kPrepRows;
+  const int b = blockIdx.x / blocks_per_item, i0 = blockIdx.x % blocks_per_item * kPrepRows;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float acc = 0.f;
+  for (int c = wid; c < C; c += 8) {
+    const int i = i0 + lane;
+    float lo = 0.f, hi = 0.f;
+    if (i < T) {
+      const int64_t x = (static_cast<int64_t>(b) * C + c) * T + i;
+      const float ls = logstd[x], m = mean[x];
+      const float inv_var = expf(-2.f * ls);
+      lo = -0.5f * inv_var;
+      hi = m * inv_var;
+      acc += -0.91893853320467274f - ls - 0.5f * m * m * inv_var;  // -0.5 log(2 pi)
     }
-    for (int c = 2 * C; c < Kp; ++c) a[c] = __float2bfloat16_rn(0.f);
-    bias[k] = acc;
+    sm[lane * ld + c] = lo;
+    sm[lane * ld + C + c] = hi;
+  }
+  sbias[wid][lane] = acc;
+  __syncthreads();
+  if (threadIdx.x < kPrepRows) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += sbias[w][threadIdx.x];
+    bias[static_cast<int64_t>(b) * Tp + i0 + threadIdx.x] = t;
+  }
+  const int words = kPrepRows * Kp / 2;
+  uint32_t* out = reinterpret_cast<uint32_t*>(A + (static_cast<int64_t>(b) * Tp + i0) * Kp);
+  for (int L = threadIdx.x; L < words; L += blockDim.x) {
+    const int r = L / (Kp / 2), k = 2 * (L % (Kp / 2));
+    const float v0 = k < 2 * C ? sm[r * ld + k] : 0.f;
+    const float v1 = k + 1 < 2 * C ? sm[r * ld + k + 1] : 0.f;
+    out[L] = pack_bf16x2(v0, v1);
   }
 }
 
-__global__ void gauss_prep_frames_kernel(const float* __restrict__ z, int B, int C, int S, int Sp,
-                                         int Kp, __nv_bfloat16* __restrict__ Bm) {
-  const int64_t n = static_cast<int64_t>(B) * Sp;
-  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
-       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int b = static_cast<int>(k / Sp), j = static_cast<int>(k % Sp);
-    __nv_bfloat16* o = Bm + k * Kp;
-    for (int c = 0; c < C; ++c) {
-      const float v = j < S ? z[(static_cast<int64_t>(b) * C + c) * S + j] : 0.f;
-      o[c] = __float2bfloat16_rn(v * v);
-      o[C + c] = __float2bfloat16_rn(v);
+__global__ void __launch_bounds__(256) gauss_prep_frames_kernel(const float* __restrict__ z, int B,
+                                                                 int C, int S, int Sp, int Kp,
+                                                                 __nv_bfloat16* __restrict__ Bm) {
+  extern __shared__ float sm[];  // [kPrepRows][C + 1] z
+  const int ld = C + 1;
+  const int blocks_per_item = Sp / kPrepRows;
+  const int b = blockIdx.x / blocks_per_item, j0 = blockIdx.x % blocks_per_item * kPrepRows;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c = wid; c < C; c += 8) {
+    const int j = j0 + lane;
+    sm[lane * ld + c] = j < S ? z[(static_cast<int64_t>(b) * C + c) * S + j] : 0.f;
+  }
+  __syncthreads();
+  const int words = kPrepRows * Kp / 2;
+  uint32_t* out = reinterpret_cast<uint32_t*>(Bm + (static_cast<int64_t>(b) * Sp + j0) * Kp);
+  for (int L = threadIdx.x; L < words; L += blockDim.x) {
+    const int r = L / (Kp / 2), k = 2 * (L % (Kp / 2));
+    float v[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int kk = k + e;
+      const float x = kk < 2 * C ? sm[r * ld + (kk < C ? kk : kk - C)] : 0.f;
+      v[e] = kk < C ? x * x : x;  // z^2 rows first, then z
     }
-    for (int c = 2 * C; c < Kp; ++c) o[c] = __float2bfloat16_rn(0.f);
+    out[L] = pack_bf16x2(v[0], v[1]);
   }
 }
 
@@ -103,8 +136,24 @@ struct QArgs {
   int tmem_cols;
 };
 
+// Epilogue staging per warp: two [32 rows][32 frames] fp32 tiles (128-byte
+// swizzle), each written out by one TMA store {32, 32, 1} of the 3-D q map
+// {S, T, B} (clipped per item at T and S).
+constexpr uint32_t kQStage = 32 * 32 * 4;
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1,
+                                             int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(kQThreads, 1)
-    gauss_q_kernel(const __grid_constant__ CUtensorMap tmb, const QArgs a) {
+    gauss_q_kernel(const __grid_constant__ CUtensorMap tmb, const __grid_constant__ CUtensorMap tmq,
+                   const QArgs a) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment for the swizzled B atoms
   const uint32_t raw = smem_addr(smem_raw);
@@ -117,6 +166,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
   const uint32_t zfull = bars, zfree = bars + 8u * kQStages;
   const uint32_t dfull = zfree + 8u * kQStages, dempty = dfull + 16u;
   volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(sbase + kQStages * stage_bytes + 8 * (2 * kQStages + 4));
+  const uint32_t qstage = base + kQStages * stage_bytes + 1024;  // [4 warps][2][kQStage]
 
   const int tiles_t = a.Tp / umma::kM;
   const int cblocks = (a.Sp + kQColsPerCta - 1) / kQColsPerCta;
@@ -188,28 +238,48 @@ __global__ void __launch_bounds__(kQThreads, 1)
         umma::mma_commit(dfull + 8u * d);
       }
     }
-  } else {  // ---- epilogue: TMEM -> +bias -> q
+  } else {  // ---- epilogue: TMEM -> +bias -> swizzled smem tile -> TMA store
     const int qd = warp & 3;
     const int i = tr * umma::kM + 32 * qd + lane;
     const float bi = a.bias[static_cast<int64_t>(b) * a.Tp + i];
-    float* qrow = a.q + (static_cast<int64_t>(b) * a.T + i) * a.pitch;
+    const uint32_t my_stage = qstage + static_cast<uint32_t>(qd) * 2 * kQStage;
+    uint8_t* const my_stage_p = sbase + (my_stage - base);
+    int buf = 0;
+    if (lane == 0) prefetch_tensormap(&tmq);
     for (int m = 0; m < nst; ++m) {
       const int d = m & 1;
       mbar_wait(dfull + 8u * d, (m / 2) & 1u);
       umma::fence_after_sync();
-      float v[32];
-      umma::tmem_ld32(tmem + (static_cast<uint32_t>(32 * qd) << 16) + colD + static_cast<uint32_t>(d * umma::kN), v);
+      float v[2][32];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        umma::tmem_ld32(tmem + (static_cast<uint32_t>(32 * qd) << 16) + colD +
+                            static_cast<uint32_t>(d * umma::kN + h * umma::kStageN),
+                        v[h]);
       umma::tmem_wait_ld();
       umma::fence_before_sync();
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(dempty + 8u * d) : "memory");
       const int j0 = c0 + m * umma::kN;
-      if (i < a.T) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
-          if (j0 + e < a.S) qrow[j0 + e] = v[e] + bi;
+      for (int h = 0; h < 2; ++h, buf ^= 1) {
+        // the buffer's previous store (two tiles ago) has been read
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        uint8_t* t = my_stage_p + buf * kQStage + lane * 128;
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4)
+          *reinterpret_cast<float4*>(t + ((c4 ^ (lane & 7)) << 4)) =
+              make_float4(v[h][4 * c4] + bi, v[h][4 * c4 + 1] + bi, v[h][4 * c4 + 2] + bi,
+                          v[h][4 * c4 + 3] + bi);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0)
+          tma_store_3d(&tmq, my_stage + buf * kQStage, j0 + 32 * h, tr * umma::kM + 32 * qd, b);
       }
     }
+    if (lane == 0) bulk_store_drain();
+    __syncwarp();
   }
   umma::fence_before_sync();
   __syncthreads();
@@ -217,8 +287,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
 }
 
 size_t q_smem_bytes(int Kp) {
-  return 1024 + static_cast<size_t>(kQStages) * (Kp / umma::kAtomK) * umma::kAtomBytes +
-         8 * (2 * kQStages + 4) + 16;
+  return 1024 + static_cast<size_t>(kQStages) * (Kp / umma::kAtomK) * umma::kAtomBytes + 1024 +
+         4 * 2 * kQStage;
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -250,7 +320,7 @@ cudaError_t gauss_alloc(int B, int C, int T, int S, cudaStream_t stream, GaussOp
                         void** ws) {
   g->Kp = gauss_kp(C);
   g->Tp = (T + umma::kM - 1) / umma::kM * umma::kM;
-  g->Sp = (S + umma::kN - 1) / umma::kN * umma::kN;
+  g->Sp = (S + 127) / 128 * 128;  // whole 64- and 128-frame MMA groups
   const size_t a_bytes = static_cast<size_t>(B) * g->Tp * g->Kp * 2;
   const size_t b_bytes = static_cast<size_t>(B) * g->Sp * g->Kp * 2;
   const size_t bias_bytes = static_cast<size_t>(B) * g->Tp * 4;
@@ -266,12 +336,12 @@ cudaError_t gauss_alloc(int B, int C, int T, int S, cudaStream_t stream, GaussOp
 
 int gauss_kp(int C) { return ((2 * C + umma::kAtomK - 1) / umma::kAtomK) * umma::kAtomK; }
 
-bool encode_gauss_b_map(const void* Bm, int64_t rows, int Kp, CUtensorMap* m) {
+bool encode_gauss_b_map(const void* Bm, int64_t rows, int Kp, CUtensorMap* m, int box_rows) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(Kp) * 2};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(umma::kAtomK), static_cast<cuuint32_t>(umma::kN)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(umma::kAtomK), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(Bm), dims, strides, box,
              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -280,19 +350,62 @@ bool encode_gauss_b_map(const void* Bm, int64_t rows, int Kp, CUtensorMap* m) {
 
 cudaError_t gauss_prep(const float* z, const float* mean, const float* logstd, int B, int C, int T,
                        int S, const GaussOperands& g, cudaStream_t stream) {
-  const int sms = sm_count();
-  const int64_t nr = static_cast<int64_t>(B) * g.Tp, nf = static_cast<int64_t>(B) * g.Sp;
-  gauss_prep_rows_kernel<<<static_cast<unsigned>(std::min<int64_t>((nr + 127) / 128, sms * 8)), 128, 0,
-                           stream>>>(mean, logstd, B, C, T, g.Tp, g.Kp, g.A, g.bias);
-  gauss_prep_frames_kernel<<<static_cast<unsigned>(std::min<int64_t>((nf + 127) / 128, sms * 8)), 128, 0,
-                             stream>>>(z, B, C, S, g.Sp, g.Kp, g.B);
+  constexpr int kMaxDevices = 64;
+  static std::once_flag once[kMaxDevices];
+  static cudaError_t status[kMaxDevices];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || dev >= kMaxDevices) return e != cudaSuccess ? e : cudaErrorInvalidDevice;
+  std::call_once(once[dev], [dev] {
+    const int max_bytes = (2 * kGaussMaxChannels + 1) * kPrepRows * 4;
+    cudaError_t r = cudaFuncSetAttribute(gauss_prep_rows_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(gauss_prep_frames_kernel,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
+    status[dev] = r;
+  });
+  if (status[dev] != cudaSuccess) return status[dev];
+  gauss_prep_rows_kernel<<<static_cast<unsigned>(B * (g.Tp / kPrepRows)), 256,
+                           static_cast<size_t>(2 * C + 1) * kPrepRows * 4, stream>>>(
+      mean, logstd, B, C, T, g.Tp, g.Kp, g.A, g.bias);
+  gauss_prep_frames_kernel<<<static_cast<unsigned>(B * (g.Sp / kPrepRows)), 256,
+                             static_cast<size_t>(C + 1) * kPrepRows * 4, stream>>>(z, B, C, S, g.Sp,
+                                                                                 g.Kp, g.B);
   return cudaGetLastError();
 }
 
 cudaError_t gauss_q(const GaussOperands& g, int B, int T, int S, float* q, int64_t pitch,
                     cudaStream_t stream) {
-  CUtensorMap tmb;
+  if ((pitch % 4) != 0 || (reinterpret_cast<uintptr_t>(q) & 15u) != 0) {
+    // the TMA store needs 16-byte rows: compute into an aligned scratch copy
+    const int64_t p4 = (static_cast<int64_t>(S) + 3) & ~int64_t(3);
+    float* tmp = nullptr;
+    cudaError_t e = pool_alloc(reinterpret_cast<void**>(&tmp),
+                               static_cast<size_t>(B) * T * p4 * sizeof(float), stream);
+    if (e == cudaSuccess) e = gauss_q(g, B, T, S, tmp, p4, stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(q, pitch * sizeof(float), tmp, p4 * sizeof(float), S * sizeof(float),
+                            static_cast<size_t>(B) * T, cudaMemcpyDeviceToDevice, stream);
+    if (tmp) cudaFreeAsync(tmp, stream);
+    return e;
+  }
+  CUtensorMap tmb, tmq;
   if (!encode_gauss_b_map(g.B, static_cast<int64_t>(B) * g.Sp, g.Kp, &tmb)) return cudaErrorInvalidValue;
+  {
+    EncodeTiledFn enc = encode_fn();
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(T),
+                                static_cast<cuuint64_t>(B)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch) * 4,
+                                   static_cast<cuuint64_t>(pitch) * 4 * T};
+    const cuuint32_t box[3] = {32, 32, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    if (!enc || (pitch * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(q) & 15u) != 0 ||
+        enc(&tmq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, q, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
   const size_t smem = q_smem_bytes(g.Kp);
   constexpr int kMaxDevices = 64;
   static std::once_flag once[kMaxDevices];
@@ -318,7 +431,7 @@ cudaError_t gauss_q(const GaussOperands& g, int B, int T, int S, float* q, int64
   qa.Kp = g.Kp;
   qa.tmem_cols = static_cast<int>(umma::tmem_cols_pow2(static_cast<uint32_t>(g.Kp / 2 + 2 * umma::kN)));
   const int tiles = g.Tp / umma::kM, cblocks = (g.Sp + kQColsPerCta - 1) / kQColsPerCta;
-  gauss_q_kernel<<<static_cast<unsigned>(B * tiles * cblocks), kQThreads, smem, stream>>>(tmb, qa);
+  gauss_q_kernel<<<static_cast<unsigned>(B * tiles * cblocks), kQThreads, smem, stream>>>(tmb, tmq, qa);
   return cudaGetLastError();
 }
 

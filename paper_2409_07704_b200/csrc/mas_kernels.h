@@ -42,7 +42,7 @@ cudaError_t gauss_prep(const float* z, const float* mean, const float* logstd, i
                        int S, const GaussOperands& g, cudaStream_t stream);
 cudaError_t gauss_q(const GaussOperands& g, int B, int T, int S, float* q, int64_t pitch,
                     cudaStream_t stream);
-bool encode_gauss_b_map(const void* Bm, int64_t rows, int Kp, CUtensorMap* m);
+bool encode_gauss_b_map(const void* Bm, int64_t rows, int Kp, CUtensorMap* m, int box_rows = 64);
 
 struct FwdArgs {
   int b0;                   // first item of this launch (items b0 .. b0 + grid/K - 1)
@@ -74,6 +74,7 @@ struct FwdArgs {
   int bnd_pitch;
   // Gaussian source (Kp > 0): q computed in-kernel from mas_gauss.cu's operands
   int Kp;                   // padded K (0: q read from HBM)
+  int gstages, gacc, gN;    // B stages / TMEM accumulators in flight, frames per MMA (gauss_cfg)
   int Tp, Sp;               // padded rows / frames per item of the operands
   const __nv_bfloat16* gA;  // [B][Tp][Kp]
   const float* gbias;       // [B][Tp]
@@ -112,6 +113,10 @@ int forward_scores_host_lengths(float* d_values, int64_t row_pitch, int32_t batc
                                 int32_t rows_per_item, int32_t speech_cap, const uint32_t* lengths,
                                 float max_neg_val, cudaStream_t stream, mas_error_t* err);
 size_t fwd4_smem_bytes(int R, int W, int N, int Kp = 0);
+struct GaussCfg {
+  int gN, gstages, gacc;
+};
+GaussCfg gauss_cfg(int W, int Kp);
 cudaError_t fwd4_configure();
 int fwd4_max_active_clusters(int R, int W, int N, int K, int Kp = 0);
 cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorMap& tm_out,

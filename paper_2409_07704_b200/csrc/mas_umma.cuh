@@ -5,11 +5,13 @@
 // the instruction descriptor of a BF16 x BF16 -> FP32 MMA, the MMA with its
 // A operand in TMEM, and the commit to an mbarrier.  sm_100a only.
 //
-// Operand shapes used here: D[128 rows x 32 columns] fp32 in TMEM (lane =
+// Operand shapes used here: D[128 rows x 64 columns] fp32 in TMEM (lane =
 // row, column = speech frame), A[128 rows x K] bf16 in TMEM (lane = row, two
 // bf16 per 32-bit column, element k in column k/2, even k in the low half),
-// B[K x 32 columns] bf16 in shared memory, K-major (each column's K values
-// contiguous) in 64-element (128-byte) swizzle atoms of 32 rows.
+// B[K x 64 columns] bf16 in shared memory, K-major (each column's K values
+// contiguous) in 64-element (128-byte) swizzle atoms of 64 rows.  (N = 32
+// measured 2x slower on the issue side: ~120 cycles per tcgen05.mma
+// regardless of N at these sizes, r12.)
 #pragma once
 
 #include <cstdint>
@@ -18,10 +20,11 @@ namespace mas {
 namespace umma {
 
 constexpr int kM = 128;         // rows per MMA (TMEM lanes)
-constexpr int kN = 32;          // columns per MMA (one K1 stage)
+constexpr int kN = 64;          // columns (frames) per MMA: two K1 stages
+constexpr int kStageN = 32;     // columns per K1 stage / TMEM load
 constexpr int kKStep = 16;      // K per kind::f16 MMA
 constexpr int kAtomK = 64;      // bf16 elements per 128-byte swizzle row
-constexpr int kAtomBytes = kN * 128;  // one B atom: 32 columns x 128 bytes
+constexpr int kAtomBytes = kN * 128;  // one B atom: 64 columns x 128 bytes
 
 // ---- instruction descriptor (kind::f16): BF16 A/B, FP32 D, both K-major ----
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
@@ -116,14 +119,31 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
                : "memory");
 }
 
-// D[128 x 32] = A[128 x Kp] . B[Kp x 32] for one tile: Kp / 16 MMAs, the
-// B stage being Kp / 64 atoms of 32 columns x 128 bytes at `b_smem`.
+// D[128 x 64] = A[128 x Kp] . B[Kp x 64] for one tile: Kp / 16 MMAs, the
+// B stage being Kp / 64 atoms of 64 columns x 128 bytes at `b_smem`.
+// (mma_tiles interleaves the K steps of several tiles: consecutive MMAs then
+// accumulate into different TMEM tiles instead of waiting on each other.)
 __device__ __forceinline__ void mma_tile(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_smem, int Kp,
                                          uint32_t idesc) {
   for (int ks = 0; ks < Kp / kKStep; ++ks) {
     const uint32_t b_addr = b_smem + static_cast<uint32_t>((ks / 4) * kAtomBytes + (ks % 4) * 32);
     mma_ts(d_tmem, a_tmem + static_cast<uint32_t>(ks * (kKStep / 2)), sdesc_kmajor_sw128(b_addr),
            idesc, ks > 0);
+  }
+}
+
+// `ntiles` tiles sharing B: D_t = A_t . B, tile t's D at d_tmem + t * d_step
+// and A at a_tmem + t * a_step (TMEM columns), K steps interleaved.
+__device__ __forceinline__ void mma_tiles(uint32_t d_tmem, uint32_t d_step, uint32_t a_tmem,
+                                          uint32_t a_step, int ntiles, uint32_t b_smem, int Kp,
+                                          uint32_t idesc, uint32_t atom_bytes = kAtomBytes) {
+  for (int ks = 0; ks < Kp / kKStep; ++ks) {
+    const uint64_t bd =
+        sdesc_kmajor_sw128(b_smem + static_cast<uint32_t>(ks / 4) * atom_bytes + (ks % 4) * 32);
+    for (int t = 0; t < ntiles; ++t)
+      mma_ts(d_tmem + static_cast<uint32_t>(t) * d_step,
+             a_tmem + static_cast<uint32_t>(t) * a_step + static_cast<uint32_t>(ks * (kKStep / 2)),
+             bd, idesc, ks > 0);
   }
 }
 
