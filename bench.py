@@ -81,6 +81,14 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def _bf16_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"])
+    except Exception:
+        return 2250.0  # B200 dense bf16 nominal
+
+
 def _ncu_traffic():
     """dram bytes per launch of the forward kernel from the committed
     `ncu --set full` summary (profiles/ncu_fwd_latest.json), if present."""
@@ -387,6 +395,61 @@ def run_ours(args):
                    "ms_per_step": round(sc_best, 4), "bytes_per_cell": 8,
                    "path": "forward_parallel(torch CUDA tensor): the parallel engine's score "
                            "table written in place (forward_scores_kernel)"}
+    # ---- fused log-likelihood + MAS: q from the
+    # Glow-TTS prior (C = 80 channels) computed on tcgen05 inside K1, never
+    # written; against the unfused pipeline (gaussian_loglik writes q, then
+    # the plan aligns it).  Same batch shape as the step, on this rank.
+    gauss_line = None
+    try:
+        C = 80
+        gz = torch.Generator(device="cpu").manual_seed(1)
+        zz = torch.randn(B, C, S, generator=gz).to(dev)
+        mu = (torch.randn(B, C, T, generator=gz) * 0.8).to(dev)
+        lsd = ((torch.rand(B, C, T, generator=gz) - 0.5) * 0.6).to(dev)
+
+        def unfused_call():
+            qg = mas.gaussian_loglik(zz, mu, lsd)
+            plan.enqueue(qg, out, stream=torch.cuda.current_stream(dev))
+
+        def fused_call():
+            return mas.align_gaussian(zz, mu, lsd)
+
+        fused_out = fused_call()["alignment"]
+        unfused_call()
+        torch.cuda.synchronize(dev)
+        assert torch.equal(fused_out, out), "fused != unfused alignment"
+        del fused_out
+
+        def ev_ms(fn, n=5):
+            fn()
+            torch.cuda.synchronize(dev)
+            ts = []
+            for _ in range(n):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                torch.cuda.synchronize(dev)
+                ts.append(e0.elapsed_time(e1))
+            return statistics.median(ts)
+
+        f_ms, u_ms = ev_ms(fused_call), ev_ms(unfused_call)
+        kp = ((2 * C + 63) // 64) * 64
+        gauss_line = {
+            "value": round(total_cells / (f_ms / 1e3) / 1e9, 2), "unit": "Gcells/s",
+            "ms_per_step": round(f_ms, 4), "unfused_ms_per_step": round(u_ms, 4),
+            "speedup_vs_unfused": round(u_ms / f_ms, 3), "channels": C,
+            "bytes_per_cell": 1.125,
+            "tensor": {"achieved_tflops": round(2 * kp * cells / (f_ms / 1e3) / 1e12, 1),
+                       "flops_per_cell": 2 * kp, "peak_tflops": _bf16_peak(),
+                       "frac": round(2 * kp * cells / (f_ms / 1e3) / 1e12 / _bf16_peak(), 4)},
+            "path": "align_gaussian(z, mean, logstd): operand prep + K1 computing q tiles with "
+                    "tcgen05 (bf16 operands, fp32 accumulation) into the DP ring + K2; vs "
+                    "gaussian_loglik (q to HBM) + plan.enqueue",
+        }
+        del zz, mu, lsd
+    except Exception as e:  # reported, not fatal for the headline line
+        gauss_line = {"error": str(e)[:200]}
     durations_line = {
         "value": round(total_cells / (dur_ms / 1e3) / 1e9, 2), "unit": "Gcells/s",
         "ms_per_step": round(dur_ms, 4), "bytes_per_cell": 4.125,
@@ -442,7 +505,7 @@ def run_ours(args):
                 "path": "mas_align_host (C-ABI), pinned host in/out, H2D+kernels+D2H+checks"},
         "gpu_launches": K * launches_per_step,
         "variants": {"durations_only": durations_line, "numpy_e2e": numpy_line,
-                     "score_export": scores_line},
+                     "score_export": scores_line, "gaussian_fused": gauss_line},
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
     }
