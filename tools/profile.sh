@@ -12,3 +12,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:mas_
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:bt_walk -s 2 -c 1 \
   -o $O/prof_bt_$TAG -f python tools/prof_run.py 32 1024 8192 4 > $O/ncu_bt_$TAG.log 2>&1
 ls -la $O | grep $TAG
+# K1g (fused log-likelihood) full capture
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:mas_fwd4 -s 1 -c 1 \
+  -o $O/prof_fwdg_$TAG -f python tools/gauss_k1.py 80 > $O/ncu_fwdg_$TAG.log 2>&1
+bash tools/l2_sequence.sh $TAG
