@@ -266,10 +266,9 @@ bool cached_geometry(int B, int t_max, int S_cap, Geometry* g, int kp = 0) {
 // The input [B*T_pad][pitch] as a 3-D tensor {columns, row groups of R,
 // row residue mod R}: one {32, 32, R} box is a 32R-row x 32-column stage of
 // mas_fwd4.cu laid out [residue][group][column] (128-byte swizzle).
-#ifndef MAS_Q_L2PROMO
-#define MAS_Q_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-#endif
-constexpr CUtensorMapL2promotion kQPromotion = MAS_Q_L2PROMO;
+// 256-byte promotion: each 128-byte row segment also brings the row's next
+// stage into L2 (K1 15 us faster than without; r12, profiles/r12_l2_policy.md)
+constexpr CUtensorMapL2promotion kQPromotion = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
 
 bool encode_map4(const float* q, int64_t pitch, int64_t rows_total, int64_t S, int R,
                  CUtensorMap* m) {
@@ -531,11 +530,7 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
   if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_dirs),
                            nB * g.M * g.T_alloc * sizeof(uint32_t), st)) != cudaSuccess)
     return fail(e, "mas::pool_alloc(dirs)");
-  static const int bt_rows_cap = [] {
-    const char* e = std::getenv("MAS_BT_ROWS");  // experiment override
-    return e ? std::max(16, std::min(256, std::atoi(e))) & ~15 : 256;
-  }();
-  p->bt_rows = std::min(bt_rows_cap, g.T_alloc);
+  p->bt_rows = std::min(256, g.T_alloc);  // backtrack window rows
   if (g.bands > 1) {
     p->bnd_pitch = (speech_cap + 31) & ~31;
     if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_bnd),
@@ -667,11 +662,7 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     // B256 T512 S4096: 527 us fused vs 380 + ~80 us).  Estimate: the chains
     // take S x ~50 cycles per warp (x warps per SM sub-partition beyond
     // one), the stream cells x 4.125 B at ~5.9 TB/s.  Ragged batches always
-    // take the memset.  MAS_FUSED_ZERO=0/1 forces either.
-    static const int fuse_env = [] {
-      const char* e = std::getenv("MAS_FUSED_ZERO");
-      return e ? std::atoi(e) : -1;
-    }();
+    // take the memset.
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
     const double warps = static_cast<double>(nb) * g.bands * g.K * g.W;
@@ -684,7 +675,7 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     // TMA clips past the end).  Chunked host calls run other chunks
     // concurrently, so they fuse only row-aligned items.
     const bool rows_own = (p->T % (32 * g.R)) == 0 || (b0 == 0 && nb == p->B);
-    const bool fused_zero = d_out && (fuse_env >= 0 ? fuse_env == 1 : chain_bound) &&
+    const bool fused_zero = d_out && chain_bound &&
                             p->all_full && rows_own && (p->S % 16) == 0 &&
                             (reinterpret_cast<uintptr_t>(d_out) & 15u) == 0;
     const size_t item_bytes = static_cast<size_t>(p->T) * p->S;
@@ -704,12 +695,7 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
       p->tm_out_ptr = d_out;
     }
     fa.zero_fill = fused_zero ? 1 : 0;
-    static const int l2_ahead = [] {
-      const char* e = std::getenv("MAS_L2_AHEAD");  // experiment override
-      return e ? std::max(0, std::atoi(e)) : -1;
-    }();
-    // L2 prefetch lead (stages beyond the smem ring) when the ring is short.
-    fa.l2_ahead = l2_ahead >= 0 ? l2_ahead : 0;  // measured: L2 prefetch only hurts
+    fa.l2_ahead = 0;  // measured: an L2 prefetch lead beyond the ring only hurts
     fa.one = 1u;
     fa.zero = 0.0f;
     fa.T_cap = p->T;
@@ -1124,13 +1110,9 @@ int align_host_impl(const float* values, int32_t batch, int32_t text_cap, int32_
   // item each: the finer the chunks, the shorter the un-overlapped head
   // (first H2D) and tail (last compute + D2H).  B32 T1024 S8192: 32 chunks,
   // 13.1 Gcells/s vs 12.2 with 4 (PCIe-bound either way).
-  static const int chunk_env = [] {
-    const char* e = std::getenv("MAS_HOST_CHUNKS");  // experiment override
-    return e ? std::max(1, std::atoi(e)) : 0;
-  }();
   const int64_t in_bytes = static_cast<int64_t>(batch) * text_cap * speech_cap * 4;
   const int by_size = static_cast<int>(std::max<int64_t>(1, in_bytes / (8ll << 20)));
-  const int nchunk = std::min(batch, chunk_env > 0 ? chunk_env : std::min(by_size, 64));
+  const int nchunk = std::min(batch, std::min(by_size, 64));
   const int per = (batch + nchunk - 1) / nchunk;
   // Pageable input / output: stage through pinned slots (two each).
   const size_t in_chunk = static_cast<size_t>(per) * o_item * sizeof(float);

@@ -29,12 +29,6 @@ namespace mas {
 
 namespace {
 
-#ifndef MAS_BT_WORDS
-#define MAS_BT_WORDS 8
-#endif
-constexpr int kBtWords = MAS_BT_WORDS;          // direction words per stage (32 columns each)
-constexpr int kBtStages = 32 / MAS_BT_WORDS;    // ring depth (stages of direction words in flight)
-constexpr int kBtCols = 32 * kBtWords;          // speech positions per stage
 constexpr int kBtMaxRows = 256;  // rows per window (TMA box limit)
 
 // Window load of stage n: words [8n, 8n + 8) (those < M) of rows
@@ -144,9 +138,7 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
   __syncthreads();
   // Everything below reads the forward kernel's direction bits or writes
   // after its zero fill (programmatic dependent launch).
-#ifndef MAS_BT_NO_PDL
   asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
   // Durations (row sums of the alignment): the buffer first holds each
   // row's last column (-1 = before column 0), written by the expander at the
   // walk's exits, and is turned into differences at the end.
@@ -173,15 +165,7 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
     // allowed (bit-reversed) bits of the item's last word: positions <= P
     uint32_t lim = 0xffffffffu << (31 - ((s - 1) & 31));
     uint32_t ph_full = 0, ph_free = 0, pend = 0;
-#ifdef MAS_BT_PROFILE
-    long long pr_t0 = clock64(), pr_free = 0, pr_full = 0, pr_recenter = 0, pr_words = 0;
-    long long pr_inner = 0;
-    __shared__ unsigned pr_ts[300];
-    __shared__ unsigned char pr_ex[300];
-#define PR_T(v) long long v = clock64()
-#else
 #define PR_T(v)
-#endif
     for (int k = 0; k < kBtStages && n_top - k >= 0; ++k) {
       const int n = n_top - k, slot = n & (kBtStages - 1);
       s_ylo[slot] = bt_row0(y, R, T_alloc);
@@ -195,9 +179,6 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
         PR_T(a0);
         mbar_wait(free_s + 8u * slot, (ph_free >> slot) & 1u);
         ph_free ^= 1u << slot;
-#ifdef MAS_BT_PROFILE
-        pr_free += clock64() - a0;
-#endif
       }
       int ml = Mg - kBtWords * n;  // first word of this stage to walk
       for (int k = kBtWords - 1; k > ml; --k) {  // above the item's last column
@@ -210,16 +191,10 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
           mbar_wait(full_s + 8u * slot, (ph_full >> slot) & 1u);
           ph_full ^= 1u << slot;
           pend &= ~(1u << slot);
-#ifdef MAS_BT_PROFILE
-          pr_full += clock64() - a1;
-#endif
         }
         const uint32_t slot_base = win_s + slot * kSlotBytes;
         int ylo = s_ylo[slot];
         auto recenter = [&]() {
-#ifdef MAS_BT_PROFILE
-          ++pr_recenter;
-#endif
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           ylo = bt_row0(y, R, T_alloc);
           s_ylo[slot] = ylo;
@@ -264,9 +239,6 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
     (Q) = ld64(pb - (OFF), PAIR);              \
   }
           // (the common paired case runs with unconditional loads)
-#ifdef MAS_BT_PROFILE
-          const long long pr_in0 = clock64();
-#endif
           if (pair) {
             while (true) {
               MAS_BT_STEP(q1, 20u, true) MAS_BT_STEP(q2, 24u, true) MAS_BT_STEP(q3, 28u, true)
@@ -283,9 +255,6 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
             }
           }
 #undef MAS_BT_STEP
-#ifdef MAS_BT_PROFILE
-          pr_inner += clock64() - pr_in0;
-#endif
           exw |= x;  // a pending exit at the pair's position 0
           const int ex_lo = __popc(static_cast<uint32_t>(exw));
           const int ex = ex_lo + __popc(static_cast<uint32_t>(exw >> 32));
@@ -309,10 +278,6 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
             rec_ex[slot][ml - 1] = static_cast<uint32_t>(exw >> 32);
             rec_y[slot][ml - 1] = y - ex_lo;
           }
-#ifdef MAS_BT_PROFILE
-          if (pr_words < 300) { pr_ts[pr_words] = static_cast<unsigned>(clock64() - pr_t0); pr_ex[pr_words] = static_cast<unsigned char>(ex); }
-          ++pr_words;
-#endif
           y = y_n;
           ml = ml_n;
           if (!more) break;
@@ -341,15 +306,6 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
     }
     for (int k = 0; k < kBtStages; ++k)  // no copy may still be writing our smem
       if (pend & (1u << k)) mbar_wait(full_s + 8u * k, (ph_full >> k) & 1u);
-#ifdef MAS_BT_PROFILE
-    if (b < 2) {
-      printf("bt item %d: total %lld cyc, wait free %lld, wait full %lld, recenters %lld, words %lld, inner %lld\n",
-             b, clock64() - pr_t0, pr_free, pr_full, pr_recenter, pr_words, pr_inner);
-      if (b == 0)
-        for (int i = 1; i < 300 && i < pr_words; ++i)
-          printf("word %d t=%u dt=%u ex=%d\n", i, pr_ts[i], pr_ts[i] - pr_ts[i - 1], pr_ex[i]);
-    }
-#endif
     return;
   }
 
@@ -485,18 +441,10 @@ cudaError_t launch_backtrack(const BtArgs& a, cudaStream_t stream, int* launches
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-#ifdef MAS_BT_NO_PDL
-  cfg.numAttrs = 0;
-#else
   cfg.numAttrs = 1;
-#endif
   if (launches) *launches = 1;
   // shallow paths (at most one text row per four speech frames): wider stages
-  static const int words_env = [] {
-    const char* e = std::getenv("MAS_BT_WORDS");  // A/B override: 8 or 16
-    return e ? std::atoi(e) : 0;
-  }();
-  const bool wide = words_env ? words_env == 16 : 4 * a.T_cap <= a.S_cap;
+  const bool wide = 4 * a.T_cap <= a.S_cap;
   return wide ? cudaLaunchKernelEx(&cfg, bt_walk_kernel<16>, a)
               : cudaLaunchKernelEx(&cfg, bt_walk_kernel<8>, a);
 }

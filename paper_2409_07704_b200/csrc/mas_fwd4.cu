@@ -27,10 +27,8 @@
 //     3-input FMNMX per two values); the output's zero fill rides along as
 //     TMA stores of a zero tile.
 //
-// Measurement builds (never the default; DESIGN.md 3 quotes their results):
-// MAS_FWD_PROFILE prints per-warp clock64 breakdowns, MAS_FWD_TIMELINE per-CTA
-// globaltimer spans; MAS_ABL_{NOQLDS,NOSHFL,NOBITS,NOFOLD,NOPROBE} remove one
-// part of the per-column work (results are wrong) to price it.
+// (DESIGN.md 3 quotes per-warp clock64 breakdowns and ablations measured with
+// instrumented builds of earlier revisions; the product source carries none.)
 #include <algorithm>
 #include <cstdio>
 #include <mutex>
@@ -46,27 +44,18 @@ namespace {
 // R = text rows per lane (4 or 2): a warp owns 32 R rows; a stage is one
 // [R residues][32 groups][32 cols] fp32 box (R * 4 KiB).
 constexpr int kCols4 = 32;  // columns per TMA box / direction word ("chunk")
-#ifndef MAS_STAGE_COLS
-#define MAS_STAGE_COLS 32
-#endif
-constexpr int kSC = MAS_STAGE_COLS;     // columns per stage (32 or 64)
+constexpr int kSC = 32;     // columns per stage (32 or 64)
 constexpr int kChunks = kSC / kCols4;   // chunks (direction words per row) per stage
 // The output's fused zero fill: one TMA store of a {kZCols, 32 R} uint8
 // zero box every kZCols / 32 stages (128-byte row segments: whole L2 lines,
 // a quarter of the scattered 32-byte writes a per-stage box would make).
 constexpr int kZCols = kZeroCols;
 constexpr int kZStages = kZCols / kSC;
-#ifndef MAS_BAND_PUB
-#define MAS_BAND_PUB 4
-#endif
-constexpr int kBandPub = MAS_BAND_PUB;  // quads per band-progress publication
+constexpr int kBandPub = 4;  // quads per band-progress publication
 __host__ __device__ constexpr int rows_of(int R) { return 32 * R; }
 __host__ __device__ constexpr int chunk_bytes(int R) { return rows_of(R) * kCols4 * 4; }
 __host__ __device__ constexpr int stage_bytes(int R) { return chunk_bytes(R) * kChunks; }
-#ifndef MAS_QUAD4
-#define MAS_QUAD4 32
-#endif
-constexpr int kQuad = MAS_QUAD4;            // columns per FIFO hand-off (16 or 32)
+constexpr int kQuad = 32;           // columns per FIFO hand-off (16 or 32)
 constexpr int kSlot4 = kQuad * 4;           // FIFO slot bytes
 constexpr int kQuadsPerStage = kSC / kQuad;
 constexpr int kFifoIt4 = kFifoSlots / kQuadsPerStage;  // FIFO depth in stages
@@ -173,14 +162,9 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
                                           bool row0_is_zero) {
   if (GENERIC && U0 >= nvalid) return false;
   float4 qv[R];
-#ifndef MAS_ABL_NOQLDS
 #pragma unroll
   for (int r = 0; r < R; ++r)
     qv[r] = *reinterpret_cast<const float4*>(tile + r * 4096 + coff);
-#else
-#pragma unroll
-  for (int r = 0; r < R; ++r) qv[r] = make_float4(mnv * 1e-36f, 1.f, 2.f, 3.f);
-#endif
   const float4 vv = slot[(U0 % kQuad) / 4];  // producer's bottom row
   const float bnds[4] = {L.vlast, vv.x, vv.y, vv.z};
 #pragma unroll
@@ -190,12 +174,7 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
 #pragma unroll
     for (int r = 0; r < R; ++r) q[r] = e == 0 ? qv[r].x : e == 1 ? qv[r].y : e == 2 ? qv[r].z : qv[r].w;
     const float send = is31 ? bnds[e] : L.o[R - 1];
-#ifndef MAS_ABL_NOSHFL
     const float up = __shfl_sync(0xffffffffu, send, srclane);
-#else
-    const float up = send;
-#endif
-#ifndef MAS_ABL_NOBITS
     switch ((U0 + e) % 16) {  // compile-time bit 15 - column-in-half-word
 #define MAS_B4(U)                   \
   case U:                           \
@@ -205,7 +184,6 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
       MAS_B4(8) MAS_B4(9) MAS_B4(10) MAS_B4(11) MAS_B4(12) MAS_B4(13) MAS_B4(14) MAS_B4(15)
 #undef MAS_B4
     }
-#endif
     float n[R];
     n[0] = q[0] + fmaxf(up, L.o[0]);
 #pragma unroll
@@ -223,16 +201,8 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
         for (int r = 1; r < R; ++r) n[r] = mnv;
       }
     }
-#ifndef MAS_ABL_NOFOLD
-#ifndef MAS_FOLD_FFMA
 #pragma unroll
     for (int r = 0; r + 1 < R; r += 2) fold_abs_max_nan(L.acc[r / 2], q[r], q[r + 1]);
-#else
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-      asm("fma.rn.f32 %0, %1, 0f00000000, %0;" : "+f"(L.acc[r / 2]) : "f"(q[r]));
-#endif
-#endif
     ex[(U0 % kQuad) + e] = n[R - 1];
 #pragma unroll
     for (int r = 0; r < R; ++r) L.o[r] = n[r];
@@ -266,18 +236,12 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
   const int q1 = q + 1;
   const uint32_t bar1 = F.full + 8u * (q1 & (kFifoSlots - 1));
   if (lane == 0 && next && F.has_in) mbar_arrive_expect_tx(bar1, kSlot4);
-#ifndef MAS_ABL_NOPROBE
   const bool probe = mbar_test_wait_all(bar1, static_cast<uint32_t>(q1 / kFifoSlots) & 1u);
-#else
-  const bool probe = false;  // ablation: always the blocking wait
-#endif
   bool p_stage = false, p_empty = false;
   if (K == 0) {
     if (P.arm_empty && is31) mbar_arrive_expect_tx(P.empty_bar, 4u);
-#ifndef MAS_ABL_NOPROBE
     p_stage = mbar_test_wait_all(P.stage_bar, P.stage_par);
     p_empty = mbar_test_wait_all(P.empty_bar, P.empty_par);
-#endif
   }
   const float4* slot = reinterpret_cast<const float4*>(F.buf + fs * kSlot4);
   bool ok = true;
@@ -357,22 +321,8 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
 // and four epilogue warps (warps W+2..W+5, one per TMEM sub-partition) add
 // the row bias and write each 32-column tile into the compute warps' ring in
 // the layout TMA would have used.  The compute warps run unchanged.
-// Waits of the Gaussian source's helper warps, which share SM sub-partitions
-// with the compute warps: back off between probes instead of spinning.
-__device__ __forceinline__ void mbar_wait_idle(uint32_t bar, uint32_t parity) {
-#ifdef MAS_GAUSS_SLEEP
-  while (!mbar_try_wait(bar, parity)) __nanosleep(MAS_GAUSS_SLEEP);
-#else
-  mbar_wait(bar, parity);
-#endif
-}
-
 template <int R, int MODE, int SRC>
-#ifdef MAS_DUMMY_WARPS
-__global__ void __launch_bounds__(12 * 32, 1)
-#else
 __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
-#endif
     mas_fwd4_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tm_out,
                     const FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -410,12 +360,6 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
   const int t_b = static_cast<int>(a.lengths[2 * b]);
   const int s_b = static_cast<int>(a.lengths[2 * b + 1]);
   const int nit = (s_b + kSC - 1) / kSC;
-#ifdef MAS_FWD_TIMELINE
-  unsigned long long tl_start;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_start));
-  unsigned tl_smid;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(tl_smid));
-#endif
 
   const int band = band_idx * a.band_rows;  // first text row of this cluster
   const bool fed = band_idx > 0;              // band's first warp fed from the band above
@@ -484,18 +428,6 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     tmem = *reinterpret_cast<volatile uint32_t*>(sbase + SL.tslot);
   }
 
-#ifdef MAS_DUMMY_WARPS  // experiment: SRC 0 with 8 extra warps waiting like the epilogue
-  if (SRC == 0 && warp > W) {
-    const int w = (warp - W - 1) & 1;
-    if (s_b > 0 && band + (crank * W + w) * kRows4 < t_b)
-      for (int m = N; m < nit; ++m)
-        mbar_wait(base + SL.ebars + static_cast<uint32_t>((w * N + m % N) * 8),
-                  (static_cast<uint32_t>(m / N) & 1u) ^ 1u);
-    __syncwarp();
-    cluster_sync_all();
-    return;
-  }
-#endif
   if (SRC == 1 && warp == W + 1) {
     // ---- Gaussian source, MMA warp: waits converged, lane 0 issues --------
     const uint32_t zb = base + SL.zbars;
@@ -506,48 +438,26 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     int wl = 0;
     for (int v = 0; v < W; ++v)
       if (s_b > 0 && band + (crank * W + v) * kRows4 < t_b) wl = v + 1;
-#ifdef MAS_GAUSS_BARE
-    wl = 0;
-#endif
     if (wl > 0) {
       const uint32_t idesc = umma::idesc_bf16_f32(umma::kM, GN);
-      mbar_wait_idle(aready, 0u);
+      mbar_wait(aready, 0u);
       umma::fence_after_sync();
-#ifdef MAS_GAUSS_PROFILE
-      long long gp_t0 = clock64(), gp_z = 0, gp_d = 0, gp_i = 0;
-#endif
       const int ngr = (nit + kGS - 1) / kGS;  // MMA groups of kGS stages
       for (int m = 0; m < ngr; ++m) {
         const int zs = m % NB, d = m % NA;
-#ifdef MAS_GAUSS_PROFILE
-        long long gp_a = clock64();
-#endif
-        mbar_wait_idle(zfull + 8u * zs, static_cast<uint32_t>(m / NB) & 1u);
-#ifdef MAS_GAUSS_PROFILE
-        long long gp_b = clock64();
-        gp_z += gp_b - gp_a;
-#endif
-        if (m >= NA) mbar_wait_idle(dempty + 8u * d, (static_cast<uint32_t>(m / NA) & 1u) ^ 1u);
-#ifdef MAS_GAUSS_PROFILE
-        gp_d += clock64() - gp_b;
-#endif
+        mbar_wait(zfull + 8u * zs, static_cast<uint32_t>(m / NB) & 1u);
+        if (m >= NA) mbar_wait(dempty + 8u * d, (static_cast<uint32_t>(m / NA) & 1u) ^ 1u);
         umma::fence_after_sync();
         __syncwarp();
         if (lane == 0) {
-#ifndef MAS_GAUSS_NOMMA  // experiment: pipeline without tensor work (wrong results)
           umma::mma_tiles(tmem + static_cast<uint32_t>(W * a.Kp / 2 + d * W * GN),
                           static_cast<uint32_t>(GN), tmem, static_cast<uint32_t>(a.Kp / 2), wl,
                           base + SL.zst + zs * stage_bytes, a.Kp, idesc, atom_bytes);
-#endif
           umma::mma_commit(zfree + 8u * zs);
           umma::mma_commit(dfull + 8u * d);
         }
         __syncwarp();
       }
-#ifdef MAS_GAUSS_PROFILE
-      if (lane == 0 && b == 0)
-        printf("MMA cta %d: total %lld zfull-wait %lld dempty-wait %lld\n", crank, clock64() - gp_t0, gp_z, gp_d);
-#endif
     }
     __syncwarp();
     cluster_sync_all();
@@ -596,32 +506,17 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     int wl = 0;
     for (int v = 0; v < W; ++v)
       if (s_b > 0 && band + (crank * W + v) * kRows4 < t_b) wl = v + 1;
-#ifdef MAS_GAUSS_PROFILE
-    long long ge_t0 = clock64(), ge_e = 0, ge_d = 0;
-#endif
     const int ngr = wl > 0 ? (nit + kGS - 1) / kGS : 0;
     for (int gi = 0; gi < ngr; ++gi) {
       const int d = gi % NA;
-#ifdef MAS_GAUSS_PROFILE
-      long long ge_b = clock64();
-#endif
-#ifndef MAS_GAUSS_BARE  // experiment: ring fed without the MMA pipeline (wrong results)
-      mbar_wait_idle(dfull + 8u * d, static_cast<uint32_t>(gi / NA) & 1u);
-#endif
+      mbar_wait(dfull + 8u * d, static_cast<uint32_t>(gi / NA) & 1u);
       umma::fence_after_sync();
-#ifdef MAS_GAUSS_PROFILE
-      ge_d += clock64() - ge_b;
-#endif
       // 32-frame chunks: TMEM -> registers; the accumulator is released
       // after the last chunk is read, each chunk written to its ring stage
       for (int h = 0; h < kGS; ++h) {
         const int m = gi * kGS + h;
         float v[32];
-#ifdef MAS_GAUSS_NOEPI  // experiment: no TMEM read (wrong results)
-        if (false) {
-#else
         if (live_w) {
-#endif
           umma::tmem_ld32(tmem + lane_base +
                               static_cast<uint32_t>(W * a.Kp / 2 + (d * W + w) * GN + h * umma::kStageN),
                           v);
@@ -630,21 +525,13 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
         if (h == kGS - 1) {
           umma::fence_before_sync();
           __syncwarp();
-#ifndef MAS_GAUSS_BARE
           if (lane == 0) mbar_arrive_local(dempty + 8u * d);
-#endif
         }
         if (!live_w || m >= nit) continue;
         const int st = m % N;
-#ifdef MAS_GAUSS_PROFILE
-        long long ge_a = clock64();
-#endif
         if (m >= N)  // ring slot st of warp w consumed in iteration m - N
-          mbar_wait_idle(base + SL.ebars + static_cast<uint32_t>((w * N + st) * 8),
+          mbar_wait(base + SL.ebars + static_cast<uint32_t>((w * N + st) * 8),
                          (static_cast<uint32_t>(m / N) & 1u) ^ 1u);
-#ifdef MAS_GAUSS_PROFILE
-        ge_e += clock64() - ge_a;
-#endif
         uint8_t* dst = ring_w + st * kStage4;
 #pragma unroll
         for (int c4 = 0; c4 < 8; ++c4)
@@ -655,11 +542,6 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
         if (lane == 0) mbar_arrive_local(base + SL.bars + static_cast<uint32_t>((w * N + st) * 8));
       }
     }
-#ifdef MAS_GAUSS_PROFILE
-    if (lane == 0 && b == 0)
-      printf("EPI cta %d tile %d qd %d: total %lld ebar-wait %lld dfull-wait %lld\n", crank, w, qd,
-             clock64() - ge_t0, ge_e, ge_d);
-#endif
     umma::fence_before_sync();
     __syncwarp();
     cluster_sync_all();
@@ -754,9 +636,6 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
       int wl = 0;
       for (int v = 0; v < W; ++v)
         if (band + (crank * W + v) * kRows4 < t_b) wl = v + 1;
-#ifdef MAS_GAUSS_BARE
-      wl = 0;
-#endif
       if (lane == 0 && wl > 0) {  // B stages of this item's frames
         prefetch_tensormap(&tmq);
         const uint64_t pol_b = policy_evict_last();  // the cluster's CTAs share them
@@ -789,10 +668,8 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     }
     if (SRC == 0 && w < W && s_b > 0 && i0w < t_b) {
       prefetch_tensormap(&tmq);
-#ifndef MAS_Q_POLICY
-#define MAS_Q_POLICY policy_evict_unchanged  // measured: evict_first re-reads 8 % of q (r12)
-#endif
-      const uint64_t pol_q = MAS_Q_POLICY();
+      // evict_unchanged: evict_first re-read 8 % of q (r12, profiles/r12_l2_policy.md)
+      const uint64_t pol_q = policy_evict_unchanged();
       const bool zero_fill = a.zero_fill != 0;
       const uint32_t zero_tile = base + SL.zero;
       const int group = (b * a.T_pad + i0w) / R;
@@ -892,9 +769,6 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     // Look-ahead results of the previous iteration's probes (see Probes).
     bool stage_ready = false;
     bool empty_ready = true;
-#ifdef MAS_FWD_PROFILE
-    long long pf_t0 = clock64(), pf_stage = 0, pf_empty = 0, pf_comp = 0, pf_rest = 0;
-#endif
 
     auto store_words = [&](uint32_t* p, const uint32_t (&v)[R]) {
       if constexpr (R == 4)
@@ -907,14 +781,7 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     int slot = 0;
     uint32_t par = 0;
     for (int m = 0; m < nit; ++m) {
-#ifdef MAS_FWD_PROFILE
-      long long pf_a = clock64();
-#endif
       if (!stage_ready) mbar_wait_all(bar0 + 8u * slot, par);
-#ifdef MAS_FWD_PROFILE
-      long long pf_b = clock64();
-      pf_stage += pf_b - pf_a;
-#endif
       const uint8_t* stage = ring_ptr + slot * kStage4;
       const int c_base = m * kSC;
       const int nvalid = s_b - c_base < kSC ? s_b - c_base : kSC;
@@ -944,10 +811,6 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
         P.stage_ok = false;
         P.empty_ok = false;
       }
-#ifdef MAS_FWD_PROFILE
-      long long pf_c = clock64();
-      pf_empty += pf_c - pf_b;
-#endif
       if (generic) {
         fwd4_stage<R, MODE, true>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
                                kQuadsPerStage * m, c_base, nvalid, row0, mnv, row0_is_zero,
@@ -959,10 +822,6 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
       }
       stage_ready = P.stage_ok;
       empty_ready = P.empty_ok || !P.arm_empty;
-#ifdef MAS_FWD_PROFILE
-      long long pf_d = clock64();
-      pf_comp += pf_d - pf_c;
-#endif
       // Every value of this stage and of this iteration's FIFO slots has been
       // consumed: hand the stage back to the producer warp and release the
       // slots to the warp above.
@@ -988,15 +847,7 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
       dirs_ptr += kChunks * a.T_alloc;
       slot = slot + 1 == N ? 0 : slot + 1;
       par ^= slot == 0 ? 1u : 0u;
-#ifdef MAS_FWD_PROFILE
-      pf_rest += clock64() - pf_d;
-#endif
     }
-#ifdef MAS_FWD_PROFILE
-    if (b == 0 && lane == 0)
-      printf("fwd4 warp g=%d: total %lld, stage-wait %lld, empty-wait %lld, compute %lld (%.1f/col), rest %lld, nit %d\n",
-             g, clock64() - pf_t0, pf_stage, pf_empty, pf_comp, (double)pf_comp / s_b, pf_rest, nit);
-#endif
     __syncwarp();
     bool bad = false;
 #pragma unroll
@@ -1009,14 +860,6 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
   }
   __syncwarp();
   cluster_sync_all();  // no CTA leaves while a peer may still write its FIFO
-#ifdef MAS_FWD_TIMELINE
-  if (threadIdx.x == 0) {
-    unsigned long long tl_end;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_end));
-    printf("TL cta %d item %d rank %d sm %u start %llu end %llu\n", blockIdx.x, b, crank, tl_smid,
-           tl_start, tl_end);
-  }
-#endif
 }
 
 }  // namespace
@@ -1105,11 +948,7 @@ cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorM
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(B * a.K), 1, 1);
   // + the producer warp (+ the MMA warp and four epilogue warps for the Gaussian source)
-#ifdef MAS_DUMMY_WARPS
-  cfg.blockDim = dim3(static_cast<unsigned>((a.W + 1 + (gauss ? 1 + 4 * a.W : 8)) * 32), 1, 1);
-#else
   cfg.blockDim = dim3(static_cast<unsigned>((a.W + 1 + (gauss ? 1 + 4 * a.W : 0)) * 32), 1, 1);
-#endif
   cfg.dynamicSmemBytes = fwd4_smem_bytes(R, a.W, a.N, a.Kp);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

@@ -11,15 +11,9 @@
 
 namespace mas {
 
-#ifndef MAS_FIFO_SLOTS
-#define MAS_FIFO_SLOTS 32
-#endif
-constexpr int kFifoSlots = MAS_FIFO_SLOTS;  // boundary-row FIFO depth, in quads
+constexpr int kFifoSlots = 32;  // boundary-row FIFO depth, in quads
 constexpr int kMaxWarpsPerCta = 8;
-#ifndef MAS_ZCOLS
-#define MAS_ZCOLS 128
-#endif
-constexpr int kZeroCols = MAS_ZCOLS;  // mas_fwd4: columns per fused zero-fill TMA store
+constexpr int kZeroCols = 128;  // mas_fwd4: columns per fused zero-fill TMA store
 constexpr int kMaxClusterCtas = 16;
 
 // Stream-ordered device allocation from the library's own pool on the

@@ -47,49 +47,21 @@ __device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-#ifdef MAS_WATCHDOG
-// Debug builds: a wait that spins for seconds reports itself and traps.
-__device__ __forceinline__ void mbar_watchdog(uint32_t& n, uint32_t bar, uint32_t parity) {
-  if (++n == (1u << 22)) {
-    printf("WATCHDOG block %d thread %d bar %u parity %u\n", blockIdx.x, threadIdx.x, bar, parity);
-    __trap();
-  }
-}
-#define MAS_WD_DECL uint32_t wd_n = 0;
-#define MAS_WD(bar, parity) mbar_watchdog(wd_n, bar, parity);
-#else
-#define MAS_WD_DECL
-#define MAS_WD(bar, parity)
-#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  MAS_WD_DECL
   while (!mbar_try_wait(bar, parity)) {
-    MAS_WD(bar, parity)
   }
 }
 // Warp-uniform variants for warps that shuffle right after: every lane
 // leaves with the same answer, so the warp stays converged (a lane that
 // left a spin loop alone would push every later SHFL onto the divergent
 // WARPSYNC path).
-#ifndef MAS_NO_VOTE
 __device__ __forceinline__ bool mbar_test_wait_all(uint32_t bar, uint32_t parity) {
   return __all_sync(0xffffffffu, mbar_test_wait(bar, parity));
 }
 __device__ __forceinline__ void mbar_wait_all(uint32_t bar, uint32_t parity) {
-  MAS_WD_DECL
   while (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
-    MAS_WD(bar, parity)
   }
 }
-#else
-__device__ __forceinline__ bool mbar_test_wait_all(uint32_t bar, uint32_t parity) {
-  return mbar_test_wait(bar, parity);
-}
-__device__ __forceinline__ void mbar_wait_all(uint32_t bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
-  }
-}
-#endif
 
 // Predicated forms (one guarded instruction instead of a branch around it:
 // the per-quad bookkeeping otherwise costs BSSY/ISETP/BRA per operation).

@@ -42,9 +42,7 @@ namespace {
 // R rows per lane: lane l owns rows l, l + 32, ... of its warp's 32R-row
 // block; CTAs of 8/R warps, so a strip is 256 rows either way.
 constexpr int kStripRows = 256;
-#ifndef MAS_SCORES_R
 #define MAS_SCORES_R 2  // rows per lane of the spread launch (R = 4 measured 1.6x slower at c3)
-#endif
 constexpr int kSpreadSmem = 160 * 1024;  // one CTA per SM for the spread launch
 constexpr int kStripPub = 8;  // tiles per cross-strip progress release
 constexpr int kTile = 32;

@@ -1,6 +1,6 @@
 """A/B timing of K1+K2 for several library builds, interleaved (A B A B ...),
 min and median over rounds; SM clock sampled via NVML.
-usage: python scratch/ab.py B T S lib1 lib2 ..."""
+usage: python tools/ab.py B T S lib1 lib2 ..."""
 import sys, os, subprocess, json
 B, T, S = sys.argv[1:4]
 libs = sys.argv[4:]
