@@ -87,6 +87,11 @@ enum mas_status {
 enum mas_engine { MAS_ENGINE_REFERENCE = 0, MAS_ENGINE_PARALLEL = 1 };
 
 #define MAS_FLAG_UNCHECKED 0x1u /* skip validate_config (detail::align_unchecked) */
+/* ABI 3, mas_align_device[_ex] only: do not read the NonFinite flags back
+ * (no host synchronisation; the call is enqueue-only).  Host-detectable
+ * errors (config, lengths) are still returned; a non-finite likelihood is
+ * then NOT reported and its item's alignment is undefined. */
+#define MAS_FLAG_NO_CHECK 0x2u
 
 typedef struct mas_error {
   int32_t status;     /* enum mas_status */
@@ -132,7 +137,10 @@ MAS_API int mas_align_host_ex(const float* values, int32_t batch, int32_t text_c
  * Device buffers (caller-owned, current device).  `row_pitch` = elements
  * between consecutive text rows (>= speech_cap); items are text_cap rows
  * apart.  `lengths` is a HOST array as above.  Enqueues on `stream` and
- * synchronises it before returning (the NonFinite check needs the result).
+ * synchronises it before returning (the NonFinite check needs the result),
+ * unless cfg->flags has MAS_FLAG_NO_CHECK.  Plans (validation, geometry,
+ * workspace, tensor maps) are cached across calls of the same shape, lengths,
+ * config and stream (ABI 3).
  */
 MAS_API int mas_align_device(const float* d_values, int64_t row_pitch, int32_t batch, int32_t text_cap,
                      int32_t speech_cap, const uint32_t* lengths, const mas_config_t* cfg,

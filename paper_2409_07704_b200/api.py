@@ -149,9 +149,11 @@ def _run_device(values, lens, cfg, b, t, s, want_out, want_paths, want_dur=False
 
 
 def _align_impl(values, lengths, engine, max_neg_val, threads, unchecked, want_out, want_paths,
-                want_dur=False):
+                want_dur=False, check=True):
     values, lens, cfg, was_2d, b, t, s = _prepare(values, lengths, engine, max_neg_val, threads,
                                                   unchecked)
+    if not check:
+        cfg.flags |= _lib.MAS_FLAG_NO_CHECK
     if _is_torch(values) and values.is_cuda:
         out, paths, dur = _run_device(values, lens, cfg, b, t, s, want_out, want_paths, want_dur)
     else:
@@ -161,18 +163,22 @@ def _align_impl(values, lengths, engine, max_neg_val, threads, unchecked, want_o
     return out, paths, dur, was_2d, lens, b, s
 
 
-def align(values, lengths=None, engine="parallel", max_neg_val=_DEFAULT_MAX_NEG_VAL, threads=0):
+def align(values, lengths=None, engine="parallel", max_neg_val=_DEFAULT_MAX_NEG_VAL, threads=0,
+          check=True):
     """Align a [T, S] or [B, T, S] float32 likelihood array; returns a uint8
     alignment array of the same shape. Optional lengths ([B, 2] of (t, s))
     mark each item's valid region.  (module.cpp:222-228; torch CUDA tensors
-    in -> torch CUDA tensor out.)"""
+    in -> torch CUDA tensor out.)  ``check=False`` (torch CUDA input only, not
+    in the reference): the call does not wait for the device's NonFinite
+    scan -- it only enqueues, so a training step stays asynchronous; length /
+    config errors are still raised, a non-finite likelihood is not."""
     out, _, _, was_2d, _, _, _ = _align_impl(values, lengths, engine, max_neg_val, threads, False,
-                                             True, False)
+                                             True, False, check=check)
     return out[0] if was_2d else out
 
 
 def align_durations(values, lengths=None, engine="parallel", max_neg_val=_DEFAULT_MAX_NEG_VAL,
-                    threads=0):
+                    threads=0, check=True):
     """Per-token durations: the row sums of ``align``'s alignment, int32
     [B, T] ([T] for 2-D input) -- the number of speech frames spent on each
     text token, 0 past an item's text length.  Not in the reference's
@@ -180,17 +186,17 @@ def align_durations(values, lengths=None, engine="parallel", max_neg_val=_DEFAUL
     never written, so the call moves 4.125 instead of 5.125 bytes per cell.
     Same arguments, checks and errors as ``align``."""
     _, _, dur, was_2d, _, _, _ = _align_impl(values, lengths, engine, max_neg_val, threads, False,
-                                             False, False, True)
+                                             False, False, True, check=check)
     return dur[0] if was_2d else dur
 
 
 def align_paths(values, lengths=None, engine="parallel", max_neg_val=_DEFAULT_MAX_NEG_VAL,
-                threads=0):
+                threads=0, check=True):
     """Like align, but returns per-frame text indices: one int32 array per
     item (a single array for 2-D input).  Each item's array has length s_b
     (path_from_matrix walks the item's valid lengths, types.cpp:161-179)."""
     _, paths, _, was_2d, lens, b, s = _align_impl(values, lengths, engine, max_neg_val, threads,
-                                                  False, False, True)
+                                                  False, False, True, check=check)
     result = []
     for i in range(b):
         sb = s if lens is None else int(lens[i, 1])

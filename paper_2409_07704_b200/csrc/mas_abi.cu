@@ -843,23 +843,111 @@ int mas_align_device(const float* d_values, int64_t row_pitch, int32_t batch, in
                              d_paths, nullptr, stream_v, err);
 }
 
+}  // extern "C"
+
+namespace {
+
+// Plans of mas_align_device_ex kept across calls (a training loop calls with
+// the same shape every step): validation, geometry, workspace and tensor maps
+// once, then each call is the kernels and (unless MAS_FLAG_NO_CHECK) one
+// flags readback.  Keyed by everything the plan depends on, including the
+// stream (its workspace is stream-ordered); a plan is checked out while in
+// use, so concurrent callers never share one.
+struct PlanKey {
+  int dev;
+  cudaStream_t stream;
+  int32_t B, T, S;
+  int64_t pitch;
+  int32_t engine, threads;
+  uint32_t flags;
+  uint32_t mnv_bits;
+  std::vector<uint32_t> lengths;
+  bool operator==(const PlanKey& o) const {
+    return dev == o.dev && stream == o.stream && B == o.B && T == o.T && S == o.S &&
+           pitch == o.pitch && engine == o.engine && threads == o.threads && flags == o.flags &&
+           mnv_bits == o.mnv_bits && lengths == o.lengths;
+  }
+};
+
+class PlanCache {
+ public:
+  static PlanCache& get() {
+    static PlanCache* c = new PlanCache();  // never destroyed: plans outlive static teardown
+    return *c;
+  }
+  mas_plan_t* take(const PlanKey& k) {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (size_t i = 0; i < idle_.size(); ++i)
+      if (idle_[i].first == k) {
+        mas_plan_t* p = idle_[i].second;
+        idle_.erase(idle_.begin() + static_cast<long>(i));
+        return p;
+      }
+    return nullptr;
+  }
+  void give(PlanKey k, mas_plan_t* p) {
+    mas_plan_t* evict = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      idle_.emplace_back(std::move(k), p);
+      if (idle_.size() > kMax) {
+        evict = idle_.front().second;
+        idle_.erase(idle_.begin());
+      }
+    }
+    if (evict) mas_plan_destroy(evict);
+  }
+
+ private:
+  static constexpr size_t kMax = 16;
+  std::mutex mu_;
+  std::vector<std::pair<PlanKey, mas_plan_t*>> idle_;
+};
+
+PlanKey plan_key(cudaStream_t stream, int32_t B, int32_t T, int32_t S, int64_t pitch,
+                 const uint32_t* lengths, const mas_config_t& c) {
+  PlanKey k;
+  cudaGetDevice(&k.dev);
+  k.stream = stream;
+  k.B = B;
+  k.T = T;
+  k.S = S;
+  k.pitch = pitch;
+  k.engine = c.engine;
+  k.threads = c.threads;
+  k.flags = c.flags & MAS_FLAG_UNCHECKED;
+  std::memcpy(&k.mnv_bits, &c.max_neg_val, 4);
+  if (lengths) k.lengths.assign(lengths, lengths + 2 * static_cast<size_t>(B));
+  return k;
+}
+
+}  // namespace
+
+extern "C" {
+
 int mas_align_device_ex(const float* d_values, int64_t row_pitch, int32_t batch,
                         int32_t text_cap, int32_t speech_cap, const uint32_t* lengths,
                         const mas_config_t* cfg, uint8_t* d_out, int32_t* d_paths,
                         int32_t* d_durations, void* stream_v, mas_error_t* err) {
   clear_error(err);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
-  mas_plan_t* plan = nullptr;
-  int rc = plan_create(batch, text_cap, speech_cap, row_pitch, lengths, cfg, 0, &plan, err, true);
-  if (rc) return rc;
-  plan->internal = true;
-  const float* q = d_values;
-  float* scratch = nullptr;
-  if ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (row_pitch & 3) != 0 ||
-      (text_cap & 3) != 0) {
+  mas_config_t c;
+  if (cfg)
+    c = *cfg;
+  else
+    mas_config_default(&c);
+  const bool check = (c.flags & MAS_FLAG_NO_CHECK) == 0u;
+  const bool repitch = (reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (row_pitch & 3) != 0 ||
+                       (text_cap & 3) != 0;
+  if (repitch) {
+    mas_plan_t* plan = nullptr;
+    int rc = plan_create(batch, text_cap, speech_cap, row_pitch, lengths, &c, 0, &plan, err, true);
+    if (rc) return rc;
+    plan->internal = true;
     // Re-pitch into an aligned [B][T_pad][pitch'] copy the TMA path accepts.
     const int T_pad = (text_cap + 3) & ~3;
     const int64_t pitch2 = (static_cast<int64_t>(speech_cap) + 3) & ~int64_t(3);
+    float* scratch = nullptr;
     cudaError_t e = mas::pool_alloc(reinterpret_cast<void**>(&scratch),
                                     static_cast<size_t>(batch) * T_pad * pitch2 * 4, stream);
     if (e != cudaSuccess) {
@@ -879,13 +967,38 @@ int mas_align_device_ex(const float* d_values, int64_t row_pitch, int32_t batch,
     }
     plan->pitch = pitch2;
     plan->T_pad = T_pad;
-    q = scratch;
+    rc = mas_plan_enqueue_ex(plan, MAS_PART_ALL, scratch, d_out, d_paths, d_durations, stream, err);
+    if (rc == MAS_OK) rc = mas_plan_finish(plan, scratch, stream, err);
+    cudaFreeAsync(scratch, stream);
+    cudaStreamSynchronize(stream);
+    mas_plan_destroy(plan);
+    return rc;
   }
-  rc = mas_plan_enqueue_ex(plan, MAS_PART_ALL, q, d_out, d_paths, d_durations, stream, err);
-  if (rc == MAS_OK) rc = mas_plan_finish(plan, q, stream, err);
-  if (scratch) cudaFreeAsync(scratch, stream);
-  cudaStreamSynchronize(stream);
-  mas_plan_destroy(plan);
+  PlanKey key = plan_key(stream, batch, text_cap, speech_cap, row_pitch, lengths, c);
+  mas_plan_t* plan = PlanCache::get().take(key);
+  if (!plan) {
+    const int rc = plan_create(batch, text_cap, speech_cap, row_pitch, lengths, &c, 0, &plan, err,
+                               true);
+    if (rc) return rc;
+    plan->internal = true;
+  }
+  int rc = mas_plan_enqueue_ex(plan, MAS_PART_ALL, d_values, d_out, d_paths, d_durations, stream,
+                               err);
+  if (rc == MAS_OK) {
+    if (check) {
+      rc = mas_plan_finish(plan, d_values, stream, err);
+    } else if (plan->first_host_error.item >= 0) {
+      // no device readback: host-detected item errors are still reported
+      rc = set_error(err, MAS_E_VALIDATION, plan->first_host_error.errc,
+                     plan->first_host_error.item, plan->first_host_error.message);
+    }
+  }
+  if (rc == MAS_OK || rc == MAS_E_VALIDATION) {
+    PlanCache::get().give(std::move(key), plan);
+  } else {
+    cudaStreamSynchronize(stream);
+    mas_plan_destroy(plan);
+  }
   return rc;
 }
 

@@ -84,14 +84,15 @@ __global__ void __launch_bounds__(256) gauss_prep_rows_kernel(
     for (int w = 0; w < 8; ++w) t += sbias[w][threadIdx.x];
     bias[static_cast<int64_t>(b) * Tp + i0 + threadIdx.x] = t;
   }
-  const int words = kPrepRows * Kp / 2;
+  // warp wid writes rows wid, wid + 8, ...: lanes cover a row's Kp/2 words
   uint32_t* out = reinterpret_cast<uint32_t*>(A + (static_cast<int64_t>(b) * Tp + i0) * Kp);
-  for (int L = threadIdx.x; L < words; L += blockDim.x) {
-    const int r = L / (Kp / 2), k = 2 * (L % (Kp / 2));
-    const float v0 = k < 2 * C ? sm[r * ld + k] : 0.f;
-    const float v1 = k + 1 < 2 * C ? sm[r * ld + k + 1] : 0.f;
-    out[L] = pack_bf16x2(v0, v1);
-  }
+  for (int r = wid; r < kPrepRows; r += 8)
+    for (int kw = lane; kw < Kp / 2; kw += 32) {
+      const int k = 2 * kw;
+      const float v0 = k < 2 * C ? sm[r * ld + k] : 0.f;
+      const float v1 = k + 1 < 2 * C ? sm[r * ld + k + 1] : 0.f;
+      out[r * (Kp / 2) + kw] = pack_bf16x2(v0, v1);
+    }
 }
 
 __global__ void __launch_bounds__(256) gauss_prep_frames_kernel(const float* __restrict__ z, int B,
@@ -107,19 +108,19 @@ __global__ void __launch_bounds__(256) gauss_prep_frames_kernel(const float* __r
     sm[lane * ld + c] = j < S ? z[(static_cast<int64_t>(b) * C + c) * S + j] : 0.f;
   }
   __syncthreads();
-  const int words = kPrepRows * Kp / 2;
   uint32_t* out = reinterpret_cast<uint32_t*>(Bm + (static_cast<int64_t>(b) * Sp + j0) * Kp);
-  for (int L = threadIdx.x; L < words; L += blockDim.x) {
-    const int r = L / (Kp / 2), k = 2 * (L % (Kp / 2));
-    float v[2];
+  for (int r = wid; r < kPrepRows; r += 8)
+    for (int kw = lane; kw < Kp / 2; kw += 32) {
+      const int k = 2 * kw;
+      float v[2];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int kk = k + e;
-      const float x = kk < 2 * C ? sm[r * ld + (kk < C ? kk : kk - C)] : 0.f;
-      v[e] = kk < C ? x * x : x;  // z^2 rows first, then z
+      for (int e = 0; e < 2; ++e) {
+        const int kk = k + e;
+        const float x = kk < 2 * C ? sm[r * ld + (kk < C ? kk : kk - C)] : 0.f;
+        v[e] = kk < C ? x * x : x;  // z^2 rows first, then z
+      }
+      out[r * (Kp / 2) + kw] = pack_bf16x2(v[0], v[1]);
     }
-    out[L] = pack_bf16x2(v[0], v[1]);
-  }
 }
 
 // ---- K4b: q to HBM -----------------------------------------------------------

@@ -502,3 +502,29 @@ def test_durations_device_plan_and_errors(mas, oracle, cuda):
         mas.align_durations(bad)
     with pytest.raises(ValueError):
         mas.align_durations(bad[:, :, :10], lengths=[[20, 10], [20, 10]])
+
+
+def test_torch_check_false_is_enqueue_only(mas, oracle, cuda):
+    """align(torch, check=False): same alignment, no NonFinite readback
+    (a non-finite likelihood is not reported), host-side length errors still
+    raised; repeated calls reuse the cached plan."""
+    import torch
+
+    rng = np.random.default_rng(12)
+    q = rng.uniform(-5, 5, (4, 40, 120)).astype(np.float32)
+    lens = np.array([[40, 120], [13, 50], [7, 7], [30, 100]])
+    exp = oracle.align(q, lens)[3]
+    qd = torch.from_numpy(q).cuda()
+    for _ in range(3):
+        got = mas.align(qd, lengths=lens, check=False)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), exp)
+    bad = qd.clone()
+    bad[1, 2, 3] = float("nan")
+    mas.align(bad, lengths=lens, check=False)  # not reported
+    with pytest.raises(ValueError, match="non-finite"):
+        mas.align(bad, lengths=lens)
+    with pytest.raises(ValueError):
+        mas.align(qd, lengths=np.array([[40, 120], [13, 50], [8, 7], [30, 100]]), check=False)
+    d1 = mas.align_durations(qd, lengths=lens, check=False)
+    assert np.array_equal(d1.cpu().numpy(), exp.sum(2).astype(np.int32))

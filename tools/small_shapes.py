@@ -44,6 +44,22 @@ for name, (B, T, S, lens) in {"c1": (1, 64, 256, None), "c2": (32, 200, 800, c2_
         e0.record(); plan.enqueue(q, out); e1.record(); torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3)
     step = float(np.median(ts))
+    # the same enqueue captured in a CUDA graph: device time without host launch cost
+    gs = torch.cuda.Stream()
+    with torch.cuda.stream(gs):
+        plan.enqueue(q, out, stream=gs)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=gs):
+        plan.enqueue(q, out, stream=gs)
+    for _ in range(5):
+        graph.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0.record(); graph.replay(); e1.record(); torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    graph_us = float(np.median(ts))
     for _ in range(5):
         m.align(q, lengths=lens)
     torch.cuda.synchronize()
@@ -51,12 +67,17 @@ for name, (B, T, S, lens) in {"c1": (1, 64, 256, None), "c2": (32, 200, 800, c2_
     for _ in range(reps):
         t0 = time.perf_counter(); m.align(q, lengths=lens); torch.cuda.synchronize(); ts.append((time.perf_counter() - t0) * 1e6)
     torch_us = float(np.median(ts))
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter(); m.align(q, lengths=lens, check=False); ts.append((time.perf_counter() - t0) * 1e6)
+    torch.cuda.synchronize()
+    nocheck_us = float(np.median(ts))
     qn = q.cpu().numpy()
     for _ in range(3):
         m.align(qn, lengths=lens)
     ts = []
     for _ in range(max(5, reps // 5)):
         t0 = time.perf_counter(); m.align(qn, lengths=lens); ts.append((time.perf_counter() - t0) * 1e6)
-    res[name] = {"shape": [B, T, S], "step_us": round(step, 1), "align_torch_us": round(torch_us, 1),
+    res[name] = {"shape": [B, T, S], "step_us": round(step, 1), "graph_replay_us": round(graph_us, 1), "align_torch_us": round(torch_us, 1), "align_torch_nocheck_enqueue_us": round(nocheck_us, 1),
                  "align_numpy_us": round(float(np.median(ts)), 1), "launches": plan_launches if (plan_launches := None) else None}
 print(json.dumps(res))
