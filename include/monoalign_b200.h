@@ -92,6 +92,13 @@ enum mas_engine { MAS_ENGINE_REFERENCE = 0, MAS_ENGINE_PARALLEL = 1 };
  * errors (config, lengths) are still returned; a non-finite likelihood is
  * then NOT reported and its item's alignment is undefined. */
 #define MAS_FLAG_NO_CHECK 0x2u
+/* ABI 3, mas_plan_create only: consecutive enqueues of the plan may overlap
+ * -- batch i's backtrack kernel runs concurrently with batch i+1's forward
+ * kernel (programmatic dependent launch; two direction-word buffers, the
+ * forward waits on a device counter before reusing the one a backtrack two
+ * batches back read).  The caller must give consecutive enqueues distinct
+ * output buffers.  Not for CUDA-graph capture. */
+#define MAS_FLAG_PIPELINED 0x4u
 
 typedef struct mas_error {
   int32_t status;     /* enum mas_status */

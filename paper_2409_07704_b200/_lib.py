@@ -23,6 +23,7 @@ MAS_ENGINE_REFERENCE = 0
 MAS_ENGINE_PARALLEL = 1
 MAS_FLAG_UNCHECKED = 0x1
 MAS_FLAG_NO_CHECK = 0x2
+MAS_FLAG_PIPELINED = 0x4
 MAS_PART_FORWARD = 0x1
 MAS_PART_BACKTRACK = 0x2
 MAS_PART_ALL = 0x3

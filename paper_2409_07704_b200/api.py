@@ -424,7 +424,7 @@ class Plan:
     then kernels only -- what the benchmark times and a CUDA graph captures."""
 
     def __init__(self, b, t, s, row_pitch=None, lengths=None, engine="parallel",
-                 max_neg_val=_DEFAULT_MAX_NEG_VAL, unchecked=False):
+                 max_neg_val=_DEFAULT_MAX_NEG_VAL, unchecked=False, pipelined=False):
         lib = _lib.load()
         self._lib = lib
         self.b, self.t, self.s = b, t, s
@@ -432,6 +432,10 @@ class Plan:
         lens = None if lengths is None else _parse_lengths(lengths, b, t, s)
         self._lens = lens
         cfg = _make_config(engine, max_neg_val, 0, unchecked)
+        if pipelined:
+            # consecutive enqueues may overlap (batch i's backtrack with batch
+            # i+1's forward); give consecutive enqueues distinct outputs
+            cfg.flags |= _lib.MAS_FLAG_PIPELINED
         handle = ctypes.c_void_p()
         err = _lib.MasError()
         rc = lib.mas_plan_create(b, t, s, self.row_pitch,

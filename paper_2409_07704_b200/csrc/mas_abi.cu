@@ -353,9 +353,15 @@ struct mas_plan {
   ItemError first_host_error;
   // device workspace
   uint32_t* d_lengths = nullptr;
-  uint32_t* d_dirs = nullptr;
+  uint32_t* d_dirs = nullptr;       // the buffer of the current batch
+  uint32_t* d_dirs_buf[2] = {nullptr, nullptr};  // pipelined: two, alternating
+  bool pipelined = false;
+  int dirs_par = 0;
+  unsigned* d_bt_done = nullptr;     // pipelined: finished backtrack CTAs per buffer
+  unsigned bt_issued[2] = {0u, 0u};  // backtrack CTAs launched per buffer
   bool all_full = true;  // every item spans the full [T_cap x S_cap]
-  int* d_flags = nullptr;
+  int* d_flags = nullptr;  // the current batch's NonFinite flags
+  int* d_flags_buf[2] = {nullptr, nullptr};
   unsigned long long* d_locate = nullptr;
   int launches = 0;
   int device = 0;
@@ -417,8 +423,10 @@ void mas_plan_destroy(mas_plan_t* p) {
   for (auto& se : p->done) cudaEventDestroy(se.second);
   cudaStream_t st = cudaStreamPerThread;
   cudaFreeAsync(p->d_lengths, st);
-  cudaFreeAsync(p->d_dirs, st);
-  cudaFreeAsync(p->d_flags, st);
+  cudaFreeAsync(p->d_dirs_buf[0], st);
+  if (p->d_dirs_buf[1]) cudaFreeAsync(p->d_dirs_buf[1], st);
+  if (p->d_bt_done) cudaFreeAsync(p->d_bt_done, st);
+  cudaFreeAsync(p->d_flags_buf[0], st);
   cudaFreeAsync(p->d_locate, st);
   if (p->d_bnd) cudaFreeAsync(p->d_bnd, st);
   if (p->d_sync) cudaFreeAsync(p->d_sync, st);
@@ -527,9 +535,18 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
   if ((e = cudaMemcpyAsync(p->d_lengths, p->lengths.data(), nB * 2 * sizeof(uint32_t),
                            cudaMemcpyHostToDevice, st)) != cudaSuccess)
     return fail(e, "cudaMemcpyAsync(lengths)");
-  if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_dirs),
-                           nB * g.M * g.T_alloc * sizeof(uint32_t), st)) != cudaSuccess)
-    return fail(e, "mas::pool_alloc(dirs)");
+  p->pipelined = (cfg.flags & MAS_FLAG_PIPELINED) != 0u && !deferred;
+  for (int k = 0; k < (p->pipelined ? 2 : 1); ++k)
+    if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_dirs_buf[k]),
+                             nB * g.M * g.T_alloc * sizeof(uint32_t), st)) != cudaSuccess)
+      return fail(e, "mas::pool_alloc(dirs)");
+  p->d_dirs = p->d_dirs_buf[0];
+  if (p->pipelined) {
+    if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_bt_done), 2 * sizeof(unsigned), st)) !=
+            cudaSuccess ||
+        (e = cudaMemsetAsync(p->d_bt_done, 0, 2 * sizeof(unsigned), st)) != cudaSuccess)
+      return fail(e, "backtrack counters");
+  }
   p->bt_rows = std::min(256, g.T_alloc);  // backtrack window rows
   if (g.bands > 1) {
     p->bnd_pitch = (speech_cap + 31) & ~31;
@@ -541,9 +558,13 @@ int plan_create(int32_t batch, int32_t text_cap, int32_t speech_cap, int64_t row
                              nB * g.bands * sizeof(int), st)) != cudaSuccess)
       return fail(e, "mas::pool_alloc(band progress)");
   }
-  if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_flags), nB * sizeof(int), st)) !=
-      cudaSuccess)
+  // pipelined plans: consecutive forward kernels may overlap, so each
+  // direction-word buffer has its own NonFinite flags
+  if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_flags_buf[0]),
+                           (p->pipelined ? 2 : 1) * nB * sizeof(int), st)) != cudaSuccess)
     return fail(e, "mas::pool_alloc(flags)");
+  p->d_flags_buf[1] = p->pipelined ? p->d_flags_buf[0] + nB : nullptr;
+  p->d_flags = p->d_flags_buf[0];
   if ((e = mas::pool_alloc(reinterpret_cast<void**>(&p->d_locate), sizeof(unsigned long long),
                            st)) != cudaSuccess)
     return fail(e, "mas::pool_alloc(locate)");
@@ -589,6 +610,11 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
   const Geometry& g = p->geo;
   if (p->ws_ready) MAS_CUDA(cudaStreamWaitEvent(stream, p->ws_ready, 0), "workspace wait");
   int nfwd = 0, nbt = 0;
+  if (p->pipelined && (parts & MAS_PART_FORWARD)) {  // next direction-word / flags buffers
+    p->dirs_par ^= 1;
+    p->d_dirs = p->d_dirs_buf[p->dirs_par];
+    p->d_flags = p->d_flags_buf[p->dirs_par];
+  }
   if ((parts & MAS_PART_FORWARD) && p->nan_parallel) {
     // parallel::detail::align_unchecked with a NaN sentinel: std::max's rule
     // ((a < b) ? b : a, a NaN first operand wins) shapes the score table,
@@ -716,6 +742,11 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
       fa.gA = p->gauss->A;
       fa.gbias = p->gauss->bias;
     }
+    if (p->pipelined) {
+      fa.bt_done = p->d_bt_done + p->dirs_par;
+      fa.bt_need = p->bt_issued[p->dirs_par];
+      fa.pdl = 1;
+    }
     fa.ticket = p->d_sync ? p->d_sync + b0 : nullptr;
     fa.progress = p->d_sync ? p->d_sync + p->B : nullptr;
     // All bands of all items in one launch (clusters ordered by ticket).
@@ -730,7 +761,7 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     nfwd = 1;
   }
   if ((parts & MAS_PART_BACKTRACK) && (d_out || d_paths || d_dur)) {
-    mas::BtArgs ba;
+    mas::BtArgs ba = {};
     ba.b0 = b0;
     ba.lengths = p->d_lengths;
     ba.dirs = p->d_dirs;
@@ -743,7 +774,9 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     ba.M = g.M;
     ba.T_alloc = g.T_alloc;
     ba.R = p->bt_rows;
+    ba.done = p->pipelined ? p->d_bt_done + p->dirs_par : nullptr;
     MAS_CUDA(mas::launch_backtrack(ba, stream, &nbt), "launch backtrack");
+    if (p->pipelined) p->bt_issued[p->dirs_par] += static_cast<unsigned>(nb);
   }
   p->launches = nfwd + nbt;
   return MAS_OK;

@@ -136,9 +136,19 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // a pipelined plan's next forward kernel may start now (it writes the other
+  // direction-word buffer and a different output)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // Everything below reads the forward kernel's direction bits or writes
   // after its zero fill (programmatic dependent launch).
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // pipelined plans: this CTA has finished reading the direction words
+  auto signal_done = [&]() {
+    if (a.done) {
+      __threadfence();
+      atomicAdd(a.done, 1u);
+    }
+  };
   // Durations (row sums of the alignment): the buffer first holds each
   // row's last column (-1 = before column 0), written by the expander at the
   // walk's exits, and is turned into differences at the end.
@@ -152,6 +162,7 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
     int32_t* path = a.path ? a.path + static_cast<size_t>(b) * a.S_cap : nullptr;
     if (path)
       for (int j = threadIdx.x; j < a.S_cap; j += 64) path[j] = -1;
+    if (threadIdx.x == 0) signal_done();
     return;
   }
   const int n_top = (s - 1) / kBtCols;
@@ -335,6 +346,7 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
   };
   if (s == 1) {
     if (dur) finish_durations();
+    if (lane == 0) signal_done();
     return;
   }
   uint32_t ph_done = 0;
@@ -378,6 +390,8 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
       if (dur && valid && ((rx[i] >> (31 - lane)) & 1u)) dur[row] = j;
     }
   }
+  // the walker's last window copy landed before its records were handed over
+  if (lane == 0) signal_done();
   if (dur) finish_durations();
 }
 

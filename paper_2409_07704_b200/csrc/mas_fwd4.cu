@@ -415,6 +415,17 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     }
     umma::fence_before_sync();
   }
+  // Pipelined plans: this launch may run alongside the previous batch's
+  // backtrack; the one two batches back read the same direction-word buffer
+  // and must have finished with it (one poll in practice).
+  if (a.bt_done && threadIdx.x == 0) {
+    unsigned v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bt_done) : "memory");
+      if (v >= a.bt_need) break;
+      __nanosleep(256);
+    }
+  }
   // the item's NonFinite flag starts at 0 (set by atomicOr only after the
   // cluster barrier below, and in the bands below after this band's
   // progress releases)
@@ -956,8 +967,15 @@ cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorM
   attr[0].val.clusterDim.x = static_cast<unsigned>(a.K);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cudaLaunchAttribute attrs2[2] = {attr[0], {}};
+  if (a.pdl) {
+    // may start while the previous kernel in the stream (a backtrack that
+    // triggered early) still runs; it shares no buffer with it
+    attrs2[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs2[1].val.programmaticStreamSerializationAllowed = 1;
+  }
+  cfg.attrs = attrs2;
+  cfg.numAttrs = a.pdl ? 2 : 1;
   if (R != 4) return cudaErrorInvalidValue;
   if (gauss)
     return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0, 1>, tmq, tm_out, a)

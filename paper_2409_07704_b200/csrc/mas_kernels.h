@@ -72,6 +72,11 @@ struct FwdArgs {
   int Tp, Sp;               // padded rows / frames per item of the operands
   const __nv_bfloat16* gA;  // [B][Tp][Kp]
   const float* gbias;       // [B][Tp]
+  // pipelined plans: before writing `dirs`, wait until *bt_done >= bt_need
+  // (the backtrack that last read this buffer has finished with it)
+  const unsigned* bt_done;
+  unsigned bt_need;
+  int pdl;                  // launched with programmatic stream serialization
   uint32_t one;             // 1 and 0.0f passed at run time so ptxas keeps the
   float zero;               //   bit IMADs / NonFinite FFMAs on the FMA pipe
 };
@@ -85,6 +90,7 @@ struct BtArgs {
   int32_t* dur;             // [B][T_cap] int32 durations (row sums of the alignment) or null
   int B, T_cap, S_cap, M, T_alloc;
   int R;                    // rows per backtrack window (<= 256, <= T_alloc)
+  unsigned* done;           // pipelined plans: +1 per CTA once its direction words are read
 };
 
 cudaError_t launch_backtrack(const BtArgs& a, cudaStream_t stream, int* launches);

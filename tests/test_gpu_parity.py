@@ -528,3 +528,27 @@ def test_torch_check_false_is_enqueue_only(mas, oracle, cuda):
         mas.align(qd, lengths=np.array([[40, 120], [13, 50], [8, 7], [30, 100]]), check=False)
     d1 = mas.align_durations(qd, lengths=lens, check=False)
     assert np.array_equal(d1.cpu().numpy(), exp.sum(2).astype(np.int32))
+
+
+def test_pipelined_plan_overlapping_batches(mas, oracle, cuda):
+    """Plan(pipelined=True): consecutive enqueues overlap (backtrack of batch
+    i alongside the forward of batch i+1, two direction-word buffers); with
+    distinct outputs per enqueue every batch's result is exact."""
+    import torch
+
+    B, T, S = 8, 256, 1024
+    qs = [mas.generate_device(B, T, S, seed) for seed in (3, 4, 5)]
+    exp = [mas.align(q).clone() for q in qs]
+    exp_p = [torch.stack([torch.as_tensor(p) for p in mas.align_paths(q.cpu().numpy())]).cuda()
+             for q in qs]
+    plan = mas.Plan(B, T, S, pipelined=True)
+    outs = [torch.empty((B, T, S), dtype=torch.uint8, device="cuda") for _ in range(3)]
+    paths = [torch.empty((B, S), dtype=torch.int32, device="cuda") for _ in range(3)]
+    for rep in range(4):
+        for k in range(9):
+            plan.enqueue(qs[k % 3], outs[k % 3], paths[k % 3])
+        torch.cuda.synchronize()
+        for k in range(3):
+            assert torch.equal(outs[k], exp[k]), (rep, k)
+            assert torch.equal(paths[k], exp_p[k]), (rep, k)
+    plan.finish(qs[2])
