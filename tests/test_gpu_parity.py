@@ -408,6 +408,17 @@ for eng in ('parallel', 'reference'):
         assert np.array_equal(gp[b], ep[b, :ls[b]]), (eng, b)
     gd = m.align_durations(q, lengths=lens, engine=eng)
     assert np.array_equal(gd, exp.sum(axis=2, dtype=np.int64).astype(np.int32)), eng
+# a pipelined plan over the banded geometry (band tickets are reset between
+# batches, so batches do not overlap there; results must still be exact)
+import torch
+qd = torch.from_numpy(q).cuda()
+exp = torch.from_numpy(o.align(q, lens)[3]).cuda()
+pp = m.Plan({B}, {T}, {S}, lengths=lens, pipelined=True)
+outs = [torch.empty_like(exp) for _ in range(2)]
+for k in range(5):
+    pp.enqueue(qd, outs[k % 2])
+torch.cuda.synchronize()
+assert torch.equal(outs[0], exp) and torch.equal(outs[1], exp)
 print('OK')
 """
     env = dict(os.environ, MAS_BAND_WARPS="2")
