@@ -1466,8 +1466,38 @@ int mas_align_gaussian_device(const float* d_z, const float* d_mean, const float
                      "gaussian log-likelihood: at most " + std::to_string(mas::kGaussMaxChannels) +
                          " channels");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  mas_config_t c;
+  if (cfg)
+    c = *cfg;
+  else
+    mas_config_default(&c);
+  if ((c.flags & MAS_FLAG_UNCHECKED) && std::isnan(c.max_neg_val) &&
+      c.engine == MAS_ENGINE_PARALLEL) {
+    // NaN sentinel, parallel engine: std::max's NaN rule needs the score
+    // table (see nan_parallel), so q is materialised (still on the device)
+    // and aligned by the ordinary path.
+    float* q = nullptr;
+    if (batch < 1 || text_cap < 1 || speech_cap < 1)
+      return set_error(err, MAS_E_VALIDATION, MAS_ERRC_ZERO_DIM, -1,
+                       "every dimension must be at least 1");
+    const int64_t pitch = (static_cast<int64_t>(speech_cap) + 3) & ~int64_t(3);
+    cudaError_t e = mas::pool_alloc(reinterpret_cast<void**>(&q),
+                                    static_cast<size_t>(batch) * text_cap * pitch * sizeof(float),
+                                    stream);
+    int rc = MAS_OK;
+    if (e == cudaSuccess)
+      rc = mas_gaussian_loglik_device(d_z, d_mean, d_logstd, batch, channels, text_cap,
+                                      speech_cap, q, pitch, stream_v, err);
+    if (e == cudaSuccess && rc == MAS_OK)
+      rc = mas_align_device_ex(q, pitch, batch, text_cap, speech_cap, lengths, &c, d_out, d_paths,
+                               d_durations, stream_v, err);
+    if (q) cudaFreeAsync(q, stream);
+    cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) return cuda_error(err, e, "gaussian alignment");
+    return rc;
+  }
   mas_plan_t* plan = nullptr;
-  int rc = plan_create(batch, text_cap, speech_cap, speech_cap, lengths, cfg, 0, &plan, err, true,
+  int rc = plan_create(batch, text_cap, speech_cap, speech_cap, lengths, &c, 0, &plan, err, true,
                        mas::gauss_kp(channels));
   if (rc) return rc;
   plan->internal = true;

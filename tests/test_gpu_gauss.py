@@ -167,3 +167,19 @@ def test_fused_nonfinite_is_located(mas, cuda):
     z[1, 2, 17] = float("nan")  # column 17 of every row of item 1
     with pytest.raises(ValueError, match=r"item 1: non-finite likelihood at \(0, 17\)"):
         mas.align_gaussian(z, mean, logstd)
+
+
+@pytest.mark.parametrize("engine", ["parallel", "reference"])
+@pytest.mark.parametrize("mnv", [float("-inf"), -1e9, float("nan")])
+def test_fused_unchecked_sentinels(mas, cuda, engine, mnv):
+    """detail::align_unchecked sentinels through the fused path equal the
+    unfused path on the same q (NaN: std::max semantics, parallel engine via
+    the materialised score table)."""
+    import torch
+
+    z, mean, logstd = _inputs(3, 24, 90, 400, seed=21)
+    got = mas.align_gaussian(z, mean, logstd, engine=engine, max_neg_val=mnv,
+                             unchecked=True)["alignment"]
+    q = mas.gaussian_loglik(z, mean, logstd)
+    exp = mas._align_unchecked(q, engine=engine, max_neg_val=mnv)
+    assert torch.equal(got, exp)
