@@ -268,8 +268,10 @@ MAS_API int mas_gaussian_loglik_device(const float* d_z, const float* d_mean,
  * outputs, validation, errors and engines as mas_align_device_ex (lengths a
  * HOST [batch][2] array or NULL; a non-finite q is reported at its exact
  * (i, j)); the alignment equals mas_align_device_ex on the q
- * mas_gaussian_loglik_device writes, bit for bit.  Texts up to one cluster of
- * rows (4096 at 192 channels).  Synchronises `stream`.  (ABI 3) */
+ * mas_gaussian_loglik_device writes, bit for bit.  The fused kernel handles
+ * texts up to one cluster of rows (4096); taller texts, and NaN sentinels of
+ * the parallel engine, materialise q on the device and take the ordinary
+ * path.  Synchronises `stream`.  (ABI 3) */
 MAS_API int mas_align_gaussian_device(const float* d_z, const float* d_mean,
                                       const float* d_logstd, int32_t batch, int32_t channels,
                                       int32_t text_cap, int32_t speech_cap,

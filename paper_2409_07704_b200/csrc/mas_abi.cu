@@ -1471,11 +1471,22 @@ int mas_align_gaussian_device(const float* d_z, const float* d_mean, const float
     c = *cfg;
   else
     mas_config_default(&c);
-  if ((c.flags & MAS_FLAG_UNCHECKED) && std::isnan(c.max_neg_val) &&
-      c.engine == MAS_ENGINE_PARALLEL) {
-    // NaN sentinel, parallel engine: std::max's NaN rule needs the score
-    // table (see nan_parallel), so q is materialised (still on the device)
-    // and aligned by the ordinary path.
+  // Texts taller than one cluster of rows (the fused kernel runs one band)
+  // and NaN sentinels of the parallel engine (std::max's NaN rule needs the
+  // score table, see nan_parallel): q is materialised, still on the device,
+  // and aligned by the ordinary path.
+  bool fused_ok = true;
+  {
+    uint32_t t_max = 0;
+    for (int32_t b = 0; lengths && b < batch; ++b) t_max = std::max(t_max, lengths[2 * b]);
+    if (!lengths) t_max = static_cast<uint32_t>(text_cap);
+    Geometry probe;
+    fused_ok = batch >= 1 && text_cap >= 1 && speech_cap >= 1 &&
+               cached_geometry(batch, std::max<int>(static_cast<int>(t_max), 1), speech_cap, &probe,
+                               mas::gauss_kp(channels));
+  }
+  if (!fused_ok || ((c.flags & MAS_FLAG_UNCHECKED) && std::isnan(c.max_neg_val) &&
+                    c.engine == MAS_ENGINE_PARALLEL)) {
     float* q = nullptr;
     if (batch < 1 || text_cap < 1 || speech_cap < 1)
       return set_error(err, MAS_E_VALIDATION, MAS_ERRC_ZERO_DIM, -1,

@@ -183,3 +183,15 @@ def test_fused_unchecked_sentinels(mas, cuda, engine, mnv):
     q = mas.gaussian_loglik(z, mean, logstd)
     exp = mas._align_unchecked(q, engine=engine, max_neg_val=mnv)
     assert torch.equal(got, exp)
+
+
+def test_fused_tall_text_falls_back_to_materialised_q(mas, cuda):
+    """Texts taller than one cluster (> 4096 rows): align_gaussian still
+    answers, through q materialised on the device."""
+    import torch
+
+    z, mean, logstd = _inputs(1, 16, 4200, 4300, seed=31)
+    got = mas.align_gaussian(z, mean, logstd, outputs=("paths",))["paths"]
+    exp = mas.align_paths(mas.gaussian_loglik(z, mean, logstd))
+    assert torch.equal(got[0].cpu(), torch.as_tensor(exp[0]).cpu() if not hasattr(exp[0], "cpu")
+                       else exp[0].cpu())
