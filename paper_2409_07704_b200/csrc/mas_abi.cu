@@ -801,11 +801,14 @@ int mas_plan_enqueue_ex(mas_plan_t* p, uint32_t parts, const float* d_values, ui
                         mas_error_t* err) {
   clear_error(err);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (!p->internal) MAS_CUDA(cudaStreamIsCapturing(stream, &cap), "cudaStreamIsCapturing");
+  if (p->pipelined && cap != cudaStreamCaptureStatusNone)
+    return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
+                     "pipelined plans cannot be captured in a CUDA graph");
   const int rc = enqueue_items(p, parts, 0, p->B, d_values, d_out, d_paths, d_durations, stream, err);
   if (rc != MAS_OK || p->internal) return rc;
   // remember the enqueue so mas_plan_destroy can wait for it
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  MAS_CUDA(cudaStreamIsCapturing(stream, &cap), "cudaStreamIsCapturing");
   if (cap != cudaStreamCaptureStatusNone) {
     p->captured = true;
     return MAS_OK;
