@@ -21,6 +21,7 @@
 //   path[] and the ones of the alignment matrix.
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "mas_kernels.h"
 #include "mas_ptx.cuh"
@@ -30,6 +31,10 @@ namespace mas {
 namespace {
 
 constexpr int kBtMaxRows = 256;  // rows per window (TMA box limit)
+// Stages in the ring of the 16-word variant: 2 (three / four measured 49 /
+// 56 us at c3 against 41: a deeper prefetch positions windows on a staler
+// walk row, so more of them miss and re-centre synchronously).
+constexpr int kBtWideStages = 2;
 
 // Window load of stage n: words [8n, 8n + 8) (those < M) of rows
 // [row0, row0 + R), as one bulk copy per word (a word's rows are contiguous
@@ -104,15 +109,15 @@ __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
 // WORDS direction words (32 columns each) per stage, 32 / WORDS stages in
 // the ring: 8 for steep paths (a window row count bounds the rows a stage
 // can climb), 16 for shallow ones (half the stage transitions).
-template <int WORDS>
+template <int WORDS, int STAGES>
 __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
   constexpr int kBtWords = WORDS;
-  constexpr int kBtStages = 32 / WORDS;
+  constexpr int kBtStages = STAGES;
   constexpr int kBtCols = 32 * WORDS;
   // Guard words in front: a block may read up to 8 rows below row 0, and the
   // speculative next-word load one word (R rows) before the first word.
   constexpr int kGuard = kBtMaxRows + 32;
-  __shared__ alignas(128) uint32_t win_raw[kGuard + kBtStages * kBtWords * kBtMaxRows];
+  extern __shared__ __align__(128) uint32_t win_raw[];  // [kGuard + stages * words * rows]
   __shared__ alignas(8) uint64_t bars[3 * kBtStages];  // full | done | free
   __shared__ int rec_y[kBtStages][kBtWords];
   __shared__ uint32_t rec_ex[kBtStages][kBtWords];
@@ -178,14 +183,14 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
     uint32_t ph_full = 0, ph_free = 0, pend = 0;
 #define PR_T(v)
     for (int k = 0; k < kBtStages && n_top - k >= 0; ++k) {
-      const int n = n_top - k, slot = n & (kBtStages - 1);
+      const int n = n_top - k, slot = n % kBtStages;
       s_ylo[slot] = bt_row0(y, R, T_alloc);
       bt_issue<kBtWords>(win_s + slot * kSlotBytes, full_s + 8u * slot, dirs, s_ylo[slot], n, M, T_alloc,
                R);
       pend |= 1u << slot;
     }
     for (int n = n_top; n >= 0; --n) {
-      const int slot = n & (kBtStages - 1);
+      const int slot = n % kBtStages;
       if (n + kBtStages <= n_top) {  // records of stage n + kBtStages expanded?
         PR_T(a0);
         mbar_wait(free_s + 8u * slot, (ph_free >> slot) & 1u);
@@ -351,7 +356,7 @@ __global__ void __launch_bounds__(64, 1) bt_walk_kernel(const BtArgs a) {
   }
   uint32_t ph_done = 0;
   for (int n = n_top; n >= 0; --n) {
-    const int slot = n & (kBtStages - 1);
+    const int slot = n % kBtStages;
     mbar_wait(done_s + 8u * slot, (ph_done >> slot) & 1u);
     ph_done ^= 1u << slot;
     int ry[kBtWords];
@@ -443,6 +448,33 @@ int grid_for(size_t n, int threads) {
 
 }  // namespace
 
+namespace {
+// the direction-word window ring (dynamic shared memory, above the 48 KB
+// static limit for three 16-word stages)
+constexpr size_t bt_smem_bytes(int words, int stages) {
+  return (static_cast<size_t>(kBtMaxRows + 32) + static_cast<size_t>(stages) * words * kBtMaxRows) * 4;
+}
+cudaError_t bt_kernels_configure() {
+  constexpr int kMaxDevices = 64;
+  static std::once_flag once[kMaxDevices];
+  static cudaError_t status[kMaxDevices];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::call_once(once[dev], [dev] {
+    cudaError_t r = cudaFuncSetAttribute(bt_walk_kernel<16, kBtWideStages>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(bt_smem_bytes(16, kBtWideStages)));
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(bt_walk_kernel<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(bt_smem_bytes(8, 4)));
+    status[dev] = r;
+  });
+  return status[dev];
+}
+}  // namespace
+
 cudaError_t launch_backtrack(const BtArgs& a, cudaStream_t stream, int* launches) {
   // Programmatic dependent launch: the walkers' prologue overlaps the tail
   // of the forward kernel; griddepcontrol.wait orders every data access.
@@ -459,8 +491,14 @@ cudaError_t launch_backtrack(const BtArgs& a, cudaStream_t stream, int* launches
   if (launches) *launches = 1;
   // shallow paths (at most one text row per four speech frames): wider stages
   const bool wide = 4 * a.T_cap <= a.S_cap;
-  return wide ? cudaLaunchKernelEx(&cfg, bt_walk_kernel<16>, a)
-              : cudaLaunchKernelEx(&cfg, bt_walk_kernel<8>, a);
+  const cudaError_t ce = bt_kernels_configure();
+  if (ce != cudaSuccess) return ce;
+  if (wide) {
+    cfg.dynamicSmemBytes = bt_smem_bytes(16, kBtWideStages);
+    return cudaLaunchKernelEx(&cfg, bt_walk_kernel<16, kBtWideStages>, a);
+  }
+  cfg.dynamicSmemBytes = bt_smem_bytes(8, 4);
+  return cudaLaunchKernelEx(&cfg, bt_walk_kernel<8, 4>, a);
 }
 
 cudaError_t bt_configure(int /*T_alloc*/, int /*L*/) { return cudaSuccess; }
