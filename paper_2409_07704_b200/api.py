@@ -29,8 +29,8 @@ def _is_torch(x) -> bool:
 
 # ---- module.cpp:21-35 make_config ------------------------------------------
 def _make_config(engine: str, max_neg_val: float, threads: int, unchecked: bool = False):
-    cfg = _lib.MasConfig()
-    _lib.load().mas_config_default(ctypes.byref(cfg))
+    # MasConfig defaults (mas_config_default), filled here without a C call
+    cfg = _lib.MasConfig(_lib.MAS_ENGINE_PARALLEL, _DEFAULT_MAX_NEG_VAL, 0, 0, 0)
     if engine == "reference":
         cfg.engine = _lib.MAS_ENGINE_REFERENCE
     elif engine == "parallel":
@@ -66,10 +66,9 @@ def _parse_lengths(lengths, b, t, s):
     if not flat_pair and not per_item:
         raise ValueError("lengths must have shape [B, 2] (or [2] for a single item)")
     arr = arr.reshape(b, 2)
-    for i in range(b):
-        lt, ls = int(arr[i, 0]), int(arr[i, 1])
-        if lt < 0 or ls < 0 or lt > t or ls > s:
-            raise ValueError(f"item {i}: lengths must lie in [0, T] x [0, S]")
+    bad = (arr[:, 0] < 0) | (arr[:, 1] < 0) | (arr[:, 0] > t) | (arr[:, 1] > s)
+    if bad.any():  # the lowest failing item, as the binding's loop reports it
+        raise ValueError(f"item {int(np.argmax(bad))}: lengths must lie in [0, T] x [0, S]")
     return np.ascontiguousarray(arr.astype(np.uint32))
 
 
@@ -137,13 +136,20 @@ def _run_device(values, lens, cfg, b, t, s, want_out, want_paths, want_dur=False
     paths = torch.empty((b, s), dtype=torch.int32, device=dev) if want_paths else None
     dur = torch.empty((b, t), dtype=torch.int32, device=dev) if want_dur else None
     err = _lib.MasError()
-    with torch.cuda.device(dev):
+
+    def call():
         stream = torch.cuda.current_stream(dev)
-        rc = lib.mas_align_device_ex(
+        return lib.mas_align_device_ex(
             values.data_ptr(), pitch, b, t, s, None if lens is None else lens.ctypes.data,
             ctypes.byref(cfg), None if out is None else out.data_ptr(),
             None if paths is None else paths.data_ptr(), None if dur is None else dur.data_ptr(),
-            ctypes.c_void_p(stream.cuda_stream), ctypes.byref(err))
+            stream.cuda_stream, ctypes.byref(err))
+
+    if dev.index == torch.cuda.current_device():
+        rc = call()  # (a device switch costs more than the rest of the wrapper)
+    else:
+        with torch.cuda.device(dev):
+            rc = call()
     _lib.raise_for(rc, err)
     return out, paths, dur
 
