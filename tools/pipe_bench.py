@@ -24,6 +24,7 @@ for name, pipe in (("plain", False), ("pipelined", True)):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / K
     res[name] = {"ms_per_step": round(ms, 4), "gcells": round(B * T * S / ms / 1e6, 1)}
+    res[name]["geometry"] = plan.geometry
     ref = m.align(q)
     assert torch.equal(outs[0], ref) and torch.equal(outs[1], ref), name
 print(json.dumps(res))
