@@ -166,6 +166,9 @@ class Reference:
         lib.ref_forward_parallel.restype = None
         lib.ref_forward_parallel.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int64, ctypes.c_float]
+        lib.ref_forward_reference.restype = None
+        lib.ref_forward_reference.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                              ctypes.c_int64, ctypes.c_float, ctypes.c_void_p]
         lib.ref_batch_create.restype = ctypes.c_void_p
         lib.ref_batch_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint64]
         lib.ref_batch_destroy.restype = None
@@ -191,6 +194,15 @@ class Reference:
         self.lib.ref_forward_parallel(q.ctypes.data, T if t is None else t, S if s is None else s,
                                       S, ctypes.c_float(max_neg_val))
         return q
+
+    def forward_reference(self, q, max_neg_val=-1e32):
+        """reference::forward_reference of the 2-D item q: its QCache as [t, s]."""
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        T, S = q.shape
+        out = np.empty((T, S), np.float32)
+        self.lib.ref_forward_reference(q.ctypes.data, T, S, S, ctypes.c_float(max_neg_val),
+                                       out.ctypes.data)
+        return out
 
     def write_tensor(self, path, values, lengths=None):
         """io::write_tensor (tensor_io.cpp).  Returns (errc, message); -1 = ok."""

@@ -16,6 +16,7 @@
 //   oracle::best_paths                   include/monoalign/oracle.hpp:33
 //   io::write_tensor / io::read_tensor   include/monoalign/tensor_io.hpp:29-36
 //   parallel::forward_parallel           include/monoalign/parallel.hpp:17
+//   reference::forward_reference         include/monoalign/reference.hpp:33
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -27,6 +28,7 @@
 #include "monoalign/bench.hpp"
 #include "monoalign/oracle.hpp"
 #include "monoalign/parallel.hpp"
+#include "monoalign/reference.hpp"
 #include "monoalign/tensor_io.hpp"
 
 namespace {
@@ -133,6 +135,18 @@ void ref_forward_parallel(float* q, int t, int s, std::int64_t stride, float max
   monoalign::MasConfig cfg;
   cfg.max_neg_val = max_neg_val;
   monoalign::parallel::forward_parallel(monoalign::MutableLikelihoodView{q, t, s, stride}, cfg);
+}
+
+/// reference::forward_reference on one [t][s] item (row stride `stride`):
+/// the reference engine's QCache, copied to `out` [t][s] (reference.hpp:33).
+void ref_forward_reference(const float* q, int t, int s, std::int64_t stride, float max_neg_val,
+                           float* out) {
+  monoalign::MasConfig cfg;
+  cfg.max_neg_val = max_neg_val;
+  const monoalign::reference::QCache c =
+      monoalign::reference::forward_reference(monoalign::LikelihoodView{q, t, s, stride}, cfg);
+  for (int i = 0; i < t; ++i)
+    for (int j = 0; j < s; ++j) out[static_cast<std::size_t>(i) * s + j] = c.at(i, j);
 }
 
 unsigned ref_hardware_threads() { return std::thread::hardware_concurrency(); }

@@ -782,7 +782,100 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
   return MAS_OK;
 }
 
+// q's storage as the score export's store target: {columns, row groups of R
+// within an item, residue, item}, so a warp's {32, 32, R, 1} box clips at its
+// item's last row (a flat row map would spill into the next item, whose own
+// CTAs may already have written it).
+bool encode_scores_map4(float* q, int64_t pitch, int T_cap, int64_t S, int B, int R,
+                        CUtensorMap* m) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(T_cap / R),
+                              static_cast<cuuint64_t>(R), static_cast<cuuint64_t>(B)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(R * pitch * 4),
+                                 static_cast<cuuint64_t>(pitch * 4),
+                                 static_cast<cuuint64_t>(T_cap * pitch * 4)};
+  const cuuint32_t box[4] = {32, 32, static_cast<cuuint32_t>(R), 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, q, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
+
+namespace mas {
+
+// Score export (parallel::forward_parallel / reference::forward_reference)
+// through K1 with OUT = 1: the forward pass of the maximum-path call with
+// its Q values written back over q by TMA stores (8 B/cell, HBM-bound),
+// instead of mas_scores.cu's general kernel.  Needs the TMA layout K1 reads
+// (16-byte base, pitch % 4 == 0, text_cap % 4 == 0); returns
+// MAS_E_UNSUPPORTED without launching anything otherwise.
+int forward_scores_fwd4(float* d_values, int64_t pitch, int B, int T_cap, int S_cap,
+                        const uint32_t* lengths, int mode, float mnv, cudaStream_t stream,
+                        mas_error_t* err) {
+  if ((reinterpret_cast<uintptr_t>(d_values) & 15u) != 0 || (pitch & 3) != 0 || (T_cap & 3) != 0 ||
+      (pitch * 4) % 16 != 0)
+    return MAS_E_UNSUPPORTED;
+  std::vector<uint32_t> lens(static_cast<size_t>(B) * 2);
+  int t_max = 0;
+  for (int b = 0; b < B; ++b) {
+    lens[2 * b] = lengths ? lengths[2 * b] : static_cast<uint32_t>(T_cap);
+    lens[2 * b + 1] = lengths ? lengths[2 * b + 1] : static_cast<uint32_t>(S_cap);
+    if (lens[2 * b + 1] > 0) t_max = std::max<int>(t_max, static_cast<int>(lens[2 * b]));
+  }
+  if (fwd4_configure() != cudaSuccess) return MAS_E_UNSUPPORTED;
+  Geometry g;
+  if (!cached_geometry(B, std::max(t_max, 1), S_cap, &g)) return MAS_E_UNSUPPORTED;
+  CUtensorMap tm_in, tm_st;
+  if (!encode_map4(d_values, pitch, static_cast<int64_t>(B) * T_cap, S_cap, g.R, &tm_in) ||
+      !encode_scores_map4(d_values, pitch, T_cap, S_cap, B, g.R, &tm_st))
+    return MAS_E_UNSUPPORTED;
+  // workspace: lengths [B][2] | band links [B][bands-1][bnd_pitch] | ticket + progress
+  const int bnd_pitch = (S_cap + 31) & ~31;
+  // (sub-buffers 256-byte aligned: the band links are copied in 16-byte vectors and bulk copies)
+  const size_t len_bytes = (static_cast<size_t>(B) * 2 * sizeof(uint32_t) + 255) & ~size_t{255};
+  const size_t bnd_bytes =
+      g.bands > 1 ? static_cast<size_t>(B) * (g.bands - 1) * bnd_pitch * sizeof(float) : 0;
+  const size_t sync_bytes = g.bands > 1 ? (1 + static_cast<size_t>(B) * (g.bands - 1)) * sizeof(int) : 0;
+  char* ws = nullptr;
+  MAS_CUDA(pool_alloc(reinterpret_cast<void**>(&ws), len_bytes + bnd_bytes + sync_bytes, stream),
+           "forward_scores: workspace");
+  FwdArgs fa = {};
+  fa.lengths = reinterpret_cast<uint32_t*>(ws);
+  fa.bnd = g.bands > 1 ? reinterpret_cast<float*>(ws + len_bytes) : nullptr;
+  fa.ticket = g.bands > 1 ? reinterpret_cast<int*>(ws + len_bytes + bnd_bytes) : nullptr;
+  fa.progress = g.bands > 1 ? fa.ticket + 1 : nullptr;
+  fa.bnd_pitch = bnd_pitch;
+  fa.b0 = 0;
+  fa.T_pad = T_cap;
+  fa.M = g.M;
+  fa.T_alloc = g.T_alloc;
+  fa.K = g.K;
+  fa.W = g.W;
+  fa.N = g.N;
+  fa.mnv = mnv;
+  fa.row0_up = mode == 1 ? -std::numeric_limits<float>::infinity() : mnv;
+  fa.T_cap = T_cap;
+  fa.S_cap = S_cap;
+  fa.bands = g.bands;
+  fa.band_rows = g.band_rows;
+  fa.nb = B;
+  fa.one = 1u;
+  fa.scores = 1;
+  cudaError_t e = cudaMemcpyAsync(ws, lens.data(), lens.size() * sizeof(uint32_t),
+                                  cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess && sync_bytes)
+    e = cudaMemsetAsync(fa.ticket, 0, sync_bytes, stream);
+  if (e == cudaSuccess) e = launch_fwd4(g.R, mode, tm_in, tm_st, fa, B * g.bands, stream);
+  const cudaError_t f = cudaFreeAsync(ws, stream);
+  if (e == cudaSuccess) e = f;
+  MAS_CUDA(e, "forward_scores");
+  return MAS_OK;
+}
+
+}  // namespace mas
 
 extern "C" {
 

@@ -154,12 +154,20 @@ constexpr float kBitsBase = 8388608.0f;  // 2^23
 
 // Four columns (one LDS.128 per row residue, one of the FIFO slot) of the
 // DP for one warp.  U0 = index of the first column within the stage.
-template <int R, int MODE, bool GENERIC, int U0>
+// std::max(a, b) as the reference evaluates it: (a < b) ? b : a (the first
+// argument on ties, signed zeros and NaNs included) -- the score export's
+// arithmetic, where the table itself is the output.
+__device__ __forceinline__ float ref_max(float a, float b) { return a < b ? b : a; }
+
+// OUT 1 (score export): the same columns computed with ref_max and written
+// back over q in the stage (rows below the item's text length keep q), no
+// direction bits, no NonFinite fold.
+template <int R, int MODE, bool GENERIC, int U0, int OUT>
 __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uint32_t coff,
                                           const float4* __restrict__ slot, float (&ex)[kQuad],
                                           Lane4<R>& L, float (&wf)[R], bool is31, int srclane,
                                           int c_base, int nvalid, int row0, float mnv,
-                                          bool row0_is_zero) {
+                                          bool row0_is_zero, uint32_t live) {
   if (GENERIC && U0 >= nvalid) return false;
   float4 qv[R];
 #pragma unroll
@@ -167,27 +175,51 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
     qv[r] = *reinterpret_cast<const float4*>(tile + r * 4096 + coff);
   const float4 vv = slot[(U0 % kQuad) / 4];  // producer's bottom row
   const float bnds[4] = {L.vlast, vv.x, vv.y, vv.z};
+  float4 res[R];
+  if constexpr (OUT) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) res[r] = qv[r];
+  }
+  auto put_back = [&]() {
+    if constexpr (OUT) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (live & (1u << r))
+          *reinterpret_cast<float4*>(const_cast<uint8_t*>(tile) + r * 4096 + coff) = res[r];
+    }
+  };
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    if (GENERIC && U0 + e >= nvalid) return false;
+    if (GENERIC && U0 + e >= nvalid) {
+      put_back();
+      return false;
+    }
     float q[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) q[r] = e == 0 ? qv[r].x : e == 1 ? qv[r].y : e == 2 ? qv[r].z : qv[r].w;
     const float send = is31 ? bnds[e] : L.o[R - 1];
-    const float up = __shfl_sync(0xffffffffu, send, srclane);
-    switch ((U0 + e) % 16) {  // compile-time bit 15 - column-in-half-word
+    float up = __shfl_sync(0xffffffffu, send, srclane);
+    float n[R];
+    if constexpr (OUT) {
+      // reference.cpp:20-24: row 0 is a running sum (prev + q, not a max)
+      if (MODE == 1 && row0_is_zero) up = L.o[0];
+      n[0] = q[0] + ref_max(up, L.o[0]);
+#pragma unroll
+      for (int r = 1; r < R; ++r) n[r] = q[r] + ref_max(L.o[r - 1], L.o[r]);
+    } else {
+      switch ((U0 + e) % 16) {  // compile-time bit 15 - column-in-half-word
 #define MAS_B4(U)                   \
   case U:                           \
     bits4<R, 15 - U>(wf, up, L.o);  \
     break;
-      MAS_B4(0) MAS_B4(1) MAS_B4(2) MAS_B4(3) MAS_B4(4) MAS_B4(5) MAS_B4(6) MAS_B4(7)
-      MAS_B4(8) MAS_B4(9) MAS_B4(10) MAS_B4(11) MAS_B4(12) MAS_B4(13) MAS_B4(14) MAS_B4(15)
+        MAS_B4(0) MAS_B4(1) MAS_B4(2) MAS_B4(3) MAS_B4(4) MAS_B4(5) MAS_B4(6) MAS_B4(7)
+        MAS_B4(8) MAS_B4(9) MAS_B4(10) MAS_B4(11) MAS_B4(12) MAS_B4(13) MAS_B4(14) MAS_B4(15)
 #undef MAS_B4
-    }
-    float n[R];
-    n[0] = q[0] + fmaxf(up, L.o[0]);
+      }
+      n[0] = q[0] + fmaxf(up, L.o[0]);
 #pragma unroll
-    for (int r = 1; r < R; ++r) n[r] = q[r] + fmaxf(L.o[r - 1], L.o[r]);
+      for (int r = 1; r < R; ++r) n[r] = q[r] + fmaxf(L.o[r - 1], L.o[r]);
+    }
     if (GENERIC) {
       const int c = c_base + U0 + e;
       if (MODE == 1) {
@@ -196,17 +228,29 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
           if (c < row0 + r) n[r] = mnv;
       }
       if (c == 0) {  // first column: parallel.cpp:73-75 / reference.cpp:16-24
-        n[0] = row0_is_zero ? q[0] : mnv;
+        // (the reference engine's running sum starts at 0.f + q[0][0])
+        n[0] = row0_is_zero ? (OUT && MODE == 1 ? 0.f + q[0] : q[0]) : mnv;
 #pragma unroll
         for (int r = 1; r < R; ++r) n[r] = mnv;
       }
     }
+    if constexpr (!OUT) {
 #pragma unroll
-    for (int r = 0; r + 1 < R; r += 2) fold_abs_max_nan(L.acc[r / 2], q[r], q[r + 1]);
+      for (int r = 0; r + 1 < R; r += 2) fold_abs_max_nan(L.acc[r / 2], q[r], q[r + 1]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (e == 0) res[r].x = n[r];
+        if (e == 1) res[r].y = n[r];
+        if (e == 2) res[r].z = n[r];
+        if (e == 3) res[r].w = n[r];
+      }
+    }
     ex[(U0 % kQuad) + e] = n[R - 1];
 #pragma unroll
     for (int r = 0; r < R; ++r) L.o[r] = n[r];
   }
+  put_back();
   L.vlast = vv.w;
   return true;
 }
@@ -222,13 +266,13 @@ struct Probes {
   bool stage_ok, empty_ok;        // results
 };
 
-template <int R, int MODE, bool GENERIC, int K>
+template <int R, int MODE, bool GENERIC, int K, int OUT>
 __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (&coff)[8],
                                          const Fifo4& F, float (&ex)[kQuad], Lane4<R>& L,
                                          uint32_t (&w)[kChunks][R], bool& ready, bool more, bool is31,
                                          int lane, int srclane, int q, int c_base, int nvalid,
                                          int row0, float mnv, bool row0_is_zero,
-                                         Probes& P) {
+                                         Probes& P, uint32_t live) {
   if (GENERIC && K * kQuad >= nvalid) return false;
   const int fs = q & (kFifoSlots - 1);
   if (F.has_in && !ready) mbar_wait_all(F.full + 8u * fs, static_cast<uint32_t>(q / kFifoSlots) & 1u);
@@ -255,10 +299,11 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
       _Pragma("unroll") for (int r = 0; r < R; ++r) wf[r] = kBitsBase;                          \
     }                                                                                           \
     if (ok)                                                                                     \
-      ok = fwd4_group<R, MODE, GENERIC, U0>(stage + (U0 / kCols4) * chunk_bytes(R),            \
-                                            coff[(U0 / 4) & 7], slot, ex, L, wf, is31,          \
-                                            srclane, c_base, nvalid, row0, mnv, row0_is_zero);  \
-    if constexpr (U0 % 16 == 12) {                                                              \
+      ok = fwd4_group<R, MODE, GENERIC, U0, OUT>(stage + (U0 / kCols4) * chunk_bytes(R),       \
+                                                 coff[(U0 / 4) & 7], slot, ex, L, wf, is31,     \
+                                                 srclane, c_base, nvalid, row0, mnv,            \
+                                                 row0_is_zero, live);                           \
+    if constexpr (U0 % 16 == 12 && !OUT) {                                                      \
       _Pragma("unroll") for (int r = 0; r < R; ++r) {                                           \
         const uint32_t v = __float_as_uint(wf[r]) & 0xffffu;                                    \
         w[U0 / kCols4][r] |= U0 % kCols4 < 16 ? v << 16 : v;                                    \
@@ -283,19 +328,20 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
   return ok;
 }
 
-template <int R, int MODE, bool GENERIC>
+template <int R, int MODE, bool GENERIC, int OUT>
 __device__ __forceinline__ void fwd4_stage(const uint8_t* stage, const uint32_t (&coff)[8],
                                           const Fifo4& F, float (&ex)[kQuad], Lane4<R>& L,
                                           uint32_t (&w)[kChunks][R], bool& ready, bool more, bool is31,
                                           int lane, int srclane, int q0, int c_base, int nvalid,
                                           int row0, float mnv, bool row0_is_zero,
-                                          Probes& P) {
-  if (!fwd4_quad<R, MODE, GENERIC, 0>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane, q0,
-                                   c_base, nvalid, row0, mnv, row0_is_zero, P))
+                                          Probes& P, uint32_t live) {
+  if (!fwd4_quad<R, MODE, GENERIC, 0, OUT>(stage, coff, F, ex, L, w, ready, more, is31, lane,
+                                           srclane, q0, c_base, nvalid, row0, mnv, row0_is_zero,
+                                           P, live))
     return;
   if constexpr (kQuadsPerStage > 1)
-    fwd4_quad<R, MODE, GENERIC, 1>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
-                                   q0 + 1, c_base, nvalid, row0, mnv, row0_is_zero, P);
+    fwd4_quad<R, MODE, GENERIC, 1, OUT>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
+                                        q0 + 1, c_base, nvalid, row0, mnv, row0_is_zero, P, live);
 }
 
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
@@ -321,7 +367,15 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
 // and four epilogue warps (warps W+2..W+5, one per TMEM sub-partition) add
 // the row bias and write each 32-column tile into the compute warps' ring in
 // the layout TMA would have used.  The compute warps run unchanged.
-template <int R, int MODE, int SRC>
+//
+// OUT 1 (SRC 0 only): score export, parallel::forward_parallel /
+// reference::forward_reference (parallel.cpp:95-108, reference.cpp:9-36):
+// the compute warps write each stage's Q values back over q in the ring and
+// the producer lane TMA-stores the stage to tm_out (q's own storage, a 4-D
+// {columns, row groups, residues, items} map, so stores clip at the item's
+// last row) before refilling the slot.  No direction words, flags or zero
+// fill.
+template <int R, int MODE, int SRC, int OUT>
 __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     mas_fwd4_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tm_out,
                     const FwdArgs a) {
@@ -429,7 +483,7 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
   // the item's NonFinite flag starts at 0 (set by atomicOr only after the
   // cluster barrier below, and in the bands below after this band's
   // progress releases)
-  if (band_idx == 0 && crank == 0 && threadIdx.x == 0) a.flags[b] = 0;
+  if (!OUT && band_idx == 0 && crank == 0 && threadIdx.x == 0) a.flags[b] = 0;
   fence_proxy_async_smem();
   fence_mbar_init();
   cluster_sync_all();  // every CTA's FIFO / stage barriers exist before any use
@@ -687,6 +741,14 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
       const int orow = b * a.T_cap + i0w;
       const int l2a = a.l2_ahead;
       for (int m = 0; m < l2a && m < nit; ++m) tma_prefetch_3d(&tmq, m * kSC, group, 0);
+      // OUT: the stage's Q values go back to q's storage (this item's row
+      // groups i0w / R ..) before the slot is refilled
+      const int ogroup = i0w / R;
+      auto store_stage = [&](int mm) {
+        tma_store_4d(&tm_out,
+                     base + SL.ring + static_cast<uint32_t>((w * N + mm % N) * kStage4),
+                     mm * kSC, ogroup, 0, b);
+      };
       for (int m = 0; m < nit; ++m) {
         const int st = m % N;
         const uint32_t bar = base + SL.bars + static_cast<uint32_t>((w * N + st) * 8);
@@ -694,6 +756,10 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
           // stage st of warp w was consumed in iteration m - N
           const uint32_t eb = base + SL.ebars + static_cast<uint32_t>((w * N + st) * 8);
           mbar_wait(eb, (static_cast<uint32_t>(m / N) & 1u) ^ 1u);
+          if constexpr (OUT) {
+            store_stage(m - N);
+            bulk_store_drain();  // the store has read the slot
+          }
         }
         if (l2a > 0 && m + l2a < nit) tma_prefetch_3d(&tmq, (m + l2a) * kSC, group, 0);
         mbar_arrive_expect_tx(bar, kStage4);
@@ -705,6 +771,14 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
         if (zero_fill && m % kZStages == 0) tma_store_2d(&tm_out, zero_tile, m * kSC, orow);
       }
       if (zero_fill) bulk_store_drain();
+      if constexpr (OUT) {
+        for (int m = nit > N ? nit - N : 0; m < nit; ++m) {
+          mbar_wait(base + SL.ebars + static_cast<uint32_t>((w * N + m % N) * 8),
+                    static_cast<uint32_t>(m / N) & 1u);
+          store_stage(m);
+        }
+        bulk_store_complete();
+      }
     }
     __syncwarp();
     cluster_sync_all();
@@ -763,6 +837,9 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     const int row0 = i0 + R * lane;
     const bool row0_is_zero = row0 == 0;
     const uint32_t row0_mask = row0_is_zero ? 0u : 0xffffffffu;
+    uint32_t live_rows = 0;  // OUT: this lane's rows inside the item's text
+#pragma unroll
+    for (int r = 0; r < R; ++r) live_rows |= row0 + r < t_b ? 1u << r : 0u;
     const float mnv = a.mnv;
     Lane4<R> L;
 #pragma unroll
@@ -823,14 +900,17 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
         P.empty_ok = false;
       }
       if (generic) {
-        fwd4_stage<R, MODE, true>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
-                               kQuadsPerStage * m, c_base, nvalid, row0, mnv, row0_is_zero,
-                               P);
+        fwd4_stage<R, MODE, true, OUT>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
+                                       kQuadsPerStage * m, c_base, nvalid, row0, mnv,
+                                       row0_is_zero, P, live_rows);
       } else {
-        fwd4_stage<R, MODE, false>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
-                                kQuadsPerStage * m, c_base, kSC, row0, mnv, row0_is_zero,
-                                P);
+        fwd4_stage<R, MODE, false, OUT>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
+                                        kQuadsPerStage * m, c_base, kSC, row0, mnv, row0_is_zero,
+                                        P, live_rows);
       }
+      // OUT: the Q values written into the stage are read by the producer's
+      // TMA store (async proxy)
+      if constexpr (OUT) fence_proxy_async_smem();
       stage_ready = P.stage_ok;
       empty_ready = P.empty_ok || !P.arm_empty;
       // Every value of this stage and of this iteration's FIFO slots has been
@@ -842,6 +922,11 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
         if (has_in)
           st_async_b32(F.prev_sink, static_cast<uint32_t>(m),
                        F.prev_empty + 8u * static_cast<uint32_t>(m % kFifoIt4));
+      }
+      if constexpr (OUT) {
+        slot = slot + 1 == N ? 0 : slot + 1;
+        par ^= slot == 0 ? 1u : 0u;
+        continue;
       }
       // Row 0 and column -1 are stored as zero bits (the backtrack never
       // steps above row 0 or left of column 0).
@@ -867,7 +952,7 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
 #pragma unroll
     for (int r = 0; r < R / 2; ++r) nonfinite |= !(L.acc[r] < INFINITY);
     bad = bad && nonfinite;
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flags + b, 1);
+    if (!OUT && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flags + b, 1);
   }
   __syncwarp();
   cluster_sync_all();  // no CTA leaves while a peer may still write its FIFO
@@ -900,14 +985,16 @@ size_t fwd4_smem_bytes(int R, int W, int N, int Kp) {
 }
 
 namespace {
-template <int R, int MODE, int SRC>
+template <int R, int MODE, int SRC, int OUT>
 const void* fwd4_fn() {
-  return reinterpret_cast<const void*>(&mas_fwd4_kernel<R, MODE, SRC>);
+  return reinterpret_cast<const void*>(&mas_fwd4_kernel<R, MODE, SRC, OUT>);
 }
+// src 0: q from HBM, 1: Gaussian source, 2: q from HBM with score export
 const void* fwd4_fn(int R, int mode, int src = 0) {
   (void)R;  // four rows per lane
-  if (src) return mode == 0 ? fwd4_fn<4, 0, 1>() : fwd4_fn<4, 1, 1>();
-  return mode == 0 ? fwd4_fn<4, 0, 0>() : fwd4_fn<4, 1, 0>();
+  if (src == 1) return mode == 0 ? fwd4_fn<4, 0, 1, 0>() : fwd4_fn<4, 1, 1, 0>();
+  if (src == 2) return mode == 0 ? fwd4_fn<4, 0, 0, 1>() : fwd4_fn<4, 1, 0, 1>();
+  return mode == 0 ? fwd4_fn<4, 0, 0, 0>() : fwd4_fn<4, 1, 0, 0>();
 }
 }  // namespace
 
@@ -922,7 +1009,7 @@ cudaError_t fwd4_configure() {
   std::call_once(once[dev], [dev] {
     int smem_max = 0;
     cudaError_t r = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    for (int v = 0; v < 4 && r == cudaSuccess; ++v) {
+    for (int v = 0; v < 6 && r == cudaSuccess; ++v) {
       const void* fn = fwd4_fn(4, v & 1, v >> 1);
       r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
       if (r == cudaSuccess)
@@ -978,10 +1065,13 @@ cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorM
   cfg.numAttrs = a.pdl ? 2 : 1;
   if (R != 4) return cudaErrorInvalidValue;
   if (gauss)
-    return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0, 1>, tmq, tm_out, a)
-                     : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 1, 1>, tmq, tm_out, a);
-  return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0, 0>, tmq, tm_out, a)
-                   : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 1, 0>, tmq, tm_out, a);
+    return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0, 1, 0>, tmq, tm_out, a)
+                     : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 1, 1, 0>, tmq, tm_out, a);
+  if (a.scores)
+    return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0, 0, 1>, tmq, tm_out, a)
+                     : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 1, 0, 1>, tmq, tm_out, a);
+  return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0, 0, 0>, tmq, tm_out, a)
+                   : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 1, 0, 0>, tmq, tm_out, a);
 }
 
 }  // namespace mas

@@ -77,6 +77,7 @@ struct FwdArgs {
   const unsigned* bt_done;
   unsigned bt_need;
   int pdl;                  // launched with programmatic stream serialization
+  int scores;               // 1: score export (Q written over q through tm_out; no dirs/flags)
   uint32_t one;             // 1 and 0.0f passed at run time so ptxas keeps the
   float zero;               //   bit IMADs / NonFinite FFMAs on the FMA pipe
 };
@@ -112,6 +113,11 @@ cudaError_t launch_flag_nonfinite(const float* q, int64_t pitch, int rows_per_it
 int forward_scores_host_lengths(float* d_values, int64_t row_pitch, int32_t batch,
                                 int32_t rows_per_item, int32_t speech_cap, const uint32_t* lengths,
                                 float max_neg_val, cudaStream_t stream, mas_error_t* err);
+// mas_abi.cu: the score export through mas_fwd4 (OUT 1) when q's layout
+// suits its TMA maps; MAS_E_UNSUPPORTED (nothing launched) otherwise.
+int forward_scores_fwd4(float* d_values, int64_t pitch, int B, int T_cap, int S_cap,
+                        const uint32_t* lengths, int mode, float mnv, cudaStream_t stream,
+                        mas_error_t* err);
 size_t fwd4_smem_bytes(int R, int W, int N, int Kp = 0);
 struct GaussCfg {
   int gN, gstages, gacc;

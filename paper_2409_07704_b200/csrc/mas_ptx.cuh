@@ -122,6 +122,20 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
       : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+// 4-D tile store shared -> global (bulk-group completion).
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t src, int c0, int c1,
+                                             int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// Wait until every bulk store of this thread has been performed.
+__device__ __forceinline__ void bulk_store_complete() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
 // Wait until every bulk store of this thread has finished reading shared
 // memory (the CTA may not exit before that).
 __device__ __forceinline__ void bulk_store_drain() {

@@ -394,6 +394,11 @@ int forward_scores(float* d_values, int64_t row_pitch, int32_t batch, int32_t te
   int rc = check_table(row_pitch, batch, text_cap, speech_cap, lengths, err);
   if (rc != MAS_OK) return rc;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  // K1 with the score export (mas_fwd4.cu OUT 1) when q's layout suits TMA
+  rc = mas::forward_scores_fwd4(d_values, row_pitch, batch, text_cap, speech_cap, lengths, mode,
+                                max_neg_val, stream, err);
+  if (rc != MAS_E_UNSUPPORTED) return rc;
+  clear(err);
   const int nstrips = (text_cap + kStripRows - 1) / kStripRows;
   // Strips run concurrently (one CTA each, handing rows down through L2)
   // while the batch alone would not fill the GPU; otherwise each CTA walks
