@@ -414,7 +414,7 @@ def run_ours(args):
     scores_line = {"value": round(total_cells / (sc_best / 1e3) / 1e9, 2), "unit": "Gcells/s",
                    "ms_per_step": round(sc_best, 4), "bytes_per_cell": 8,
                    "path": "forward_parallel(torch CUDA tensor): the parallel engine's score "
-                           "table written in place (forward_scores_kernel)"}
+                           "table written in place (K1's export variant: Q stored over q by TMA)"}
     # ---- fused log-likelihood + MAS: q from the
     # Glow-TTS prior (C = 80 channels) computed on tcgen05 inside K1, never
     # written; against the unfused pipeline (gaussian_loglik writes q, then

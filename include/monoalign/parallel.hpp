@@ -13,8 +13,8 @@ MONOALIGN_API int pad_lanes(int t, LanePadding policy);
 
 /// In-place score table of the parallel engine (reference parallel.hpp:17,
 /// parallel.cpp:95-108), bit-identical; computed on the GPU
-/// (forward_scores_kernel via mas_forward_scores), the item round-tripping
-/// through device memory.
+/// (mas_forward_scores: the forward kernel's score export), the item
+/// round-tripping through device memory.
 MONOALIGN_API void forward_parallel(MutableLikelihoodView q, const MasConfig& cfg = {});
 
 /// Argmax walk over scores produced by forward_parallel (reference

@@ -308,8 +308,10 @@ def forward_parallel(values, lengths=None, max_neg_val=_DEFAULT_MAX_NEG_VAL):
     Bit-identical to the reference (std::max tie rule, signed zeros).  A torch
     CUDA float32 tensor is updated on its device (stream-ordered on the current
     stream); a numpy float32 C-contiguous array round-trips through the GPU and
-    is written back in place.  Computed by forward_scores_kernel
-    (csrc/mas_scores.cu); there is no host implementation."""
+    is written back in place.  Computed on the GPU by the forward kernel's
+    score export (csrc/mas_fwd4.cu OUT 1), or forward_scores_kernel
+    (csrc/mas_scores.cu) for layouts its TMA maps cannot take; there is no
+    host implementation."""
     import torch
 
     lib = _lib.load()

@@ -274,8 +274,8 @@ int pad_lanes(int t, LanePadding policy) {
 }
 
 void forward_parallel(MutableLikelihoodView q, const MasConfig& cfg) {
-  // The item round-trips through device memory; forward_scores_kernel
-  // computes the table (mas_forward_scores), nothing is computed here.
+  // The item round-trips through device memory; mas_forward_scores
+  // computes the table on the GPU, nothing is computed here.
   if (q.text < 1 || q.speech < 1) return;
   DeviceScratch d(static_cast<std::size_t>(q.text) * q.speech * sizeof(float));
   float* dq = d.as<float>();
