@@ -278,6 +278,21 @@ MAS_API int mas_align_gaussian_device(const float* d_z, const float* d_mean,
                                       const uint32_t* lengths, const mas_config_t* cfg,
                                       uint8_t* d_out, int32_t* d_paths, int32_t* d_durations,
                                       void* stream, mas_error_t* err);
+/* Enqueue-only form for training loops (a plan, like mas_plan_create): the
+ * operand workspace and validation once, then per batch the operand prep and
+ * the fused kernels only, no host synchronisation (CUDA-graph capturable).
+ * mas_plan_finish(plan, NULL, ...) reports validation / NonFinite errors of
+ * the last enqueue (a flagged item materialises q to locate the cell).
+ * MAS_E_UNSUPPORTED where mas_align_gaussian_device would materialise q
+ * (texts taller than 4096 rows, NaN sentinels of the parallel engine).
+ * Destroy with mas_plan_destroy.  (ABI 3) */
+MAS_API int mas_plan_create_gaussian(int32_t batch, int32_t channels, int32_t text_cap,
+                                     int32_t speech_cap, const uint32_t* lengths,
+                                     const mas_config_t* cfg, mas_plan_t** plan,
+                                     mas_error_t* err);
+MAS_API int mas_plan_enqueue_gaussian(mas_plan_t* plan, const float* d_z, const float* d_mean,
+                                      const float* d_logstd, uint8_t* d_out, int32_t* d_paths,
+                                      int32_t* d_durations, void* stream, mas_error_t* err);
 
 /* ---- MASTENS v1 tensor files (tensor_io.hpp:11-23, tensor_io.cpp) --------
  * Host-only.  Errors are MAS_E_IO with the reference's IoError code and text

@@ -8,6 +8,7 @@ through its C-ABI (include/monoalign_b200.h).  There is no CPU fallback.
 """
 
 from .api import (
+    GaussianPlan,
     Plan,
     __version__,
     _align_unchecked,
@@ -34,6 +35,7 @@ __all__ = [
     "forward_parallel",
     "gaussian_loglik",
     "Plan",
+    "GaussianPlan",
     "read_tensor",
     "write_tensor",
 ]

@@ -122,6 +122,12 @@ _SIGS = {
                                                  ctypes.c_int32, ctypes.c_int32, _VP,
                                                  ctypes.POINTER(MasConfig), _VP, _VP, _VP, _VP,
                                                  ctypes.POINTER(MasError)]),
+    "mas_plan_create_gaussian": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                ctypes.c_int32, _VP, ctypes.POINTER(MasConfig),
+                                                ctypes.POINTER(ctypes.c_void_p),
+                                                ctypes.POINTER(MasError)]),
+    "mas_plan_enqueue_gaussian": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+                                                 ctypes.POINTER(MasError)]),
     "mas_errc_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "mas_abi_version": (ctypes.c_int, []),
 }

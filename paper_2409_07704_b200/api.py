@@ -426,6 +426,71 @@ def align_gaussian(z, mean, logstd, lengths=None, engine="parallel",
     return res
 
 
+class GaussianPlan:
+    """Enqueue-only form of align_gaussian for training loops
+    (mas_plan_create_gaussian / mas_plan_enqueue_gaussian): validation and
+    the operand workspace once, then per batch the operand prep and the fused
+    kernels only -- no host synchronisation, CUDA-graph capturable.  finish()
+    reports the last enqueue's validation / NonFinite errors as align does.
+    Texts taller than 4096 rows and NaN sentinels of the parallel engine are
+    refused (ValueError / RuntimeError); align_gaussian handles them."""
+
+    def __init__(self, b, c, t, s, lengths=None, engine="parallel",
+                 max_neg_val=_DEFAULT_MAX_NEG_VAL, unchecked=False):
+        lib = _lib.load()
+        self._lib = lib
+        self.b, self.c, self.t, self.s = b, c, t, s
+        lens = None if lengths is None else _parse_lengths(lengths, b, t, s)
+        self._lens = lens
+        cfg = _make_config(engine, max_neg_val, 0, unchecked)
+        handle = ctypes.c_void_p()
+        err = _lib.MasError()
+        rc = lib.mas_plan_create_gaussian(b, c, t, s, None if lens is None else lens.ctypes.data,
+                                          ctypes.byref(cfg), ctypes.byref(handle),
+                                          ctypes.byref(err))
+        _lib.raise_for(rc, err)
+        self._h = handle
+
+    def enqueue(self, z, mean, logstd, out=None, paths=None, durations=None, stream=None):
+        """z [B, C, S], mean / logstd [B, C, T] float32 CUDA tensors (the plan's
+        shape); writes any of out [B,T,S] uint8, paths [B,S] int32, durations
+        [B,T] int32 (device tensors)."""
+        import torch
+
+        z, mean, logstd, B, C, T, S = _gauss_inputs(z, mean, logstd)
+        if (B, C, T, S) != (self.b, self.c, self.t, self.s):
+            raise ValueError(f"inputs are [B={B}, C={C}, T={T}, S={S}], the plan "
+                             f"[{self.b}, {self.c}, {self.t}, {self.s}]")
+        err = _lib.MasError()
+        st = torch.cuda.current_stream() if stream is None else stream
+        rc = self._lib.mas_plan_enqueue_gaussian(
+            self._h, z.data_ptr(), mean.data_ptr(), logstd.data_ptr(),
+            None if out is None else out.data_ptr(), None if paths is None else paths.data_ptr(),
+            None if durations is None else durations.data_ptr(), ctypes.c_void_p(st.cuda_stream),
+            ctypes.byref(err))
+        _lib.raise_for(rc, err)
+
+    def finish(self, stream=None):
+        import torch
+
+        err = _lib.MasError()
+        st = torch.cuda.current_stream() if stream is None else stream
+        rc = self._lib.mas_plan_finish(self._h, None, ctypes.c_void_p(st.cuda_stream),
+                                       ctypes.byref(err))
+        _lib.raise_for(rc, err)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.mas_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Plan:
     """Enqueue-only execution of the maximum-path call on device buffers
     (mas_plan_* in include/monoalign_b200.h): validation and workspace once,

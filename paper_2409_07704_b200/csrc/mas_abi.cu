@@ -387,6 +387,11 @@ struct mas_plan {
   int gauss_kp = 0;
   const mas::GaussOperands* gauss = nullptr;
   const CUtensorMap* gauss_map = nullptr;
+  // Gaussian plans (mas_plan_create_gaussian): the operands they own
+  int channels = 0;
+  void* gauss_ws = nullptr;
+  mas::GaussOperands gauss_own = {};
+  CUtensorMap gauss_tmb;
 };
 
 extern "C" {
@@ -430,6 +435,7 @@ void mas_plan_destroy(mas_plan_t* p) {
   cudaFreeAsync(p->d_locate, st);
   if (p->d_bnd) cudaFreeAsync(p->d_bnd, st);
   if (p->d_sync) cudaFreeAsync(p->d_sync, st);
+  if (p->gauss_ws) cudaFreeAsync(p->gauss_ws, st);
   if (p->ws_ready) cudaEventDestroy(p->ws_ready);
   cudaSetDevice(prev);
   delete p;
@@ -932,6 +938,30 @@ int mas_plan_finish(mas_plan_t* p, const float* d_values, void* stream_v, mas_er
   const int limit = p->first_host_error.item >= 0
                         ? std::max(0, std::min(p->B, p->first_host_error.item - p->item_base))
                         : p->B;
+  // Gaussian plans: q exists only as tiles inside the forward kernel; a
+  // flagged item materialises it (error path only) from the operands of the
+  // last enqueue for the exact row-major location.
+  float* q_tmp = nullptr;
+  struct QTmp {
+    float*& q;
+    cudaStream_t s;
+    ~QTmp() {
+      if (q) cudaFreeAsync(q, s);
+    }
+  } q_guard{q_tmp, stream};
+  if (p->gauss_ws && !d_values) {
+    bool any = false;
+    for (int b = 0; b < limit; ++b) any = any || flags[b] != 0;
+    if (any) {
+      MAS_CUDA(mas::pool_alloc(reinterpret_cast<void**>(&q_tmp),
+                               static_cast<size_t>(p->B) * p->T_pad * p->pitch * sizeof(float),
+                               stream),
+               "pool_alloc(q)");
+      MAS_CUDA(mas::gauss_q(p->gauss_own, p->B, p->T, p->S, q_tmp, p->pitch, stream),
+               "gaussian q");
+      d_values = q_tmp;
+    }
+  }
   for (int b = 0; b < limit; ++b) {
     if (!flags[b]) continue;
     // Conservative device flag: confirm and locate exactly (row-major first).
@@ -1548,6 +1578,75 @@ int mas_generate_device(uint64_t seed, int32_t batch, int32_t text_cap, int32_t 
 
 extern "C" {
 
+int mas_plan_create_gaussian(int32_t batch, int32_t channels, int32_t text_cap,
+                             int32_t speech_cap, const uint32_t* lengths, const mas_config_t* cfg,
+                             mas_plan_t** plan_out, mas_error_t* err) {
+  clear_error(err);
+  if (plan_out) *plan_out = nullptr;
+  if (!plan_out) return set_error(err, MAS_E_VALIDATION, -1, -1, "plan_out is null");
+  if (channels < 1 || batch < 1 || text_cap < 1 || speech_cap < 1)
+    return set_error(err, MAS_E_VALIDATION, MAS_ERRC_ZERO_DIM, -1,
+                     "every dimension must be at least 1");
+  if (channels > mas::kGaussMaxChannels)
+    return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
+                     "gaussian log-likelihood: at most " + std::to_string(mas::kGaussMaxChannels) +
+                         " channels");
+  mas_config_t c;
+  if (cfg)
+    c = *cfg;
+  else
+    mas_config_default(&c);
+  if ((c.flags & MAS_FLAG_UNCHECKED) && std::isnan(c.max_neg_val) && c.engine == MAS_ENGINE_PARALLEL)
+    return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
+                     "gaussian plans: NaN sentinels of the parallel engine need the score table "
+                     "(use mas_align_gaussian_device)");
+  const int kp = mas::gauss_kp(channels);
+  uint32_t t_max = 0;
+  for (int32_t b = 0; lengths && b < batch; ++b)
+    if (lengths[2 * b] <= static_cast<uint32_t>(text_cap)) t_max = std::max(t_max, lengths[2 * b]);
+  if (!lengths) t_max = static_cast<uint32_t>(text_cap);
+  Geometry probe;
+  if (!cached_geometry(batch, std::max<int>(static_cast<int>(t_max), 1), speech_cap, &probe, kp))
+    return set_error(err, MAS_E_UNSUPPORTED, -1, -1,
+                     "gaussian plans: the text does not fit one cluster of the fused kernel "
+                     "(use mas_align_gaussian_device)");
+  c.flags &= ~MAS_FLAG_PIPELINED;
+  mas_plan_t* p = nullptr;
+  int rc = plan_create(batch, text_cap, speech_cap, speech_cap, lengths, &c, 0, &p, err, false, kp);
+  if (rc) return rc;
+  cudaStream_t st = cudaStreamPerThread;
+  cudaError_t e = mas::gauss_alloc(batch, channels, text_cap, speech_cap, st, &p->gauss_own,
+                                   &p->gauss_ws);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess &&
+      !mas::encode_gauss_b_map(p->gauss_own.B, static_cast<int64_t>(batch) * p->gauss_own.Sp,
+                               p->gauss_own.Kp, &p->gauss_tmb,
+                               mas::gauss_cfg(p->geo.W, p->gauss_own.Kp).gN))
+    e = cudaErrorInvalidValue;
+  if (e != cudaSuccess) {
+    mas_plan_destroy(p);
+    return cuda_error(err, e, "gaussian plan workspace");
+  }
+  p->channels = channels;
+  p->gauss = &p->gauss_own;
+  p->gauss_map = &p->gauss_tmb;
+  *plan_out = p;
+  return MAS_OK;
+}
+
+int mas_plan_enqueue_gaussian(mas_plan_t* p, const float* d_z, const float* d_mean,
+                              const float* d_logstd, uint8_t* d_out, int32_t* d_paths,
+                              int32_t* d_durations, void* stream_v, mas_error_t* err) {
+  clear_error(err);
+  if (!p || !p->gauss_ws)
+    return set_error(err, MAS_E_VALIDATION, -1, -1, "not a gaussian plan (mas_plan_create_gaussian)");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  MAS_CUDA(mas::gauss_prep(d_z, d_mean, d_logstd, p->B, p->channels, p->T, p->S, p->gauss_own,
+                           stream),
+           "gaussian operands");
+  return mas_plan_enqueue_ex(p, MAS_PART_ALL, nullptr, d_out, d_paths, d_durations, stream_v, err);
+}
+
 int mas_align_gaussian_device(const float* d_z, const float* d_mean, const float* d_logstd,
                               int32_t batch, int32_t channels, int32_t text_cap,
                               int32_t speech_cap, const uint32_t* lengths, const mas_config_t* cfg,
@@ -1604,50 +1703,16 @@ int mas_align_gaussian_device(const float* d_z, const float* d_mean, const float
     return rc;
   }
   mas_plan_t* plan = nullptr;
-  int rc = plan_create(batch, text_cap, speech_cap, speech_cap, lengths, &c, 0, &plan, err, true,
-                       mas::gauss_kp(channels));
+  int rc = mas_plan_create_gaussian(batch, channels, text_cap, speech_cap, lengths, &c, &plan, err);
   if (rc) return rc;
   plan->internal = true;
-  mas::GaussOperands g;
-  void* ws = nullptr;
-  CUtensorMap tmb;
-  cudaError_t e = mas::gauss_alloc(batch, channels, text_cap, speech_cap, stream, &g, &ws);
-  if (e == cudaSuccess)
-    e = mas::gauss_prep(d_z, d_mean, d_logstd, batch, channels, text_cap, speech_cap, g, stream);
-  if (e == cudaSuccess &&
-      !mas::encode_gauss_b_map(g.B, static_cast<int64_t>(batch) * g.Sp, g.Kp, &tmb,
-                               mas::gauss_cfg(plan->geo.W, g.Kp).gN))
-    e = cudaErrorInvalidValue;
-  if (e == cudaSuccess) {
-    plan->gauss = &g;
-    plan->gauss_map = &tmb;
-    rc = enqueue_items(plan, MAS_PART_ALL, 0, batch, nullptr, d_out, d_paths, d_durations, stream,
-                       err);
-    // NonFinite: the compute warps flag items whose q is not finite; only
-    // then is q materialised (error path) for the exact row-major location.
-    std::vector<int> flags(static_cast<size_t>(batch));
-    if (rc == MAS_OK &&
-        (e = cudaMemcpyAsync(flags.data(), plan->d_flags, sizeof(int) * batch,
-                             cudaMemcpyDeviceToHost, stream)) == cudaSuccess &&
-        (e = cudaStreamSynchronize(stream)) == cudaSuccess) {
-      float* q = nullptr;
-      bool any = false;
-      for (int f : flags) any = any || f != 0;
-      if (any) {
-        e = mas::pool_alloc(reinterpret_cast<void**>(&q),
-                            static_cast<size_t>(batch) * text_cap * speech_cap * sizeof(float), stream);
-        if (e == cudaSuccess) e = mas::gauss_q(g, batch, text_cap, speech_cap, q, speech_cap, stream);
-      }
-      if (e == cudaSuccess) rc = mas_plan_finish(plan, q, stream, err);
-      if (q) cudaFreeAsync(q, stream);
-    }
-  }
-  if (ws) cudaFreeAsync(ws, stream);
+  rc = mas_plan_enqueue_gaussian(plan, d_z, d_mean, d_logstd, d_out, d_paths, d_durations, stream_v,
+                                 err);
+  // NonFinite: the compute warps flag items whose q is not finite; only then
+  // is q materialised (error path) for the exact row-major location.
+  if (rc == MAS_OK) rc = mas_plan_finish(plan, nullptr, stream_v, err);
   cudaStreamSynchronize(stream);
-  plan->gauss = nullptr;
-  plan->gauss_map = nullptr;
   mas_plan_destroy(plan);
-  if (e != cudaSuccess) return cuda_error(err, e, "gaussian alignment");
   return rc;
 }
 

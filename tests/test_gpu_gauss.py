@@ -195,3 +195,75 @@ def test_fused_tall_text_falls_back_to_materialised_q(mas, cuda):
     exp = mas.align_paths(mas.gaussian_loglik(z, mean, logstd))
     assert torch.equal(got[0].cpu(), torch.as_tensor(exp[0]).cpu() if not hasattr(exp[0], "cpu")
                        else exp[0].cpu())
+
+
+@pytest.mark.parametrize("engine", ["parallel", "reference"])
+def test_gaussian_plan_reuse_and_graph(mas, cuda, engine):
+    """GaussianPlan: enqueue-only, reused over batches and captured in a CUDA
+    graph, equal to align_gaussian on every batch."""
+    import numpy as np
+    import torch
+
+    B, C, T, S = 3, 80, 257, 1000
+    rng = np.random.default_rng(5)
+    t = rng.integers(1, T + 1, B)
+    t[0] = T
+    s = np.maximum(t, rng.integers(1, S + 1, B))
+    lens = np.stack([t, s], 1)
+    plan = mas.GaussianPlan(B, C, T, S, lengths=lens, engine=engine)
+    out = torch.empty((B, T, S), dtype=torch.uint8, device="cuda")
+    paths = torch.empty((B, S), dtype=torch.int32, device="cuda")
+    dur = torch.empty((B, T), dtype=torch.int32, device="cuda")
+    for seed in (1, 2, 3):
+        z, mean, logstd = _inputs(B, C, T, S, seed=seed)
+        plan.enqueue(z, mean, logstd, out=out, paths=paths, durations=dur)
+        plan.finish()
+        exp = mas.align_gaussian(z, mean, logstd, lengths=lens, engine=engine,
+                                 outputs=("alignment", "paths", "durations"))
+        assert torch.equal(out, exp["alignment"]) and torch.equal(dur, exp["durations"])
+        for b in range(B):
+            assert torch.equal(paths[b, :s[b]], exp["paths"][b, :s[b]])
+    # graph capture: inputs updated in place between replays
+    z, mean, logstd = _inputs(B, C, T, S, seed=7)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        plan.enqueue(z, mean, logstd, out=out, stream=st)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        plan.enqueue(z, mean, logstd, out=out, stream=st)
+    for seed in (8, 9):
+        z2, m2, l2 = _inputs(B, C, T, S, seed=seed)
+        z.copy_(z2), mean.copy_(m2), logstd.copy_(l2)
+        g.replay()
+        torch.cuda.synchronize()
+        exp = mas.align_gaussian(z, mean, logstd, lengths=lens, engine=engine)["alignment"]
+        assert torch.equal(out, exp)
+    plan.close()
+
+
+def test_gaussian_plan_errors(mas, cuda):
+    import torch
+
+    z, mean, logstd = _inputs(3, 8, 40, 90, 4)
+    plan = mas.GaussianPlan(3, 8, 40, 90)
+    z[2, 1, 5] = float("inf")
+    out = torch.empty((3, 40, 90), dtype=torch.uint8, device="cuda")
+    plan.enqueue(z, mean, logstd, out=out)
+    with pytest.raises(ValueError, match=r"item 2: non-finite likelihood at \(0, 5\)"):
+        plan.finish()
+    with pytest.raises(ValueError):
+        plan.enqueue(z[:2], mean[:2], logstd[:2], out=out)
+    # lengths are checked as align checks them: ranges at construction,
+    # feasibility (t <= s) with the item's other errors at finish
+    with pytest.raises(ValueError, match="item 1"):
+        mas.GaussianPlan(2, 8, 40, 90, lengths=[[40, 90], [41, 90]])
+    bad = mas.GaussianPlan(2, 8, 40, 90, lengths=[[40, 90], [30, 20]])
+    bad.enqueue(*_inputs(2, 8, 40, 90, 5), out=out[:2])
+    with pytest.raises(ValueError, match="item 1"):
+        bad.finish()
+    # shapes the fused kernel cannot take are refused, not silently materialised
+    with pytest.raises((ValueError, RuntimeError)):
+        mas.GaussianPlan(1, 16, 4200, 4300)
+    with pytest.raises((ValueError, RuntimeError)):
+        mas.GaussianPlan(1, 16, 40, 90, max_neg_val=float("nan"), unchecked=True)

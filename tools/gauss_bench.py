@@ -35,18 +35,28 @@ def unfused():
     return q
 
 
+gplan = m.GaussianPlan(B, C, T, S)
+gout = torch.empty_like(out)
+
+
 def fused():
+    gplan.enqueue(z, mean, ls, out=gout)
+
+
+def fused_checked():
     return m.align_gaussian(z, mean, ls)
 
 
 # parity at this size (outside the timing)
 q = unfused(); torch.cuda.synchronize()
 a_unf = out.clone()
-a_fus = fused()["alignment"]
-assert torch.equal(a_unf, a_fus), "fused != unfused"
+a_fus = fused_checked()["alignment"]
+fused(); torch.cuda.synchronize()
+assert torch.equal(a_unf, a_fus) and torch.equal(a_unf, gout), "fused != unfused"
 del q
 t_unf = ev_time(unfused, reps)
 t_fus = ev_time(fused, reps)
+t_chk = ev_time(fused_checked, reps)
 t_q = ev_time(lambda: m.gaussian_loglik(z, mean, ls), reps)
 qq = m.gaussian_loglik(z, mean, ls)
 t_k12 = ev_time(lambda: plan.enqueue(qq, out), reps)
@@ -55,6 +65,7 @@ kp = ((2 * C + 63) // 64) * 64
 print(json.dumps({
     "shape": [B, C, T, S], "Kp": kp,
     "unfused_ms": round(t_unf, 4), "fused_ms": round(t_fus, 4),
+    "align_gaussian_checked_ms": round(t_chk, 4),
     "gaussian_loglik_ms": round(t_q, 4), "align_on_q_ms": round(t_k12, 4),
     "unfused_gcells": round(cells / t_unf / 1e6, 1), "fused_gcells": round(cells / t_fus / 1e6, 1),
     "speedup": round(t_unf / t_fus, 3),
