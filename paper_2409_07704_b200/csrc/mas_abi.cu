@@ -256,6 +256,9 @@ bool cached_geometry(int B, int t_max, int S_cap, Geometry* g, int kp = 0) {
         return e.ok;
       }
   }
+  // the occupancy queries need the kernels' shared-memory attributes set;
+  // a failed query must not be cached as "no geometry"
+  if (mas::fwd4_configure() != cudaSuccess) return false;
   const bool ok = choose_geometry(B, t_max, S_cap, g, kp);
   std::lock_guard<std::mutex> lk(mu);
   if (cache.size() >= 256) cache.erase(cache.begin());

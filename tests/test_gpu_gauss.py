@@ -267,3 +267,20 @@ def test_gaussian_plan_errors(mas, cuda):
         mas.GaussianPlan(1, 16, 4200, 4300)
     with pytest.raises((ValueError, RuntimeError)):
         mas.GaussianPlan(1, 16, 40, 90, max_neg_val=float("nan"), unchecked=True)
+
+
+def test_gaussian_plan_first_call_in_process(cuda):
+    """The geometry choice's occupancy queries need the forward kernels'
+    attributes set; a GaussianPlan (or align_gaussian) that is the process's
+    first call must still find the fused geometry (regression: it used to be
+    refused, and align_gaussian silently materialised q)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import paper_2409_07704_b200 as m; p = m.GaussianPlan(32, 80, 1024, 8192); "
+            "p.close(); print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
