@@ -400,6 +400,7 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
   // drawn by rank 0 in launch order (band-major) and shared over DSMEM.
   int cl = static_cast<int>(blockIdx.x) / a.K;
   if (a.bands > 1) {
+    cluster_sync_all();  // every peer CTA has started before its shared memory is written
     if (crank == 0 && threadIdx.x == 0) {
       const int t = atomicAdd(a.ticket, 1);
       for (int r = 0; r < a.K; ++r)
