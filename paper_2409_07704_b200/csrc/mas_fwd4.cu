@@ -47,8 +47,9 @@ constexpr int kCols4 = 32;  // columns per TMA box / direction word ("chunk")
 constexpr int kSC = 32;     // columns per stage (32 or 64)
 constexpr int kChunks = kSC / kCols4;   // chunks (direction words per row) per stage
 // The output's fused zero fill: one TMA store of a {kZCols, 32 R} uint8
-// zero box every kZCols / 32 stages (128-byte row segments: whole L2 lines,
-// a quarter of the scattered 32-byte writes a per-stage box would make).
+// zero box every kZCols / 32 stages (256-byte row segments: two whole L2
+// lines per row, an eighth of the scattered 32-byte writes a per-stage box
+// would make).
 constexpr int kZCols = kZeroCols;
 constexpr int kZStages = kZCols / kSC;
 constexpr int kBandPub = 4;  // quads per band-progress publication
