@@ -288,20 +288,6 @@ bool encode_map4(const float* q, int64_t pitch, int64_t rows_total, int64_t S, i
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// The uint8 output as {columns, rows} with kZeroCols x 32R boxes
-// (mas_fwd4.cu's fused zero fill).
-bool encode_out_map4(uint8_t* out, int64_t rows, int64_t S, int R, CUtensorMap* m) {
-  EncodeTiledFn enc = get_encode_fn();
-  if (!enc) return false;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(rows)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(S)};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(mas::kZeroCols),
-                             static_cast<cuuint32_t>(32 * R)};
-  const cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, out, dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 
 }  // namespace
 
@@ -372,11 +358,10 @@ struct mas_plan {
   float* d_bnd = nullptr; // bands: [B][bands-1][bnd_pitch] boundary rows
   cudaEvent_t ws_ready = nullptr;  // deferred plans: workspace set-up recorded here
   // tensor maps of the last input / output buffers enqueued (reused)
-  CUtensorMap tm_in, tm_out;
+  CUtensorMap tm_in;
   const float* tm_in_ptr = nullptr;
   int64_t tm_in_pitch = 0;
   int tm_in_tpad = 0;
-  const uint8_t* tm_out_ptr = nullptr;
   int* d_sync = nullptr;  // bands: tickets [B] (one per launch, at its first item) +
                           //        progress [B][bands-1]
   int bnd_pitch = 0;
@@ -704,32 +689,20 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     const double chain_s = p->S * 50.0 / 1.9e9 * std::max(1.0, warps / (4.0 * sms));
     const double stream_s = static_cast<double>(nb) * p->T * p->S * 4.125 / 5.9e12;
     const bool chain_bound = stream_s <= 1.1 * chain_s;
-    // The zero boxes are 32R rows tall on a flat [B*T] row map: with
-    // T % 32R != 0 an item's last box spills into the next item's first rows,
-    // harmless only when this launch owns the next item too (the whole batch;
-    // TMA clips past the end).  Chunked host calls run other chunks
-    // concurrently, so they fuse only row-aligned items.
-    const bool rows_own = (p->T % (32 * g.R)) == 0 || (b0 == 0 && nb == p->B);
+    // (each warp zeroes its own rows, so every row is covered only when every
+    // item is full length; the bulk stores need 16-byte rows)
     const bool fused_zero = d_out && chain_bound &&
-                            p->all_full && rows_own && (p->S % 16) == 0 &&
+                            p->all_full && (p->S % 16) == 0 &&
                             (reinterpret_cast<uintptr_t>(d_out) & 15u) == 0;
     const size_t item_bytes = static_cast<size_t>(p->T) * p->S;
     if (d_out && !fused_zero) {
       MAS_CUDA(cudaMemsetAsync(d_out + b0 * item_bytes, 0, nb * item_bytes, stream),
                "cudaMemsetAsync(out)");
     }
-    CUtensorMap tm_out;
+    CUtensorMap tm_out;  // (the score export's store map; unused here)
     std::memset(&tm_out, 0, sizeof(tm_out));
-    if (fused_zero && p->tm_out_ptr == d_out) {
-      tm_out = p->tm_out;
-    } else if (fused_zero &&
-               !encode_out_map4(d_out, static_cast<int64_t>(p->B) * p->T, p->S, g.R, &tm_out)) {
-      return set_error(err, MAS_E_CUDA, -1, -1, "cuTensorMapEncodeTiled(out) failed");
-    } else if (fused_zero) {
-      p->tm_out = tm_out;
-      p->tm_out_ptr = d_out;
-    }
     fa.zero_fill = fused_zero ? 1 : 0;
+    fa.out = d_out;
     fa.l2_ahead = 0;  // measured: an L2 prefetch lead beyond the ring only hurts
     fa.one = 1u;
     fa.zero = 0.0f;

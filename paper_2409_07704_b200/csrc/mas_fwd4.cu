@@ -46,12 +46,9 @@ namespace {
 constexpr int kCols4 = 32;  // columns per TMA box / direction word ("chunk")
 constexpr int kSC = 32;     // columns per stage (32 or 64)
 constexpr int kChunks = kSC / kCols4;   // chunks (direction words per row) per stage
-// The output's fused zero fill: one TMA store of a {kZCols, 32 R} uint8
-// zero box every kZCols / 32 stages (256-byte row segments: two whole L2
-// lines per row, an eighth of the scattered 32-byte writes a per-stage box
-// would make).
+// The output's fused zero fill: linear bulk stores of a {32 R rows x kZCols}
+// zero tile's bytes (LinearZero below).
 constexpr int kZCols = kZeroCols;
-constexpr int kZStages = kZCols / kSC;
 constexpr int kBandPub = 4;  // quads per band-progress publication
 __host__ __device__ constexpr int rows_of(int R) { return 32 * R; }
 __host__ __device__ constexpr int chunk_bytes(int R) { return rows_of(R) * kCols4 * 4; }
@@ -360,6 +357,42 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
                "r"(c0), "r"(c1), "r"(c2)
                : "memory");
 }
+
+// The output's fused zero fill as linear bulk stores: a warp's rows
+// [i0, i0 + rows) of item b are one contiguous range of the
+// [B][T_cap][S_cap] output, written in zero-tile-sized (32 KB) chunks spread
+// evenly over the item's nit stages.  Rows past T_cap belong to the next
+// item and are never written.  (The same DRAM time as {256 x 128} TMA boxes
+// of 256-byte row segments, r13, and no spill into the next item.)
+struct LinearZero {
+  uint8_t* dst = nullptr;
+  int64_t len = 0;
+  int nchunks = 0, next = 0, nit = 1;
+  static constexpr int kBytes = 128 * kZCols;  // the zero tile
+  __device__ LinearZero(const FwdArgs& a, int b, int i0, int rows_max, int nit_) : nit(nit_) {
+    if (!a.zero_fill || !a.out) return;
+    const int rows = min(rows_max, a.T_cap - i0);
+    if (rows <= 0) return;
+    dst = a.out + (static_cast<int64_t>(b) * a.T_cap + i0) * a.S_cap;
+    len = static_cast<int64_t>(rows) * a.S_cap;
+    nchunks = static_cast<int>((len + kBytes - 1) / kBytes);
+  }
+  // chunks due once stage m is issued (all of them by the last stage)
+  __device__ bool due(int m) const {
+    return next < nchunks && static_cast<int64_t>(next) * nit < static_cast<int64_t>(m + 1) * nchunks;
+  }
+  __device__ void issue_upto(int m, uint32_t zero_tile) {
+    while (due(m)) {
+      const int64_t off = static_cast<int64_t>(next) * kBytes;
+      const uint32_t bytes = static_cast<uint32_t>(len - off < kBytes ? len - off : kBytes);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + off),
+                   "r"(zero_tile), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      ++next;
+    }
+  }
+};
 
 // SRC 0: q streamed from HBM by TMA.  SRC 1: q computed in the CTA from the
 // Gaussian prior (mas_gauss.cu operands): tmq is then the map of the B
@@ -719,28 +752,28 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
         const int v = lane - 2;
         const int i0v = band + (crank * W + v) * kRows4;
         if (i0v < t_b) {
-          const int orow = b * a.T_cap + i0v;
+          LinearZero lz(a, b, i0v, kRows4, nit);
           for (int m = 0; m < nit; ++m) {
-            if (m % kZStages != 0) continue;
-            if (m >= N) {
+            if (!lz.due(m)) continue;
+            if (m >= N) {  // paced by the compute warp's ring
               const int st = m % N;
               mbar_wait(base + SL.ebars + static_cast<uint32_t>((v * N + st) * 8),
                         (static_cast<uint32_t>(m / N) & 1u) ^ 1u);
             }
-            tma_store_2d(&tm_out, base + SL.zero, m * kSC, orow);
+            lz.issue_upto(m, base + SL.zero);
           }
           bulk_store_drain();
         }
       }
     }
     if (SRC == 0 && w < W && s_b > 0 && i0w < t_b) {
+      LinearZero lz(a, b, i0w, kRows4, nit);
       prefetch_tensormap(&tmq);
       // evict_unchanged: evict_first re-read 8 % of q (r12, profiles/r12_l2_policy.md)
       const uint64_t pol_q = policy_evict_unchanged();
       const bool zero_fill = a.zero_fill != 0;
       const uint32_t zero_tile = base + SL.zero;
       const int group = (b * a.T_pad + i0w) / R;
-      const int orow = b * a.T_cap + i0w;
       const int l2a = a.l2_ahead;
       for (int m = 0; m < l2a && m < nit; ++m) tma_prefetch_3d(&tmq, m * kSC, group, 0);
       // OUT: the stage's Q values go back to q's storage (this item's row
@@ -770,7 +803,7 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
           tma_load_3d(base + SL.ring +
                           static_cast<uint32_t>((w * N + st) * kStage4 + c * chunk_bytes(R)),
                       &tmq, m * kSC + c * kCols4, group, 0, bar, pol_q);
-        if (zero_fill && m % kZStages == 0) tma_store_2d(&tm_out, zero_tile, m * kSC, orow);
+        if (zero_fill) lz.issue_upto(m, zero_tile);
       }
       if (zero_fill) bulk_store_drain();
       if constexpr (OUT) {

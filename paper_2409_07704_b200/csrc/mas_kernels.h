@@ -13,8 +13,7 @@ namespace mas {
 
 constexpr int kFifoSlots = 32;  // boundary-row FIFO depth, in quads
 constexpr int kMaxWarpsPerCta = 8;
-constexpr int kZeroCols = 256;  // mas_fwd4: columns per fused zero-fill TMA store (256-byte
-                                // row segments: c3 0.2794 -> 0.2771 ms, pipelined 0.2388 -> 0.2373)
+constexpr int kZeroCols = 256;  // mas_fwd4: zero tile {32 R rows x kZeroCols} (32 KB bulk stores)
 constexpr int kMaxClusterCtas = 16;
 
 // Stream-ordered device allocation from the library's own pool on the
@@ -52,7 +51,8 @@ struct FwdArgs {
   int N;                    // TMA stages per warp
   float mnv;                // max_neg_val
   float row0_up;            // value above row 0: mnv (parallel) / -inf (reference)
-  int zero_fill;            // 1: TMA-store zero tiles of the output (tm_out) as we go
+  int zero_fill;            // 1: zero the warps' rows of `out` as we go (linear bulk stores)
+  uint8_t* out;             // the output [B][T_cap][S_cap] (zero_fill)
   int T_cap, S_cap;         // output shape
   int l2_ahead;             // mas_fwd4: stages prefetched into L2 beyond the smem ring
   // mas_fwd4 bands (texts taller than one cluster): an item is `bands`
