@@ -257,6 +257,11 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
 // Look-ahead probes of the next stage's load and of the next iteration's
 // FIFO "empty" slot, made inside the first quad's straight-line block so
 // their results are consumed only after it (see fwd4_quad).
+template <bool V>
+struct BoolTag {
+  static constexpr bool value = V;
+};
+
 struct Probes {
   uint32_t stage_bar, stage_par;  // next stage's "loaded" barrier
   uint32_t empty_bar, empty_par;  // next iteration's consumer-slot barrier
@@ -360,7 +365,7 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
 
 // The output's fused zero fill as linear bulk stores: a warp's rows
 // [i0, i0 + rows) of item b are one contiguous range of the
-// [B][T_cap][S_cap] output, written in zero-tile-sized (32 KB) chunks spread
+// [B][T_cap][S_cap] output, written in zero-tile-sized (8 KB) chunks spread
 // evenly over the item's nit stages.  Rows past T_cap belong to the next
 // item and are never written.  (The same DRAM time as {256 x 128} TMA boxes
 // of 256-byte row segments, r13, and no spill into the next item.)
@@ -903,23 +908,27 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     };
     int slot = 0;
     uint32_t par = 0;
-    for (int m = 0; m < nit; ++m) {
+    // One 32-column stage.  GEN: the first stage, the reference engine's
+    // pinned prefix and a partial last stage take the generic code; every
+    // other stage runs the straight-line one in its own loop below, so the
+    // per-stage bookkeeping between fast stages is only the waits, the
+    // release (predicated, no branch) and the word store.
+    auto stage_body = [&](int m, auto gen_tag) {
+      constexpr bool GEN = decltype(gen_tag)::value;
       if (!stage_ready) mbar_wait_all(bar0 + 8u * slot, par);
       const uint8_t* stage = ring_ptr + slot * kStage4;
       const int c_base = m * kSC;
-      const int nvalid = s_b - c_base < kSC ? s_b - c_base : kSC;
+      const int nvalid = GEN ? (s_b - c_base < kSC ? s_b - c_base : kSC) : kSC;
       uint32_t w[kChunks][R];
 #pragma unroll
       for (int c = 0; c < kChunks; ++c)
 #pragma unroll
         for (int r = 0; r < R; ++r) w[c][r] = 0u;
-      const bool generic =
-          m == 0 || nvalid < kSC || (MODE == 1 && c_base < i0 + kRows4 - 1);
       if (has_out && m >= kFifoIt4 && !empty_ready) {
         // This iteration's slots in the consumer are free once it released
         // iteration m - kFifoIt4 (4-byte st.async on empty[m % kFifoIt4]).
         mbar_wait_all(my_empty + 8u * static_cast<uint32_t>(m % kFifoIt4),
-                  (static_cast<uint32_t>(m / kFifoIt4) & 1u) ^ 1u);
+                      (static_cast<uint32_t>(m / kFifoIt4) & 1u) ^ 1u);
       }
       const bool more = m + 1 < nit;
       Probes P;
@@ -934,15 +943,9 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
         P.stage_ok = false;
         P.empty_ok = false;
       }
-      if (generic) {
-        fwd4_stage<R, MODE, true, OUT>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
-                                       kQuadsPerStage * m, c_base, nvalid, row0, mnv,
-                                       row0_is_zero, P, live_rows);
-      } else {
-        fwd4_stage<R, MODE, false, OUT>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
-                                        kQuadsPerStage * m, c_base, kSC, row0, mnv, row0_is_zero,
-                                        P, live_rows);
-      }
+      fwd4_stage<R, MODE, GEN, OUT>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
+                                    kQuadsPerStage * m, c_base, nvalid, row0, mnv, row0_is_zero,
+                                    P, live_rows);
       // OUT: the Q values written into the stage are read by the producer's
       // TMA store (async proxy)
       if constexpr (OUT) fence_proxy_async_smem();
@@ -950,34 +953,42 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
       empty_ready = P.empty_ok || !P.arm_empty;
       // Every value of this stage and of this iteration's FIFO slots has been
       // consumed: hand the stage back to the producer warp and release the
-      // slots to the warp above.
+      // slots to the warp above (lane 0; predicated, no branch).
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_local(ebar0 + 8u * slot);
-        if (has_in)
-          st_async_b32(F.prev_sink, static_cast<uint32_t>(m),
-                       F.prev_empty + 8u * static_cast<uint32_t>(m % kFifoIt4));
-      }
-      if constexpr (OUT) {
-        slot = slot + 1 == N ? 0 : slot + 1;
-        par ^= slot == 0 ? 1u : 0u;
-        continue;
-      }
-      // Row 0 and column -1 are stored as zero bits (the backtrack never
-      // steps above row 0 or left of column 0).
-      {
-        const uint32_t col_mask = m == 0 ? 0x7fffffffu : 0xffffffffu;
+      mbar_arrive_local_if(lane == 0, ebar0 + 8u * slot);
+      st_async_b32_if(lane == 0 && has_in, F.prev_sink, static_cast<uint32_t>(m),
+                      F.prev_empty + 8u * static_cast<uint32_t>(m % kFifoIt4));
+      if constexpr (!OUT) {
+        // Row 0 and column -1 are stored as zero bits (the backtrack never
+        // steps above row 0 or left of column 0).
+        if (GEN && m == 0) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) w[0][r] &= col_mask;
-      }
+          for (int r = 0; r < R; ++r) w[0][r] &= 0x7fffffffu;
+        }
 #pragma unroll
-      for (int c = 0; c < kChunks; ++c) {
-        w[c][0] &= row0_mask;
-        if (c == 0 || m * kChunks + c < a.M) store_words(dirs_ptr + c * a.T_alloc, w[c]);
+        for (int c = 0; c < kChunks; ++c) {
+          w[c][0] &= row0_mask;
+          if (c == 0 || m * kChunks + c < a.M) store_words(dirs_ptr + c * a.T_alloc, w[c]);
+        }
+        dirs_ptr += kChunks * a.T_alloc;
       }
-      dirs_ptr += kChunks * a.T_alloc;
       slot = slot + 1 == N ? 0 : slot + 1;
       par ^= slot == 0 ? 1u : 0u;
+    };
+    // stages [mf0, mf1) take the fast code: after the first, past the
+    // reference engine's pinned cells (c_base >= i0 + kRows4 - 1), before a
+    // partial last stage
+    int mf0 = 1;
+    if (MODE == 1) mf0 = max(mf0, (i0 + kRows4 - 1 + kSC - 1) / kSC);
+    const int mf1 = s_b % kSC == 0 ? nit : nit - 1;
+    int m = 0;
+    while (m < nit) {
+      if (m >= mf0 && m < mf1) {
+        for (; m < mf1; ++m) stage_body(m, BoolTag<false>{});
+      } else {
+        stage_body(m, BoolTag<true>{});
+        ++m;
+      }
     }
     __syncwarp();
     bool bad = false;

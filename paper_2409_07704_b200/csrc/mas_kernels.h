@@ -13,7 +13,7 @@ namespace mas {
 
 constexpr int kFifoSlots = 32;  // boundary-row FIFO depth, in quads
 constexpr int kMaxWarpsPerCta = 8;
-constexpr int kZeroCols = 256;  // mas_fwd4: zero tile {32 R rows x kZeroCols} (32 KB bulk stores)
+constexpr int kZeroCols = 64;  // mas_fwd4: zero tile {32 R rows x kZeroCols} (8 KB bulk stores)
 constexpr int kMaxClusterCtas = 16;
 
 // Stream-ordered device allocation from the library's own pool on the
