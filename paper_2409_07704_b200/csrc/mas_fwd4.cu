@@ -278,7 +278,8 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
                                          Probes& P, uint32_t live) {
   if (GENERIC && K * kQuad >= nvalid) return false;
   const int fs = q & (kFifoSlots - 1);
-  if (F.has_in && !ready) mbar_wait_all(F.full + 8u * fs, static_cast<uint32_t>(q / kFifoSlots) & 1u);
+  mbar_wait_all_unless(!F.has_in || ready, F.full + 8u * fs,
+                       static_cast<uint32_t>(q / kFifoSlots) & 1u);
   const bool next = K + 1 < kQuadsPerStage ? (!GENERIC || (K + 1) * kQuad < nvalid) : more;
   const int q1 = q + 1;
   const uint32_t bar1 = F.full + 8u * (q1 & (kFifoSlots - 1));
@@ -915,7 +916,7 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     // release (predicated, no branch) and the word store.
     auto stage_body = [&](int m, auto gen_tag) {
       constexpr bool GEN = decltype(gen_tag)::value;
-      if (!stage_ready) mbar_wait_all(bar0 + 8u * slot, par);
+      mbar_wait_all_unless(stage_ready, bar0 + 8u * slot, par);
       const uint8_t* stage = ring_ptr + slot * kStage4;
       const int c_base = m * kSC;
       const int nvalid = GEN ? (s_b - c_base < kSC ? s_b - c_base : kSC) : kSC;
@@ -924,12 +925,11 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
       for (int c = 0; c < kChunks; ++c)
 #pragma unroll
         for (int r = 0; r < R; ++r) w[c][r] = 0u;
-      if (has_out && m >= kFifoIt4 && !empty_ready) {
-        // This iteration's slots in the consumer are free once it released
-        // iteration m - kFifoIt4 (4-byte st.async on empty[m % kFifoIt4]).
-        mbar_wait_all(my_empty + 8u * static_cast<uint32_t>(m % kFifoIt4),
-                      (static_cast<uint32_t>(m / kFifoIt4) & 1u) ^ 1u);
-      }
+      // This iteration's slots in the consumer are free once it released
+      // iteration m - kFifoIt4 (4-byte st.async on empty[m % kFifoIt4]).
+      mbar_wait_all_unless(!has_out || m < kFifoIt4 || empty_ready,
+                           my_empty + 8u * static_cast<uint32_t>(m % kFifoIt4),
+                           (static_cast<uint32_t>(m / kFifoIt4) & 1u) ^ 1u);
       const bool more = m + 1 < nit;
       Probes P;
       {

@@ -62,6 +62,23 @@ __device__ __forceinline__ void mbar_wait_all(uint32_t bar, uint32_t parity) {
   while (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
   }
 }
+// mbar_wait_all unless `skip` (warp-uniform: a vote result or a
+// warp-invariant flag), as ONE asm block: the compiler sees no branch, so
+// the hot loop carries no convergence barrier (BSSY/BSYNC) around the
+// rarely taken wait.
+__device__ __forceinline__ void mbar_wait_all_unless(bool skip, uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p, s;\n\t"
+      "setp.ne.b32 s, %2, 0;\n\t"
+      "@s bra.uni MAS_WAIT_DONE;\n\t"
+      "MAS_WAIT_LOOP:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "vote.sync.all.pred p, p, 0xffffffff;\n\t"
+      "@!p bra.uni MAS_WAIT_LOOP;\n\t"
+      "MAS_WAIT_DONE:\n\t}" ::"r"(bar),
+      "r"(parity), "r"(static_cast<int>(skip))
+      : "memory");
+}
 
 // Predicated forms (one guarded instruction instead of a branch around it:
 // the per-quad bookkeeping otherwise costs BSSY/ISETP/BRA per operation).
