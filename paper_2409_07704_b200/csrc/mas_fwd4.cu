@@ -283,11 +283,11 @@ __device__ __forceinline__ bool fwd4_quad(const uint8_t* stage, const uint32_t (
   const bool next = K + 1 < kQuadsPerStage ? (!GENERIC || (K + 1) * kQuad < nvalid) : more;
   const int q1 = q + 1;
   const uint32_t bar1 = F.full + 8u * (q1 & (kFifoSlots - 1));
-  if (lane == 0 && next && F.has_in) mbar_arrive_expect_tx(bar1, kSlot4);
+  mbar_arrive_expect_tx_if(lane == 0 && next && F.has_in, bar1, kSlot4);
   const bool probe = mbar_test_wait_all(bar1, static_cast<uint32_t>(q1 / kFifoSlots) & 1u);
   bool p_stage = false, p_empty = false;
   if (K == 0) {
-    if (P.arm_empty && is31) mbar_arrive_expect_tx(P.empty_bar, 4u);
+    mbar_arrive_expect_tx_if(P.arm_empty && is31, P.empty_bar, 4u);
     p_stage = mbar_test_wait_all(P.stage_bar, P.stage_par);
     p_empty = mbar_test_wait_all(P.empty_bar, P.empty_par);
   }
