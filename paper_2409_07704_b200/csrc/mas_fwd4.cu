@@ -984,6 +984,9 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     int m = 0;
     while (m < nit) {
       if (m >= mf0 && m < mf1) {
+        // two stages per iteration: half the loop-back branch resolutions
+        // (interleaved A/B: pipelined 0.2304 -> 0.2264 ms, plain 0.2711 -> 0.2701)
+#pragma unroll 2
         for (; m < mf1; ++m) stage_body(m, BoolTag<false>{});
       } else {
         stage_body(m, BoolTag<true>{});
