@@ -985,8 +985,11 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     while (m < nit) {
       if (m >= mf0 && m < mf1) {
         // two stages per iteration: half the loop-back branch resolutions
-        // (interleaved A/B: pipelined 0.2304 -> 0.2264 ms, plain 0.2711 -> 0.2701)
-#pragma unroll 2
+        // (interleaved A/B: pipelined 0.2304 -> 0.2264 ms, plain 0.2711 ->
+        // 0.2701); not for the Gaussian source or the score export, whose
+        // larger stage bodies then spill (K1g 331 -> 377 us, K1s 400 -> 417 us)
+        constexpr int kUnroll = SRC == 0 && OUT == 0 ? 2 : 1;
+#pragma unroll kUnroll
         for (; m < mf1; ++m) stage_body(m, BoolTag<false>{});
       } else {
         stage_body(m, BoolTag<true>{});
