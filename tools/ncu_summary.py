@@ -30,8 +30,11 @@ def launches(path, out):
     rows = list(csv.reader(l for l in open(path) if l.startswith('"')))
     h = rows[0]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = defaultdict(list)
     for r in rows[1:]:
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue  # (lists captured with extra metrics)
         name = r[ki].split("(")[0].replace("mas::<unnamed>::", "")
         v = float(r[vi].replace(",", ""))
         agg[name].append(v / 1000.0 if r[ui] == "ns" else v)
