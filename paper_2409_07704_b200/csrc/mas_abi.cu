@@ -594,6 +594,18 @@ namespace {
 
 // Enqueues the kernels (MAS_PART_* bits) for items [b0, b0 + nb) of the
 // plan's batch.  d_values / d_out / d_paths are the whole batch's buffers.
+// The one-launch tail (mas_fwd4.cu OUT 2) applies to a whole-batch enqueue of
+// a plain (not pipelined, not Gaussian, not NaN-sentinel) plan whose items
+// each fit one single-CTA cluster, when the direction words fit shared memory.
+bool tail_ok(const mas_plan_t* p, uint32_t parts, const uint8_t* d_out, const int32_t* d_paths,
+             const int32_t* d_dur) {
+  const Geometry& g = p->geo;
+  if (p->pipelined || p->gauss || p->nan_parallel || g.K != 1 || g.bands != 1) return false;
+  if ((parts & MAS_PART_ALL) != MAS_PART_ALL || !(d_out || d_paths || d_dur)) return false;
+  constexpr size_t kSmemMax = 227 * 1024;
+  return mas::fwd4_smem_bytes(g.R, g.W, g.N) + mas::fwd4_tail_bytes(g.R, g.W, g.M) <= kSmemMax;
+}
+
 int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_values,
                   uint8_t* d_out, int32_t* d_paths, int32_t* d_dur, cudaStream_t stream,
                   mas_error_t* err) {
@@ -729,6 +741,14 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
       fa.bt_need = p->bt_issued[p->dirs_par];
       fa.pdl = 1;
     }
+    // One launch for small batches: every item one single-CTA cluster (K = 1,
+    // one band) whose direction words fit shared memory beside the ring; the
+    // CTA then walks and expands its own item, and no backtrack kernel runs.
+    if (tail_ok(p, parts, d_out, d_paths, d_dur)) {
+      fa.tail = 1;
+      fa.path = d_paths;
+      fa.dur = d_dur;
+    }
     fa.ticket = p->d_sync ? p->d_sync + b0 : nullptr;
     fa.progress = p->d_sync ? p->d_sync + p->B : nullptr;
     // All bands of all items in one launch (clusters ordered by ticket).
@@ -742,7 +762,8 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
              "launch mas_fwd4");
     nfwd = 1;
   }
-  if ((parts & MAS_PART_BACKTRACK) && (d_out || d_paths || d_dur)) {
+  if ((parts & MAS_PART_BACKTRACK) && (d_out || d_paths || d_dur) &&
+      !tail_ok(p, parts, d_out, d_paths, d_dur)) {
     mas::BtArgs ba = {};
     ba.b0 = b0;
     ba.lengths = p->d_lengths;

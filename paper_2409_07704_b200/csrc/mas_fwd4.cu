@@ -59,7 +59,7 @@ constexpr int kQuadsPerStage = kSC / kQuad;
 constexpr int kFifoIt4 = kFifoSlots / kQuadsPerStage;  // FIFO depth in stages
 
 struct Smem4 {
-  uint32_t ring, bars, ebars, full, empty, sink, fifo, zero, ticket, total;
+  uint32_t ring, bars, ebars, full, empty, sink, fifo, zero, ticket, tbl, total;
   // Gaussian source (SRC 1): B operand stages, their barriers, TMEM slot
   uint32_t zst, zbars, tslot;
 };
@@ -70,7 +70,7 @@ constexpr int kGStages = 4;
 constexpr int kGAcc = 4;
 
 __host__ __device__ inline Smem4 smem4_layout(int R, int W, int N, int Kp = 0, int gstages = 0,
-                                              int gN = 0) {
+                                              int gN = 0, int tail_bytes = 0) {
   Smem4 L;
   L.ring = 0;
   L.bars = static_cast<uint32_t>(W * N * stage_bytes(R));
@@ -85,7 +85,10 @@ __host__ __device__ inline Smem4 smem4_layout(int R, int W, int N, int Kp = 0, i
   L.fifo = (L.sink + static_cast<uint32_t>((W + 1) * 16) + 127u) & ~127u;
   L.zero = L.fifo + static_cast<uint32_t>((W + 1) * kFifoSlots * kSlot4);
   L.ticket = L.zero + static_cast<uint32_t>(rows_of(R) * kZCols);  // after the uint8 zero tile
-  L.total = L.ticket + 16u;
+  // one-launch tail (OUT 2): the item's direction words, tail_bytes (see
+  // tail_bytes() below), 16-byte aligned
+  L.tbl = (L.ticket + 16u + 15u) & ~15u;
+  L.total = L.tbl + static_cast<uint32_t>(tail_bytes);
   L.zst = L.zbars = L.tslot = L.total;
   if (Kp > 0) {
     // zfull[kGStages] zfree[kGStages] dfull[kGAcc] dempty[kGAcc] aready, then the slot
@@ -400,6 +403,71 @@ struct LinearZero {
   }
 };
 
+// ---- one-launch tail (OUT 2, small batches) --------------------------------
+// Items that fit one single-CTA cluster (K = 1, one band) keep their
+// direction words in shared memory instead of global memory: word k of row i
+// at tbl[kTailGuard + k * rows + i] (rows = the CTA's W * 32R rows), then the
+// CTA walks and expands its own item after the forward pass, so the batch is
+// ONE launch (no backtrack kernel, no global round trip of the words).
+// Layout of the region: a guard of kTailGuard words (the walk's look-ahead
+// reads up to 4 rows below row 0 of word 0), the table, then the per-word
+// walk records rec_y[M], rec_ex[M].
+constexpr int kTailGuard = 16;
+__host__ __device__ inline int tail_bytes(int M, int rows) {
+  return (kTailGuard + M * rows + 2 * M) * 4;
+}
+
+// The backtrack (backtrack.hpp:21-32) over the shared-memory table, one
+// thread: the K2 walker's row-to-row steps (mas_bt.cu) without windows --
+// per 64-column word pair, exits are the lowest set bits of the bit-reversed
+// words, four branch-free steps per block; records each word's entry row and
+// exit mask.
+__device__ __noinline__ void tail_walk(const uint32_t* tbl, int rows, int t, int s, int* rec_y,
+                                       uint32_t* rec_ex) {
+  int y = t - 1;
+  int ml = (s - 1) >> 5;
+  // positions of the item's last word up to s - 1 (column s - 2)
+  uint32_t lim = 0xffffffffu << (31 - ((s - 1) & 31));
+  auto ld64 = [&](int k, int row, bool pair) -> uint64_t {
+    const uint64_t lo = tbl[k * rows + row];
+    return pair ? lo | (static_cast<uint64_t>(tbl[(k - 1) * rows + row]) << 32) : lo;
+  };
+  while (ml >= 0) {
+    if (y <= 0) {  // the walk reached row 0: the rest stays there
+      rec_y[ml] = 0;
+      rec_ex[ml] = 0u;
+      --ml;
+      continue;
+    }
+    const bool pair = ml > 0;
+    rec_y[ml] = y;
+    uint64_t x = ld64(ml, y, pair) & (static_cast<uint64_t>(0xffffffffu) << 32 | lim);
+    lim = 0xffffffffu;
+    uint64_t exw = 0;
+    int yy = y;
+    while (true) {
+#pragma unroll
+      for (int k = 1; k <= 4; ++k) {
+        const uint64_t d = x - 1u;
+        exw |= x & ~d;
+        x = ld64(ml, yy - k, pair) & ~(x ^ d);
+      }
+      yy -= 4;
+      if ((x & 0x7fffffffffffffffull) == 0u) break;
+    }
+    exw |= x;  // a pending exit at the pair's position 0
+    const int ex_lo = __popc(static_cast<uint32_t>(exw));
+    const int ex = ex_lo + __popc(static_cast<uint32_t>(exw >> 32));
+    rec_ex[ml] = static_cast<uint32_t>(exw);
+    if (pair) {
+      rec_ex[ml - 1] = static_cast<uint32_t>(exw >> 32);
+      rec_y[ml - 1] = y - ex_lo;
+    }
+    y -= ex;
+    ml -= pair ? 2 : 1;
+  }
+}
+
 // SRC 0: q streamed from HBM by TMA.  SRC 1: q computed in the CTA from the
 // Gaussian prior (mas_gauss.cu operands): tmq is then the map of the B
 // operand; the producer warp's lane 0 loads B stages, warp W+1 issues the
@@ -415,10 +483,16 @@ struct LinearZero {
 // {columns, row groups, residues, items} map, so stores clip at the item's
 // last row) before refilling the slot.  No direction words, flags or zero
 // fill.
+//
+// OUT 2 (SRC 0 only): the one-launch tail for items of one single-CTA
+// cluster: direction words to shared memory, then the CTA walks and expands
+// its own item (tail_walk), no backtrack kernel.
 template <int R, int MODE, int SRC, int OUT>
 __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
     mas_fwd4_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tm_out,
                     const FwdArgs a) {
+  constexpr int kExport = OUT == 1 ? 1 : 0;  // score export
+  constexpr bool kTail = OUT == 2;           // one-launch tail
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_addr(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -427,7 +501,8 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
   const int N = a.N;
   constexpr int kRows4 = rows_of(R);
   constexpr int kStage4 = stage_bytes(R);
-  const Smem4 SL = smem4_layout(R, W, N, SRC ? a.Kp : 0, SRC ? a.gstages : 0, SRC ? a.gN : 0);
+  const Smem4 SL = smem4_layout(R, W, N, SRC ? a.Kp : 0, SRC ? a.gstages : 0, SRC ? a.gN : 0,
+                                kTail ? tail_bytes(a.M, W * rows_of(R)) : 0);
   const int NB = a.gstages, NA = a.gacc;  // Gaussian source pipeline depths
   const int GN = a.gN;                    // frames per MMA (64 or 128)
   const int kGS = GN / umma::kStageN;     // K1 stages per MMA group
@@ -524,7 +599,7 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
   // the item's NonFinite flag starts at 0 (set by atomicOr only after the
   // cluster barrier below, and in the bands below after this band's
   // progress releases)
-  if (!OUT && band_idx == 0 && crank == 0 && threadIdx.x == 0) a.flags[b] = 0;
+  if (!kExport && band_idx == 0 && crank == 0 && threadIdx.x == 0) a.flags[b] = 0;
   fence_proxy_async_smem();
   fence_mbar_init();
   cluster_sync_all();  // every CTA's FIFO / stage barriers exist before any use
@@ -797,7 +872,7 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
           // stage st of warp w was consumed in iteration m - N
           const uint32_t eb = base + SL.ebars + static_cast<uint32_t>((w * N + st) * 8);
           mbar_wait(eb, (static_cast<uint32_t>(m / N) & 1u) ^ 1u);
-          if constexpr (OUT) {
+          if constexpr (kExport) {
             store_stage(m - N);
             bulk_store_drain();  // the store has read the slot
           }
@@ -811,8 +886,18 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
                       &tmq, m * kSC + c * kCols4, group, 0, bar, pol_q);
         if (zero_fill) lz.issue_upto(m, zero_tile);
       }
-      if (zero_fill) bulk_store_drain();
-      if constexpr (OUT) {
+      if (zero_fill) {
+        if constexpr (kTail) {
+          // the tail writes the ones into these rows: the zeros must be in
+          // memory (not only read out of shared memory) and visible to the
+          // generic proxy first
+          bulk_store_complete();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        } else {
+          bulk_store_drain();
+        }
+      }
+      if constexpr (kExport) {
         for (int m = nit > N ? nit - N : 0; m < nit; ++m) {
           mbar_wait(base + SL.ebars + static_cast<uint32_t>((w * N + m % N) * 8),
                     static_cast<uint32_t>(m / N) & 1u);
@@ -822,10 +907,18 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
       }
     }
     __syncwarp();
+    // one-launch tail: the compute warps expand only after this warp's zero
+    // fill is complete (named barrier 2: W compute warps + this warp)
+    if constexpr (kTail) asm volatile("bar.arrive 2, %0;" ::"r"((W + 1) * 32) : "memory");
     cluster_sync_all();
     return;
   }
 
+  // one-launch tail: the direction-word table (generic pointer into shared memory)
+  uint32_t* const tail_tbl = reinterpret_cast<uint32_t*>(sbase + SL.tbl) + kTailGuard;
+  const int tail_rows = W * kRows4;
+  (void)tail_tbl;
+  (void)tail_rows;
   const int g = crank * W + warp;
   const int i0 = band + g * kRows4;
   const bool has_in = g > 0 || fed;
@@ -943,12 +1036,12 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
         P.stage_ok = false;
         P.empty_ok = false;
       }
-      fwd4_stage<R, MODE, GEN, OUT>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
+      fwd4_stage<R, MODE, GEN, kExport>(stage, coff, F, ex, L, w, ready, more, is31, lane, srclane,
                                     kQuadsPerStage * m, c_base, nvalid, row0, mnv, row0_is_zero,
                                     P, live_rows);
       // OUT: the Q values written into the stage are read by the producer's
       // TMA store (async proxy)
-      if constexpr (OUT) fence_proxy_async_smem();
+      if constexpr (kExport) fence_proxy_async_smem();
       stage_ready = P.stage_ok;
       empty_ready = P.empty_ok || !P.arm_empty;
       // Every value of this stage and of this iteration's FIFO slots has been
@@ -958,7 +1051,7 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
       mbar_arrive_local_if(lane == 0, ebar0 + 8u * slot);
       st_async_b32_if(lane == 0 && has_in, F.prev_sink, static_cast<uint32_t>(m),
                       F.prev_empty + 8u * static_cast<uint32_t>(m % kFifoIt4));
-      if constexpr (!OUT) {
+      if constexpr (!kExport) {
         // Row 0 and column -1 are stored as zero bits (the backtrack never
         // steps above row 0 or left of column 0).
         if (GEN && m == 0) {
@@ -968,9 +1061,16 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
 #pragma unroll
         for (int c = 0; c < kChunks; ++c) {
           w[c][0] &= row0_mask;
-          if (c == 0 || m * kChunks + c < a.M) store_words(dirs_ptr + c * a.T_alloc, w[c]);
+          if constexpr (kTail) {
+            static_assert(R == 4, "the tail table stores four rows per lane");
+            const int k = m * kChunks + c;
+            *reinterpret_cast<uint4*>(tail_tbl + k * tail_rows + i0 + R * lane) =
+                make_uint4(w[c][0], w[c][1], w[c][2], w[c][3]);
+          } else {
+            if (c == 0 || m * kChunks + c < a.M) store_words(dirs_ptr + c * a.T_alloc, w[c]);
+          }
         }
-        dirs_ptr += kChunks * a.T_alloc;
+        if constexpr (!kTail) dirs_ptr += kChunks * a.T_alloc;
       }
       slot = slot + 1 == N ? 0 : slot + 1;
       par ^= slot == 0 ? 1u : 0u;
@@ -1004,9 +1104,66 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
 #pragma unroll
     for (int r = 0; r < R / 2; ++r) nonfinite |= !(L.acc[r] < INFINITY);
     bad = bad && nonfinite;
-    if (!OUT && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flags + b, 1);
+    if (!kExport && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flags + b, 1);
   }
   __syncwarp();
+  if constexpr (kTail) {
+    // ---- one-launch tail: walk and expand this CTA's item ----------------
+    // (every compute warp, live or not, takes part in the barriers)
+    const int nthr = W * 32;
+    const int tid = threadIdx.x;
+    int* const rec_y = reinterpret_cast<int*>(tail_tbl + a.M * tail_rows);
+    uint32_t* const rec_ex = reinterpret_cast<uint32_t*>(rec_y + a.M);
+    int32_t* const path = a.path ? a.path + static_cast<size_t>(b) * a.S_cap : nullptr;
+    int32_t* const dur = a.dur ? a.dur + static_cast<size_t>(b) * a.T_cap : nullptr;
+    uint8_t* const out = a.out ? a.out + static_cast<size_t>(b) * a.T_cap * a.S_cap : nullptr;
+    const bool any = t_b > 0 && s_b > 0;
+    // durations buffer first holds each row's last column (-1 before column 0)
+    if (dur)
+      for (int i = tid; i < a.T_cap; i += nthr) dur[i] = any ? -1 : 0;
+    if (path)
+      for (int j = (any ? s_b : 0) + tid; j < a.S_cap; j += nthr) path[j] = -1;
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");  // the table is complete
+    if (any && tid == 0 && s_b > 1) tail_walk(tail_tbl, tail_rows, t_b, s_b, rec_y, rec_ex);
+    // the zeros are in memory (producer warp, barrier 2) and the walk is done
+    asm volatile("bar.sync 2, %0;" ::"r"((W + 1) * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+    if (any) {
+      if (tid == 0) {  // backtrack.hpp:23-24: the last column is on the last row
+        if (path) path[s_b - 1] = t_b - 1;
+        if (out) out[static_cast<size_t>(t_b - 1) * a.S_cap + s_b - 1] = 1;
+        if (dur) dur[t_b - 1] = s_b - 1;
+      }
+      // word k covers columns 32k - 1 .. 32k + 30 (position p = column + 1 - 32k)
+      const int ktop = (s_b - 1) >> 5;
+      for (int k = warp; k <= ktop && s_b > 1; k += W) {
+        const int j = 32 * k + lane - 1;
+        const bool valid = j >= 0 && j <= s_b - 2;
+        const uint32_t rx = rec_ex[k];
+        const int row = rec_y[k] - __popc(rx << lane);
+        if (valid) {
+          if (path) path[j] = row;
+          if (out) out[static_cast<size_t>(row) * a.S_cap + j] = 1;
+          // an exit here: the row's last column
+          if (dur && ((rx >> (31 - lane)) & 1u)) dur[row] = j;
+        }
+      }
+    }
+    if (dur) {
+      asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+      if (warp == 0) {  // last columns -> durations: dur[r] = last[r] - last[r - 1], 0 past t
+        int carry = -1;
+        for (int r0 = 0; r0 < a.T_cap; r0 += 32) {
+          const int r = r0 + lane;
+          const int v = r < t_b ? dur[r] : 0;
+          const int up = __shfl_up_sync(0xffffffffu, v, 1);
+          const int prev = lane == 0 ? carry : up;
+          carry = __shfl_sync(0xffffffffu, v, 31);
+          if (r < a.T_cap) dur[r] = r < t_b ? v - prev : 0;
+        }
+      }
+    }
+  }
   cluster_sync_all();  // no CTA leaves while a peer may still write its FIFO
 }
 
@@ -1031,6 +1188,7 @@ GaussCfg gauss_cfg(int W, int Kp) {
   }
   return c;
 }
+size_t fwd4_tail_bytes(int R, int W, int M) { return static_cast<size_t>(tail_bytes(M, W * rows_of(R))); }
 size_t fwd4_smem_bytes(int R, int W, int N, int Kp) {
   const GaussCfg c = gauss_cfg(W, Kp);
   return smem4_layout(R, W, N, Kp, c.gstages, c.gN).total + 1024u;
@@ -1046,6 +1204,7 @@ const void* fwd4_fn(int R, int mode, int src = 0) {
   (void)R;  // four rows per lane
   if (src == 1) return mode == 0 ? fwd4_fn<4, 0, 1, 0>() : fwd4_fn<4, 1, 1, 0>();
   if (src == 2) return mode == 0 ? fwd4_fn<4, 0, 0, 1>() : fwd4_fn<4, 1, 0, 1>();
+  if (src == 3) return mode == 0 ? fwd4_fn<4, 0, 0, 2>() : fwd4_fn<4, 1, 0, 2>();
   return mode == 0 ? fwd4_fn<4, 0, 0, 0>() : fwd4_fn<4, 1, 0, 0>();
 }
 }  // namespace
@@ -1061,7 +1220,7 @@ cudaError_t fwd4_configure() {
   std::call_once(once[dev], [dev] {
     int smem_max = 0;
     cudaError_t r = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    for (int v = 0; v < 6 && r == cudaSuccess; ++v) {
+    for (int v = 0; v < 8 && r == cudaSuccess; ++v) {
       const void* fn = fwd4_fn(4, v & 1, v >> 1);
       r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
       if (r == cudaSuccess)
@@ -1099,7 +1258,8 @@ cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorM
   cfg.gridDim = dim3(static_cast<unsigned>(B * a.K), 1, 1);
   // + the producer warp (+ the MMA warp and four epilogue warps for the Gaussian source)
   cfg.blockDim = dim3(static_cast<unsigned>((a.W + 1 + (gauss ? 1 + 4 * a.W : 0)) * 32), 1, 1);
-  cfg.dynamicSmemBytes = fwd4_smem_bytes(R, a.W, a.N, a.Kp);
+  cfg.dynamicSmemBytes = fwd4_smem_bytes(R, a.W, a.N, a.Kp) +
+                         (a.tail ? static_cast<size_t>(tail_bytes(a.M, a.W * rows_of(R))) : 0);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1122,6 +1282,9 @@ cudaError_t launch_fwd4(int R, int mode, const CUtensorMap& tmq, const CUtensorM
   if (a.scores)
     return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0, 0, 1>, tmq, tm_out, a)
                      : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 1, 0, 1>, tmq, tm_out, a);
+  if (a.tail)
+    return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0, 0, 2>, tmq, tm_out, a)
+                     : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 1, 0, 2>, tmq, tm_out, a);
   return mode == 0 ? cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 0, 0, 0>, tmq, tm_out, a)
                    : cudaLaunchKernelEx(&cfg, mas_fwd4_kernel<4, 1, 0, 0>, tmq, tm_out, a);
 }

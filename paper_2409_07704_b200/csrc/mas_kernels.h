@@ -79,6 +79,10 @@ struct FwdArgs {
   unsigned bt_need;
   int pdl;                  // launched with programmatic stream serialization
   int scores;               // 1: score export (Q written over q through tm_out; no dirs/flags)
+  int tail;                 // 1: one-launch tail (K = 1, one band): words in shared memory,
+                            //    the CTA walks and expands its item (no backtrack kernel)
+  int32_t* path;            // tail outputs: [B][S_cap] path rows, [B][T_cap] durations (or null)
+  int32_t* dur;
   uint32_t one;             // 1 and 0.0f passed at run time so ptxas keeps the
   float zero;               //   bit IMADs / NonFinite FFMAs on the FMA pipe
 };
@@ -120,6 +124,7 @@ int forward_scores_fwd4(float* d_values, int64_t pitch, int B, int T_cap, int S_
                         const uint32_t* lengths, int mode, float mnv, cudaStream_t stream,
                         mas_error_t* err);
 size_t fwd4_smem_bytes(int R, int W, int N, int Kp = 0);
+size_t fwd4_tail_bytes(int R, int W, int M);  // shared memory of the one-launch tail
 struct GaussCfg {
   int gN, gstages, gacc;
 };
