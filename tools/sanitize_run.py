@@ -22,7 +22,13 @@ for eng in ("parallel", "reference"):
     m.align(q, lengths=lens, engine=eng)
     m.align_paths(q, lengths=lens, engine=eng)
     m.align_durations(q, lengths=lens, engine=eng)
-m.align(m.generate_device(2, 64, 256, 3))  # one warp per item
+m.align(m.generate_device(2, 64, 256, 3))  # one warp per item (one-launch tail)
+qs = m.generate_device(3, 120, 300, 4)      # one-launch tail, ragged, every output
+ls = np.array([[120, 300], [7, 40], [100, 100]])
+for eng in ("parallel", "reference"):
+    m.align(qs, lengths=ls, engine=eng)
+    m.align_paths(qs, lengths=ls, engine=eng)
+    m.align_durations(qs, lengths=ls, engine=eng)
 bands = os.environ.get("MAS_SANITIZE_NO_BANDS") != "1"
 if bands:
     qt = m.generate_device(1, 4500, 4600, 2)
