@@ -563,3 +563,53 @@ def test_pipelined_plan_overlapping_batches(mas, oracle, cuda):
             assert torch.equal(outs[k], exp[k]), (rep, k)
             assert torch.equal(paths[k], exp_p[k]), (rep, k)
     plan.finish(qs[2])
+
+
+@pytest.mark.parametrize("engine", ["parallel", "reference"])
+@pytest.mark.parametrize("shape,ragged", [((1, 64, 256), False), ((32, 200, 800), True),
+                                          ((5, 128, 1000), True), ((3, 256, 2100), False)])
+def test_one_launch_tail(mas, oracle, cuda, engine, shape, ragged):
+    """Small batches (every item one single-CTA cluster) run as ONE launch:
+    the forward kernel walks and expands its own items from direction words
+    in shared memory (mas_fwd4.cu OUT 2).  Alignment, paths and durations
+    equal the oracle; a plan of a taller text still launches two kernels."""
+    import torch
+
+    B, T, S = shape
+    rng = np.random.default_rng(B * T + S)
+    lens = None
+    if ragged:
+        t = rng.integers(1, T + 1, B)
+        s = np.maximum(t, rng.integers(1, S + 1, B))
+        t[0], s[0] = T, S
+        lens = np.stack([t, s], 1)
+    q = mas.generate_device(B, T, S, 7)
+    exp = oracle.align(oracle.generate(B, T, S, 7), lengths=lens, engine=engine)[3]
+    plan = mas.Plan(B, T, S, lengths=lens, engine=engine)
+    out = torch.full((B, T, S), 5, dtype=torch.uint8, device=cuda)
+    paths = torch.empty((B, S), dtype=torch.int32, device=cuda)
+    dur = torch.empty((B, T), dtype=torch.int32, device=cuda)
+    plan.enqueue(q, out, paths, durations=dur)
+    plan.finish(q)
+    assert plan.launches == 1
+    got = out.cpu().numpy()
+    np.testing.assert_array_equal(got, exp)
+    pth, du = paths.cpu().numpy(), dur.cpu().numpy()
+    for b in range(B):
+        tb, sb = (T, S) if lens is None else lens[b]
+        np.testing.assert_array_equal(pth[b, :sb], got[b, :, :sb].argmax(0))
+        assert (pth[b, sb:] == -1).all()
+        np.testing.assert_array_equal(du[b], got[b].sum(1))
+    # durations only / paths only
+    plan.enqueue(q, None, None, durations=dur)
+    np.testing.assert_array_equal(dur.cpu().numpy(), got.sum(2))
+    plan.enqueue(q, None, paths)
+    for b in range(B):
+        sb = S if lens is None else lens[b][1]
+        np.testing.assert_array_equal(paths.cpu().numpy()[b, :sb], got[b, :, :sb].argmax(0))
+    plan.close()
+    tall = mas.Plan(1, 600, 900)
+    tall.enqueue(mas.generate_device(1, 600, 900, 1), torch.empty((1, 600, 900), dtype=torch.uint8,
+                                                                  device=cuda))
+    assert tall.launches == 2
+    tall.close()
