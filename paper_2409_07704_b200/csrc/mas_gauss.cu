@@ -95,32 +95,64 @@ __global__ void __launch_bounds__(256) gauss_prep_rows_kernel(
     }
 }
 
+// 64 frames per block: each warp loads its channels' 64 frames as float2
+// per lane (256-byte segments, every load of the thread issued before the
+// first shared store), the block transposes through shared memory (row
+// stride C + 1), and writes its 64 K-major rows as 16-byte vectors of eight
+// bf16 (the 64 x Kp block is contiguous).
+constexpr int kPrepFrames = 64;
+constexpr int kPrepPer = (kGaussMaxChannels + 7) / 8;  // channels per warp, at most
 __global__ void __launch_bounds__(256) gauss_prep_frames_kernel(const float* __restrict__ z, int B,
                                                                  int C, int S, int Sp, int Kp,
                                                                  __nv_bfloat16* __restrict__ Bm) {
-  extern __shared__ float sm[];  // [kPrepRows][C + 1] z
+  extern __shared__ float sm[];  // [kPrepFrames][C + 1] z
   const int ld = C + 1;
-  const int blocks_per_item = Sp / kPrepRows;
-  const int b = blockIdx.x / blocks_per_item, j0 = blockIdx.x % blocks_per_item * kPrepRows;
+  const int blocks_per_item = Sp / kPrepFrames;
+  const int b = blockIdx.x / blocks_per_item, j0 = blockIdx.x % blocks_per_item * kPrepFrames;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int c = wid; c < C; c += 8) {
-    const int j = j0 + lane;
-    sm[lane * ld + c] = j < S ? z[(static_cast<int64_t>(b) * C + c) * S + j] : 0.f;
+  const int j = j0 + 2 * lane;  // this lane's two frames
+  float2 zv[kPrepPer];
+#pragma unroll
+  for (int u = 0; u < kPrepPer; ++u) {
+    const int c = wid + 8 * u;
+    zv[u] = make_float2(0.f, 0.f);
+    if (c < C) {
+      const float* row = z + (static_cast<int64_t>(b) * C + c) * S;
+      if (j + 1 < S && (S & 1) == 0)
+        zv[u] = __ldg(reinterpret_cast<const float2*>(row + j));
+      else
+        zv[u] = make_float2(j < S ? __ldg(row + j) : 0.f, j + 1 < S ? __ldg(row + j + 1) : 0.f);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kPrepPer; ++u) {
+    const int c = wid + 8 * u;
+    if (c < C) {
+      sm[(2 * lane) * ld + c] = zv[u].x;
+      sm[(2 * lane + 1) * ld + c] = zv[u].y;
+    }
   }
   __syncthreads();
-  uint32_t* out = reinterpret_cast<uint32_t*>(Bm + (static_cast<int64_t>(b) * Sp + j0) * Kp);
-  for (int r = wid; r < kPrepRows; r += 8)
-    for (int kw = lane; kw < Kp / 2; kw += 32) {
-      const int k = 2 * kw;
-      float v[2];
+  // row r (frame j0 + r), 16-byte vector v: K indices 8v .. 8v + 7 (z^2 rows
+  // first, then z, zero past 2C)
+  uint4* out = reinterpret_cast<uint4*>(Bm + (static_cast<int64_t>(b) * Sp + j0) * Kp);
+  const int vec_per_row = Kp / 8;
+  for (int e = threadIdx.x; e < kPrepFrames * vec_per_row; e += blockDim.x) {
+    const int r = e / vec_per_row, v = e - r * vec_per_row;
+    uint32_t w[4];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int kk = k + e;
-        const float x = kk < 2 * C ? sm[r * ld + (kk < C ? kk : kk - C)] : 0.f;
-        v[e] = kk < C ? x * x : x;  // z^2 rows first, then z
+    for (int h = 0; h < 4; ++h) {
+      float x[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int kk = 8 * v + 2 * h + q;
+        const float zz = kk < 2 * C ? sm[r * ld + (kk < C ? kk : kk - C)] : 0.f;
+        x[q] = kk < C ? zz * zz : zz;
       }
-      out[r * (Kp / 2) + kw] = pack_bf16x2(v[0], v[1]);
+      w[h] = pack_bf16x2(x[0], x[1]);
     }
+    out[e] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
 }
 
 // ---- K4b: q to HBM -----------------------------------------------------------
@@ -358,7 +390,8 @@ cudaError_t gauss_prep(const float* z, const float* mean, const float* logstd, i
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess || dev >= kMaxDevices) return e != cudaSuccess ? e : cudaErrorInvalidDevice;
   std::call_once(once[dev], [dev] {
-    const int max_bytes = (2 * kGaussMaxChannels + 1) * kPrepRows * 4;
+    const int max_bytes = std::max((2 * kGaussMaxChannels + 1) * kPrepRows,
+                                   (kGaussMaxChannels + 1) * kPrepFrames) * 4;
     cudaError_t r = cudaFuncSetAttribute(gauss_prep_rows_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
     if (r == cudaSuccess)
@@ -370,9 +403,9 @@ cudaError_t gauss_prep(const float* z, const float* mean, const float* logstd, i
   gauss_prep_rows_kernel<<<static_cast<unsigned>(B * (g.Tp / kPrepRows)), 256,
                            static_cast<size_t>(2 * C + 1) * kPrepRows * 4, stream>>>(
       mean, logstd, B, C, T, g.Tp, g.Kp, g.A, g.bias);
-  gauss_prep_frames_kernel<<<static_cast<unsigned>(B * (g.Sp / kPrepRows)), 256,
-                             static_cast<size_t>(C + 1) * kPrepRows * 4, stream>>>(z, B, C, S, g.Sp,
-                                                                                 g.Kp, g.B);
+  gauss_prep_frames_kernel<<<static_cast<unsigned>(B * (g.Sp / kPrepFrames)), 256,
+                             static_cast<size_t>(C + 1) * kPrepFrames * 4, stream>>>(z, B, C, S, g.Sp,
+                                                                                   g.Kp, g.B);
   return cudaGetLastError();
 }
 
