@@ -2,7 +2,7 @@
 // host-side validation with the reference's exact error text, workspace and
 // launch-geometry planning, TMA descriptor encoding, and the host / device
 // entry points.  There is no CPU compute path: every alignment is produced
-// by the kernels in mas_fwd.cu / mas_bt.cu.
+// by the kernels in mas_fwd4.cu / mas_bt.cu.
 #include <cuda.h>
 #include <cuda_runtime.h>
 

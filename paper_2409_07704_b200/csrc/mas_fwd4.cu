@@ -1,31 +1,33 @@
-// mas_fwd4.cu -- K1 with four text rows per lane (128 rows per warp).
+// mas_fwd4.cu -- K1: the forward DP of the maximum-path call, four text rows
+// per lane (128 rows per warp).
 //
-// Same restatement and output as mas_fwd.cu (parallel engine relax_column,
-// src/parallel.cpp:25-31; reference engine forward_reference,
-// src/reference.cpp:9-36; one direction bit per cell,
-// bit(i, c) = Q[i-1][c] > Q[i][c], strict as backtrack.hpp:26), with the
-// work per lane doubled:
+// Restates the parallel engine's relax_column (src/parallel.cpp:25-31) and
+// the reference engine's forward_reference (src/reference.cpp:9-36) with one
+// direction bit per cell, bit(i, c) = Q[i-1][c] > Q[i][c] (strict, as
+// backtrack.hpp:26):
 //   * lane k of warp g owns rows 128 g + 4k .. 128 g + 4k + 3.  Per column
 //     only the first of the four needs the row above from another lane (one
-//     SHFL + one FSEL per four cells instead of per two), and the four rows
-//     are four independent FMNMX/FADD chains, so one warp per SM
-//     sub-partition issues at ~2x the rate of the two-row kernel;
+//     SHFL + one FSEL per four cells), and the four rows are four
+//     independent FMNMX/FADD chains;
 //   * q is staged per warp in 32-column stages by ONE TMA box
 //     {32 columns, 32 lane groups, 4 row residues} of a 3-D view of the
 //     input (rows split by i mod 4), 128-byte swizzle: every LDS.128 of a
 //     residue tile is conflict-free;
 //   * direction bits: FSET (0.0 / 1.0) + FFMA into a float accumulator per
-//     row and 16-column quad (no predicates, see bits4); four rows x one
-//     word per 32-column stage, stored as one 16-byte STG per lane (L2
-//     evict_last);
+//     row and 16-column half-word (no predicates, see bits4); four rows x
+//     one word per 32-column stage, stored as one 16-byte STG per lane (L2
+//     evict_last) -- or into shared memory for the one-launch tail (OUT 2);
 //   * the compute warps wait and probe with warp-uniform votes, so a warp
-//     never enters a quad's shuffles partly diverged;
-//   * boundary row between warps: the same 16-column FIFO hand-offs with
-//     look-ahead mbarrier probes as mas_fwd.cu (st.async / DSMEM across the
-//     CTAs of a cluster);
+//     never enters a stage's shuffles partly diverged;
+//   * boundary row between warps: 32-column FIFO hand-offs (st.async into
+//     the consumer's shared memory, DSMEM across the CTAs of a cluster) with
+//     look-ahead mbarrier probes;
 //   * NonFinite (types.cpp:107-115) folded as max.NaN over |q| (one
 //     3-input FMNMX per two values); the output's zero fill rides along as
-//     TMA stores of a zero tile.
+//     linear bulk stores of a zero tile.
+// Variants: SRC 1 computes q in the CTA from the Gaussian prior on the
+// tensor cores (K1g); OUT 1 writes the score table back (K1s); OUT 2 walks
+// small items in the same launch (K1t).  DESIGN.md 3.
 //
 // (DESIGN.md 3 quotes per-warp clock64 breakdowns and ablations measured with
 // instrumented builds of earlier revisions; the product source carries none.)
@@ -256,7 +258,7 @@ __device__ __forceinline__ bool fwd4_group(const uint8_t* __restrict__ tile, uin
   return true;
 }
 
-// 16 columns with the FIFO hand-off around them (see mas_fwd.cu fwd_quad).
+// One FIFO quad (32 columns) with the hand-off around it.
 // Look-ahead probes of the next stage's load and of the next iteration's
 // FIFO "empty" slot, made inside the first quad's straight-line block so
 // their results are consumed only after it (see fwd4_quad).
