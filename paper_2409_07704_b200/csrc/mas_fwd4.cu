@@ -43,7 +43,7 @@ namespace mas {
 
 namespace {
 
-// R = text rows per lane (4 or 2): a warp owns 32 R rows; a stage is one
+// R = text rows per lane (4): a warp owns 32 R rows; a stage is one
 // [R residues][32 groups][32 cols] fp32 box (R * 4 KiB).
 constexpr int kCols4 = 32;  // columns per TMA box / direction word ("chunk")
 constexpr int kSC = 32;     // columns per stage (32 or 64)

@@ -104,7 +104,7 @@ cudaError_t launch_locate_nonfinite(const float* q, int64_t row_pitch, int T_pad
                                     int s, unsigned long long* d_result, cudaStream_t stream);
 cudaError_t launch_generate(uint64_t s0, int64_t first_elem, int B, int T, int S, int64_t pitch,
                             float* out, cudaStream_t stream);
-// mas_fwd4.cu: R (4 or 2) rows per lane, 32 R rows per warp, 32-column stages.
+// mas_fwd4.cu: R = 4 rows per lane, 32 R rows per warp, 32-column stages.
 // mas_scores.cu: score tables (std::max arithmetic, bit-exact with the
 // reference's forward_parallel) and their direction words in the backtrack
 // kernel's [B][M][T_alloc] layout; used for NaN sentinels (mas_abi.cu).

@@ -1,6 +1,8 @@
-// mas_scores.cu -- score-table export: the parallel
-// engine's forward pass written back in place, as the reference's
-// parallel::forward_parallel does on a MutableLikelihoodView
+// mas_scores.cu -- score-table export: the entry
+// points, and the general kernel for layouts the forward kernel's export
+// (mas_fwd4.cu OUT 1, forward_scores_fwd4 in mas_abi.cu; tried first)
+// cannot map.  The parallel engine's forward pass written back in place, as
+// the reference's parallel::forward_parallel does on a MutableLikelihoodView
 // (include/monoalign/parallel.hpp:17, src/parallel.cpp:95-108):
 //
 //   Q[i][0] = mnv                            i >= 1   (Q[0][0] = q[0][0])
