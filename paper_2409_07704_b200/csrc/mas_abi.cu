@@ -702,9 +702,11 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     const double stream_s = static_cast<double>(nb) * p->T * p->S * 4.125 / 5.9e12;
     const bool chain_bound = stream_s <= 1.1 * chain_s;
     // (each warp zeroes its own rows, so every row is covered only when every
-    // item is full length; the bulk stores need 16-byte rows)
-    const bool fused_zero = d_out && chain_bound &&
-                            p->all_full && (p->S % 16) == 0 &&
+    // item is full length -- or in the one-launch tail, whose producer lanes
+    // also zero the rows of warps past a short item; the bulk stores need
+    // 16-byte rows)
+    const bool tail = tail_ok(p, parts, d_out, d_paths, d_dur);
+    const bool fused_zero = d_out && (tail || (chain_bound && p->all_full)) && (p->S % 16) == 0 &&
                             (reinterpret_cast<uintptr_t>(d_out) & 15u) == 0;
     const size_t item_bytes = static_cast<size_t>(p->T) * p->S;
     if (d_out && !fused_zero) {
@@ -744,7 +746,7 @@ int enqueue_items(mas_plan_t* p, uint32_t parts, int b0, int nb, const float* d_
     // One launch for small batches: every item one single-CTA cluster (K = 1,
     // one band) whose direction words fit shared memory beside the ring; the
     // CTA then walks and expands its own item, and no backtrack kernel runs.
-    if (tail_ok(p, parts, d_out, d_paths, d_dur)) {
+    if (tail) {
       fa.tail = 1;
       fa.path = d_paths;
       fa.dur = d_dur;

@@ -849,8 +849,20 @@ __global__ void __launch_bounds__(SRC ? 12 * 32 : (kMaxWarpsPerCta + 1) * 32, 1)
         }
       }
     }
+    // one-launch tail (one CTA per item): the last warp's zero fill also
+    // covers the item's rows past the CTA's W * 128 (a ragged batch whose
+    // longest text is shorter than text_cap)
+    const int zrows = kTail && w == W - 1 ? a.T_cap : kRows4;
+    if (kTail && w < W && a.zero_fill && !(s_b > 0 && i0w < t_b)) {
+      // one-launch tail, a warp with no rows to compute (past a short item's
+      // text, or an empty item): its rows of the output are zeroed at once
+      LinearZero lz(a, b, i0w, zrows, 1);
+      lz.issue_upto(0, base + SL.zero);
+      bulk_store_complete();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     if (SRC == 0 && w < W && s_b > 0 && i0w < t_b) {
-      LinearZero lz(a, b, i0w, kRows4, nit);
+      LinearZero lz(a, b, i0w, zrows, nit);
       prefetch_tensormap(&tmq);
       // evict_unchanged: evict_first re-read 8 % of q (r12, profiles/r12_l2_policy.md)
       const uint64_t pol_q = policy_evict_unchanged();

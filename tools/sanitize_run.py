@@ -23,6 +23,9 @@ for eng in ("parallel", "reference"):
     m.align_paths(q, lengths=lens, engine=eng)
     m.align_durations(q, lengths=lens, engine=eng)
 m.align(m.generate_device(2, 64, 256, 3))  # one warp per item (one-launch tail)
+# one-launch tail with rows past the CTA's 128 (text_cap 131, longest text 120)
+qg = m.generate_device(2, 131, 300, 5)
+m.align(qg, lengths=np.array([[120, 300], [5, 50]]))
 qs = m.generate_device(3, 120, 300, 4)      # one-launch tail, ragged, every output
 ls = np.array([[120, 300], [7, 40], [100, 100]])
 for eng in ("parallel", "reference"):
